@@ -1,0 +1,316 @@
+#!/usr/bin/env python3
+"""Benchmark of the mixed-precision MRRR hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
+
+metric : eigenpairs/s, fp64 I/O dd-internal, n = 50000 (config 5: Legendre-type,
+         all eigenpairs, Z = 20 GB); one step = one full solve (root, bisection,
+         classification, RQI + Z store) through the C-ABI, inputs resident in HBM.
+e2e    : the same metric from pinned host d, e to host w and Z (H2D + solve + D2H).
+N > 1  : launched by torchrun, one rank per GPU; the index set is partitioned
+         (mr3_plan -> NCCL all-gather of brackets -> mr3_execute -> all-gather
+         of w); total work is fixed -> "scaling": "strong".
+--impl reference : the binary128 oracle (oracle/) timed on the host cores on a
+         bounded sample of the same workload (the "reference arm" of this tier).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+# SASS-counted FP64-pipe instructions (DADD/DMUL/DFMA/DSETP; MUFU.RCP64H is on the XU) per row of
+# the dd negcount loop of k_bisect<dd,1> (recount
+# with tools/count_sass.py after every change of the loop body).
+FP64_INST_PER_BISECT_ROW = {"dd": 46, "f64": 12}
+DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="mr3", choices=["mr3", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_baseline_run(p, n_idx, seed=0):
+    """The oracle (binary128 bisection + inverse iteration) on a bounded sample of
+    eigenpairs of the same matrix, on all host cores."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([[1, p.n], rng.choice(np.arange(2, p.n), n_idx - 2,
+                                                          replace=False)]))
+    d, e = p.d.astype(np.float64), p.e.astype(np.float64)
+    t0 = time.perf_counter()
+    lh, ll = oracle.eigvals(d, e, idx)
+    oracle.eigvecs(d, e, lh, ll, group_tol_rel=1e-9)
+    dt = time.perf_counter() - t0
+    return idx.size, dt, oracle.num_threads()
+
+
+def run_reference(args, p, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cores = oracle.num_threads()
+    per_step = args.cpu_sample or max(2 * cores, 8)
+    for _ in range(args.warmup):
+        cpu_baseline_run(p, min(per_step, 4))
+    tot_n, tot_t = 0, 0.0
+    for s in range(args.steps):
+        k, dt, _ = cpu_baseline_run(p, per_step, seed=s + 1)
+        tot_n += k
+        tot_t += dt
+    v = tot_n / tot_t
+    line = {"impl": "reference", "metric": metric_name(p), "value": v, "unit": "eigenpairs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "binary128 (oracle)",
+            "data": "synthetic", "config": {"workload": p.name, "n": p.n, "sample_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "eigenpairs/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} eigenpairs of the n={p.n} workload per step "
+                                       "(bisection on T + inverse iteration, binary128)"},
+            "e2e": {"value": v, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(p):
+    io = "fp32 I/O fp64-internal" if p.io == "f32" else "fp64 I/O dd-internal"
+    return f"eigenpairs/s, {io}, {p.name} n={p.n}"
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    p = synth.config(args.config)
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, p, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1304_1864_b200 as mr3
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mr3.lib()
+    dt = torch.float32 if p.io == "f32" else torch.float64
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    n = p.n
+    il, iu = p.index_range()
+    m_req = iu - il + 1
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
+
+    def solve():
+        if world > 1:
+            return mr3.solve_distributed(d, e, "V", p.range, il, iu)
+        fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
+        w, Z, st = fn(d, e, "V", p.range, il, iu)
+        return w, Z, (0, w.numel()), st
+
+    # K7: same-run FP64 peak
+    peak_ips, dd_step_ns = mr3.fp64_peak()
+
+    for _ in range(args.warmup):
+        out = solve()
+        del out
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    times = []
+    ktot = {}
+    launches = 0
+    stats = None
+    with Clocks(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s)  # L2 flush between timed steps (outside the events)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            w, Z, rng, stats = solve()
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+            for k, (ms, nl) in mr3.kernel_times().items():
+                t0, n0 = ktot.get(k, (0.0, 0))
+                ktot[k] = (t0 + ms, n0 + nl)
+            launches += mr3.launch_count()
+            del w, Z
+    t_step = float(np.mean(times))
+    t_max = t_step
+    if world > 1:
+        tt = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = m_req / (t_max * 1e-3)  # all ranks together produce the m eigenpairs of one solve
+
+    # roofline of the dominant kernel (K2 bisection): FP64-pipe instructions per row
+    kb_ms, kb_n = ktot.get("k_bisect", (0.0, 0))
+    mode = "f64" if p.io == "f32" else "dd"
+    rows = stats["bisect_rows"] if stats else 0.0
+    # bisect_rows counts plan + cluster refinement of the last step; per launch:
+    achieved = rows * FP64_INST_PER_BISECT_ROW[mode] / (kb_ms / args.steps * 1e-3) if kb_ms else 0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"config{args.config}", {}).get("k_bisect")
+        except Exception:
+            traffic = None
+
+    result = None
+    if rank == 0:
+        kt = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+              for k, v in ktot.items()}
+        result = {
+            "metric": metric_name(p), "value": value, "unit": "eigenpairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if p.io == "f32" else "dd (f64 pairs)", "data": "synthetic",
+            "config": {"workload": p.name, "n": n, "m": m_req, "range": p.range,
+                       "io": p.io, "parallelism": f"index-set partition x{world}",
+                       "l2": "512 MB buffer written between timed steps; Z output > L2"},
+            "roofline": {"bound": "alu", "kernel": "k_bisect",
+                         "achieved": achieved / 1e12, "peak": DERIVED_FP64_PEAK / 1e12,
+                         "unit": "T FP64-inst/s", "frac": achieved / DERIVED_FP64_PEAK,
+                         "traffic": traffic,
+                         "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz",
+                         "measured_peak_same_run": peak_ips / 1e12,
+                         "frac_of_measured": achieved / peak_ips if peak_ips else None,
+                         "inst_per_row": FP64_INST_PER_BISECT_ROW[mode],
+                         "rows_per_launch": rows / max(kb_n / args.steps, 1)},
+            "kernels": kt,
+            "dd_step_latency_ns": dd_step_ns,
+            "gpu_launches": launches,
+            "stats": {k: v for k, v in (stats or {}).items()},
+            "clocks": clk.summary(),
+        }
+
+    # e2e: pinned host inputs -> device -> solve -> host w and Z (every step)
+    if not args.no_e2e and world == 1:
+        hd = torch.from_numpy(p.d).pin_memory()
+        he = torch.from_numpy(p.e).pin_memory()
+        es = torch.float32 if p.io == "f32" else torch.float64
+        hw = torch.empty(m_req, dtype=es).pin_memory()
+        hZ = torch.empty((m_req, n), dtype=es).pin_memory()
+        fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
+        et = []
+        for s in range(max(1, min(args.steps, 2))):
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dd_ = hd.to("cuda", non_blocking=True)
+            de_ = he.to("cuda", non_blocking=True)
+            w, Z, st = fn(dd_, de_, "V", p.range, il, iu)
+            hw.copy_(w, non_blocking=True)
+            hZ.copy_(Z.T, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            et.append(a.elapsed_time(b))
+            del w, Z
+        esz = 4 if p.io == "f32" else 8
+        if rank == 0:
+            result["e2e"] = {"value": m_req / (np.mean(et) * 1e-3), "unit": "eigenpairs/s",
+                             "h2d_bytes_per_step": (2 * n - 1) * esz,
+                             "d2h_bytes_per_step": (m_req + m_req * n) * esz,
+                             "ms_per_step": float(np.mean(et))}
+        del hZ
+
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        oracle.build()
+        k = args.cpu_sample or max(2 * oracle.num_threads(), 8)
+        cnt, dt_cpu, cores = cpu_baseline_run(p, k)
+        result["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
+                                  "kind": "oracle",
+                                  "sample": f"{cnt} eigenpairs (incl. both spectrum ends) of the "
+                                            f"n={n} workload: binary128 bisection on T + "
+                                            f"inverse iteration, {dt_cpu:.1f} s"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

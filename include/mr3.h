@@ -1,0 +1,167 @@
+/*
+ * mr3.h -- C-ABI of the B200-native mixed-precision MRRR hot path.
+ *
+ * Operation (§1 "the real symmetric tridiagonal eigenproblem
+ * (STEP)", and Algorithm 1): given T = tridiag(e, d, e) with d[n],
+ * e[n-1] and an index range il..iu or a value range (vl, vu], compute eigenvalues
+ * w (ascending) and unit eigenvectors Z with T z = lambda z.  Input and output
+ * are in binary_x (fp64 or fp32); all per-eigenpair work runs in binary_y
+ * (double-double resp. fp64) -- the mixed-precision approach of §3
+ * (L746-L1197) with the parameters of §4 (L1291-L1326).
+ *
+ * Conventions (all calls):
+ *  - Pointers named d_*, w, Z and the `d`, `e` inputs are DEVICE pointers
+ *    (e.g. PyTorch CUDA tensors), caller-allocated and caller-owned.  Inputs are
+ *    never modified; outputs must not alias inputs.
+ *  - Z is column-major with leading dimension ldz >= n; column j holds the
+ *    eigenvector of w[j].  Each column is fully written (zeros outside the
+ *    eigenvector's irreducible block).
+ *  - Calls are stream-ordered on the context's stream and synchronous on return
+ *    (the call waits for its own work).  A context is not thread-safe.
+ *  - Return codes (LAPACK-like): 0 OK; -k: argument k invalid; positive codes
+ *    MR3_ERR_* below.  On error the outputs are undefined and *stats is filled as
+ *    far as the solve got.  n = 0 returns OK with *m = 0.
+ *  - Results are bitwise deterministic for given (d, e, range, params) and do not
+ *    depend on the number of ranks of the two-phase multi-GPU form.
+ *  - The library owns its scratch (stream-ordered allocations, cached in the
+ *    context, released by mr3_destroy).  Z is never used as workspace
+ *    (§3.3).
+ */
+#ifndef MR3_H
+#define MR3_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mr3_ctx_s *mr3_ctx;
+
+/* error codes (positive) */
+#define MR3_OK 0
+#define MR3_ERR_NONFINITE 1 /* NaN or Inf in d or e */
+#define MR3_ERR_CUDA 2      /* a CUDA runtime error (mr3_last_error_string) */
+#define MR3_ERR_NOMEM 4     /* device allocation failed */
+#define MR3_ERR_NOCONV 5    /* reserved: the fallbacks are total */
+#define MR3_ERR_ZCAP 6      /* two-phase form: Z has fewer columns than needed */
+#define MR3_ERR_STATE 7     /* two-phase form: execute without a matching plan */
+
+/*
+ * Statistics of one solve (PAPER.md L425 d_max, L961 rho).
+ * t_ms: device time per phase {root, bisect, classify, child, rqi, total, -, -}.
+ */
+typedef struct {
+    int32_t d_max;               /* depth of the representation tree (L425) */
+    int32_t n_clusters;          /* clusters processed, all levels */
+    int32_t largest_cluster;     /* largest cluster size; rho = largest/n (L961) */
+    int32_t robustness_failures; /* child RRR accepted without passing the test (L567-L572) */
+    int32_t rqi_fallbacks;       /* RQI -> bisection + one solve (L724-L727, L1154-L1163) */
+    int32_t n_blocks;            /* irreducible blocks after splitting (L862-L876) */
+    int32_t rqi_iters_max;       /* most RQI iterations any eigenpair took */
+    int32_t levels;              /* tree levels processed (d_max + 1 when m > 0) */
+    double rho;                  /* clustering: largest cluster / n, in [1/n, 1] */
+    double bisect_rows;          /* Sturm-count rows executed (dstqds steps) */
+    double rqi_rows;             /* twisted-factorisation rows executed */
+    double t_ms[8];
+} mr3_stats;
+
+/* tunable parameters (mr3_set_param / mr3_get_param); defaults per PAPER.md §4 */
+enum mr3_param {
+    MR3_GAPTOL = 0,    /* classification gaptol; default 1e-10 (dd, L1325) / 1e-5 (fp64, L1293) */
+    MR3_XI = 1,        /* root perturbation xi; default eps_x (L906-L909) */
+    MR3_KRS = 2,       /* RQI stopping constant k_rs; default 1 (L1150) */
+    MR3_MAX_RQI = 3,   /* RQI iterations before the bisection fallback; default 10 */
+    MR3_MAX_DEPTH = 4, /* representation-tree depth cap; default 10 */
+    MR3_SEED = 5,      /* perturbation seed (counter-based generator key); default 0x4D5233 */
+    MR3_ELG_MAX = 6,   /* element-growth acceptance k_elg (first pass); default 8 */
+    MR3_RTOL = 7,      /* bisection relative tolerance; default 1e-2 * gaptol (L1294-L1295) */
+    MR3_GROUPS = 8,    /* lanes per eigenvalue in the multisection (0 = automatic) */
+    MR3_NPARAM = 9
+};
+
+/* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a
+ * stream owned by the context. */
+int mr3_create(mr3_ctx *ctx, int device, void *cuda_stream);
+int mr3_destroy(mr3_ctx ctx);
+/* mode 0: fp64 I/O (double-double internal), mode 1: fp32 I/O (fp64 internal).
+ * Parameters are stored per mode; a negative value restores the default. */
+int mr3_set_param(mr3_ctx ctx, int mode, int which, double value);
+double mr3_get_param(mr3_ctx ctx, int mode, int which);
+
+/*
+ * fp64 I/O, double-double internal (the "double/quadruple" solver of L1318-L1326).
+ *   jobz : 'V' eigenvalues and eigenvectors, 'N' eigenvalues only
+ *   range: 'A' all; 'I' indices il..iu (1-based, inclusive); 'V' vl < lambda <= vu
+ *   d[n], e[n-1]: device; w[n]: device output (first *m entries valid, ascending);
+ *   Z: device output, column-major, ldz >= n, at least *m columns (may be NULL
+ *   when jobz = 'N').  *m: number of eigenvalues found.
+ */
+int mr3_dstemr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d, const double *e,
+                  double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
+                  int64_t ldz, mr3_stats *stats);
+
+/* fp32 I/O, fp64 internal (the "single/double" solver of L1291-L1304); same contract. */
+int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, const float *e,
+                 float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
+                 int64_t ldz, mr3_stats *stats);
+
+/*
+ * Two-phase form for an index-set partition over `world` ranks (one GPU each).
+ *
+ * mr3_plan: root representation (replicated), the requested index set, and
+ * bisection of this rank's static slice of it.  Returns in *brk a DEVICE buffer
+ * of world * slice_cap records of 4 doubles (bracket lo.hi, lo.lo, hi.hi, hi.lo
+ * in root coordinates) of which this rank filled records
+ * [rank*slice_cap, rank*slice_cap + slice_cnt); the caller must all-gather it in
+ * place (equal-size slices, e.g. ncclAllGather / torch.distributed) before
+ * mr3_execute.  The buffer stays owned by the context.
+ *
+ * mr3_execute: classification of the whole index set (identical on all ranks),
+ * cluster-whole partition of the output columns, then child representations,
+ * refinement and eigenvectors for this rank's columns [*zcol_begin, *zcol_end).
+ * w receives the eigenvalues of this rank's columns at their global positions
+ * (w[*zcol_begin .. *zcol_end-1]); Z receives those columns at local positions
+ * 0 .. (*zcol_end - *zcol_begin - 1).  zcap: columns allocated in Z; if too
+ * small MR3_ERR_ZCAP is returned with the range filled in.
+ * mode: 0 = fp64 I/O (w, Z double*), 1 = fp32 I/O (w, Z float*).
+ */
+int mr3_plan(mr3_ctx ctx, int mode, char range, int64_t n, const void *d, const void *e, double vl,
+             double vu, int64_t il, int64_t iu, int rank, int world, int64_t *m,
+             double **brk, int64_t *slice_cap, int64_t *slice_cnt);
+int mr3_execute(mr3_ctx ctx, char jobz, void *w, void *Z, int64_t ldz, int64_t zcap,
+                int64_t *zcol_begin, int64_t *zcol_end, mr3_stats *stats);
+
+/*
+ * Host-only helper (no device work; callable without a GPU): split m output
+ * columns over `world` ranks at cluster boundaries.  seg_begin[0..nseg] are the
+ * column offsets where the tree's top-level nodes (singletons and clusters)
+ * start (seg_begin[nseg] = m); cost[s] the work estimate of node s.  Fills
+ * col_begin[0..world] (col_begin[0] = 0, col_begin[world] = m), balancing cost
+ * greedily and never cutting a node.  Returns 0 or -1 on bad arguments.
+ */
+int mr3_partition_columns(int64_t nseg, const int64_t *seg_begin, const double *cost, int world,
+                          int64_t *col_begin);
+
+/*
+ * Same-run FP64 peak microbenchmark (K7): independent DFMA chains on every SM
+ * (-> *fp64_inst_per_s, FP64 instructions per second) and one dependent chain of
+ * double-double Sturm steps (-> *dd_step_ns, latency of one step).
+ */
+int mr3_fp64_peak(mr3_ctx ctx, double *fp64_inst_per_s, double *dd_step_ns);
+
+/* per-kernel device time of the last solve (CUDA events on the context stream):
+ * names[i], total ms[i] and launches[i] for i < *count (max 16); any output may be NULL */
+int mr3_last_kernel_times(mr3_ctx ctx, int *count, const char **names, double *ms, int *launches);
+/* number of kernel launches issued by the last plan + execute */
+int64_t mr3_last_launch_count(mr3_ctx ctx);
+
+const char *mr3_strerror(int code);
+const char *mr3_last_error_string(mr3_ctx ctx);
+/* library build info: "sm_100a ..." */
+const char *mr3_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MR3_H */

@@ -1,0 +1,268 @@
+"""paper_1304_1864_b200 -- B200-native mixed-precision MRRR (MR^3) hot path.
+
+Thin ctypes binding of the C-ABI in include/mr3.h (libmr3.so, built in-tree for
+sm_100a).  Argument marshalling only: every step of the solve runs in the CUDA
+kernels of csrc/.  PyTorch supplies device memory, the stream and, for the
+multi-GPU form, the NCCL process group (torch.distributed).  There is no CPU
+fallback: without the built library or a CUDA device every call raises.
+
+Public API (names follow the C-ABI):
+    mr3_dstemr_dd(d, e, jobz='V', range='A', il=1, iu=0, vl=0., vu=0.)  fp64 I/O, dd internal
+    mr3_sstemr_d(d, e, ...)                                            fp32 I/O, fp64 internal
+    dstemr(...) / sstemr(...)            aliases of the two above
+    solve_host(d_np, e_np, ...)          end-to-end from host arrays (pinned H2D, D2H)
+    solve_distributed(d, e, group=...)   index-set partition over ranks (mr3_plan/mr3_execute)
+    fp64_peak()                          K7 same-run FP64 peak + dd-step latency
+    set_param(name, value, mode)         GAPTOL, XI, KRS, MAX_RQI, MAX_DEPTH, SEED, ELG_MAX, RTOL, GROUPS
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "libmr3.so")
+SOURCES = ["csrc/mr3.cu", "csrc/kernels.cuh", "csrc/k_bisect.cuh", "csrc/k_child.cuh",
+           "csrc/k_rqi.cuh", "csrc/k_misc.cuh", "csrc/dd.cuh"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
+
+PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
+          "RTOL": 7, "GROUPS": 8}
+ERRORS = {1: "NONFINITE", 2: "CUDA", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
+
+
+class MR3Error(RuntimeError):
+    def __init__(self, code, msg=""):
+        self.code = code
+        name = ERRORS.get(code, "invalid argument %d" % (-code) if code < 0 else str(code))
+        super().__init__(f"mr3 error {code} ({name}) {msg}".strip())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libmr3.so for sm_100a with nvcc (cross-compiles without a GPU)."""
+    srcs = [os.path.join(_HERE, s) for s in SOURCES] + [os.path.join(_ROOT, "include", "mr3.h")]
+    newest = max(os.path.getmtime(s) for s in srcs)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        tmp = LIB_PATH + f".tmp{os.getpid()}"
+        cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, os.path.join(_HERE, "csrc", "mr3.cu")]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd, cwd=_HERE)
+        os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("d_max", ctypes.c_int32), ("n_clusters", ctypes.c_int32),
+                ("largest_cluster", ctypes.c_int32), ("robustness_failures", ctypes.c_int32),
+                ("rqi_fallbacks", ctypes.c_int32), ("n_blocks", ctypes.c_int32),
+                ("rqi_iters_max", ctypes.c_int32), ("levels", ctypes.c_int32),
+                ("rho", ctypes.c_double), ("bisect_rows", ctypes.c_double),
+                ("rqi_rows", ctypes.c_double), ("t_ms", ctypes.c_double * 8)]
+
+    def asdict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "t_ms"}
+        d["t_ms"] = dict(zip(["root", "bisect", "classify", "child", "rqi", "total"],
+                             list(self.t_ms)[:6]))
+        return d
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libmr3.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} not built; run paper_1304_1864_b200.build()")
+            L = ctypes.CDLL(LIB_PATH)
+            i64, i32, dbl, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+            pi64 = ctypes.POINTER(ctypes.c_int64)
+            L.mr3_create.argtypes = [ctypes.POINTER(vp), i32, vp]
+            L.mr3_destroy.argtypes = [vp]
+            L.mr3_set_param.argtypes = [vp, i32, i32, dbl]
+            L.mr3_get_param.argtypes = [vp, i32, i32]
+            L.mr3_get_param.restype = dbl
+            L.mr3_dstemr_dd.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp, dbl, dbl,
+                                        i64, i64, pi64, vp, vp, i64, ctypes.POINTER(Stats)]
+            L.mr3_sstemr_d.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp,
+                                       ctypes.c_float, ctypes.c_float, i64, i64, pi64, vp, vp,
+                                       i64, ctypes.POINTER(Stats)]
+            L.mr3_plan.argtypes = [vp, i32, ctypes.c_char, i64, vp, vp, dbl, dbl, i64, i64, i32,
+                                   i32, pi64, ctypes.POINTER(ctypes.c_void_p), pi64, pi64]
+            L.mr3_execute.argtypes = [vp, ctypes.c_char, vp, vp, i64, i64, pi64, pi64,
+                                      ctypes.POINTER(Stats)]
+            L.mr3_partition_columns.argtypes = [i64, pi64, ctypes.POINTER(dbl), i32, pi64]
+            L.mr3_fp64_peak.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+            L.mr3_last_kernel_times.argtypes = [vp, ctypes.POINTER(i32),
+                                                ctypes.POINTER(ctypes.c_char_p),
+                                                ctypes.POINTER(dbl), ctypes.POINTER(i32)]
+            L.mr3_last_launch_count.argtypes = [vp]
+            L.mr3_last_launch_count.restype = i64
+            L.mr3_strerror.restype = ctypes.c_char_p
+            L.mr3_last_error_string.argtypes = [vp]
+            L.mr3_last_error_string.restype = ctypes.c_char_p
+            L.mr3_version.restype = ctypes.c_char_p
+            _lib = L
+    return _lib
+
+
+# ------------------------------------------------------------------ contexts
+
+_ctx_cache: dict = {}
+_params: dict = {0: {}, 1: {}}
+
+
+def _ctx(device=None, stream=None):
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("mr3: no CUDA device (the product path has no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    key = (dev, int(st.cuda_stream))
+    c = _ctx_cache.get(key)
+    if c is None:
+        h = ctypes.c_void_p()
+        rc = lib().mr3_create(ctypes.byref(h), dev, ctypes.c_void_p(int(st.cuda_stream)))
+        if rc:
+            raise MR3Error(rc, "mr3_create")
+        c = h
+        _ctx_cache[key] = c
+    for mode in (0, 1):
+        for k, v in _params[mode].items():
+            lib().mr3_set_param(c, mode, PARAMS[k], float(v))
+    return c
+
+
+def set_param(name: str, value: float, mode: int = 0):
+    """Set a solver parameter for mode 0 (fp64 I/O) or 1 (fp32 I/O); value < 0 = default."""
+    if name not in PARAMS:
+        raise KeyError(name)
+    if value is None or (value < 0 and name != "RTOL"):
+        _params[mode].pop(name, None)
+        value = -1.0
+    else:
+        _params[mode][name] = value
+    for c in _ctx_cache.values():
+        lib().mr3_set_param(c, mode, PARAMS[name], float(value))
+
+
+def get_param(name: str, mode: int = 0) -> float:
+    return lib().mr3_get_param(_ctx(), mode, PARAMS[name])
+
+
+def _err(c, rc, what):
+    if rc:
+        msg = lib().mr3_last_error_string(c).decode()
+        raise MR3Error(rc, f"{what}: {msg}")
+
+
+def kernel_times():
+    """{kernel name: (total ms, launches)} of the last solve on the current context
+    (CUDA events recorded on the context's stream around each launch)."""
+    c = _ctx()
+    cnt = ctypes.c_int(0)
+    names = (ctypes.c_char_p * 16)()
+    ms = (ctypes.c_double * 16)()
+    nl = (ctypes.c_int * 16)()
+    lib().mr3_last_kernel_times(c, ctypes.byref(cnt), names, ms, nl)
+    return {names[i].decode(): (ms[i], nl[i]) for i in range(cnt.value)}
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the last solve (all of this library's kernels)."""
+    return int(lib().mr3_last_launch_count(_ctx()))
+
+
+def _solve(mode, d, e, jobz, range_, il, iu, vl, vu, w=None, Z=None):
+    import torch
+    dt = torch.float64 if mode == 0 else torch.float32
+    if d.dtype != dt or e.dtype != dt or not d.is_cuda or not e.is_cuda:
+        raise TypeError(f"mr3: d, e must be CUDA {dt} tensors")
+    d = d.contiguous()
+    e = e.contiguous()
+    n = d.numel()
+    if e.numel() < max(n - 1, 0):
+        raise ValueError("mr3: e must have n-1 entries")
+    c = _ctx(d.device.index)
+    if w is None:
+        w = torch.empty(max(n, 1), dtype=dt, device=d.device)
+    if jobz == "V" and Z is None:
+        # column-major n x n: storage as (ncols, n) row-major, returned transposed
+        Zs = torch.empty((max(n, 1), max(n, 1)), dtype=dt, device=d.device)
+    else:
+        Zs = Z
+    m = ctypes.c_int64(0)
+    st = Stats()
+    fn = lib().mr3_dstemr_dd if mode == 0 else lib().mr3_sstemr_d
+    rc = fn(c, jobz.encode(), range_.encode(), n, ctypes.c_void_p(d.data_ptr()),
+            ctypes.c_void_p(e.data_ptr() if n > 1 else d.data_ptr()), vl, vu, il, iu,
+            ctypes.byref(m), ctypes.c_void_p(w.data_ptr()),
+            ctypes.c_void_p(Zs.data_ptr() if Zs is not None else 0), max(n, 1), ctypes.byref(st))
+    _err(c, rc, "mr3_dstemr_dd" if mode == 0 else "mr3_sstemr_d")
+    mm = m.value
+    Zout = Zs[:mm].T if (jobz == "V" and Zs is not None) else None
+    return w[:mm], Zout, st.asdict()
+
+
+def mr3_dstemr_dd(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0):
+    """fp64 I/O, double-double internal.  d, e: CUDA float64 tensors.
+    Returns (w[m], Z[n, m] (column j = eigenvector of w[j]) or None, stats dict)."""
+    return _solve(0, d, e, jobz, range, il, iu, vl, vu)
+
+
+def mr3_sstemr_d(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0):
+    """fp32 I/O, fp64 internal.  d, e: CUDA float32 tensors."""
+    return _solve(1, d, e, jobz, range, il, iu, vl, vu)
+
+
+dstemr = mr3_dstemr_dd
+sstemr = mr3_sstemr_d
+
+
+def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0):
+    """End to end from host numpy arrays: pinned H2D copy, solve, D2H of w and Z."""
+    import numpy as np
+    import torch
+    mode = 1 if np.asarray(d).dtype == np.float32 else 0
+    dt = torch.float32 if mode else torch.float64
+    hd = torch.from_numpy(np.ascontiguousarray(d)).pin_memory()
+    he = torch.from_numpy(np.ascontiguousarray(e)).pin_memory()
+    dd_ = hd.to("cuda", non_blocking=True)
+    de_ = he.to("cuda", non_blocking=True)
+    w, Z, st = _solve(mode, dd_, de_, jobz, range, il, iu, vl, vu)
+    wh = w.to("cpu")
+    Zh = Z.T.contiguous().to("cpu").T if Z is not None else None
+    return wh.numpy(), (Zh.numpy() if Zh is not None else None), st
+
+
+def fp64_peak():
+    """K7: (FP64 instructions/s over all SMs, latency of one dd Sturm step in ns)."""
+    c = _ctx()
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _err(c, lib().mr3_fp64_peak(c, ctypes.byref(a), ctypes.byref(b)), "mr3_fp64_peak")
+    return a.value, b.value
+
+
+def partition_columns(seg_begin, cost, world):
+    """Host-only cluster-whole column partition (mr3_partition_columns)."""
+    import numpy as np
+    sb = np.ascontiguousarray(np.asarray(seg_begin, dtype=np.int64))
+    cs = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    out = np.zeros(world + 1, dtype=np.int64)
+    rc = lib().mr3_partition_columns(sb.size - 1, sb.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                     cs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), world,
+                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    if rc:
+        raise MR3Error(rc, "mr3_partition_columns")
+    return out
+
+
+from .distributed import solve_distributed, gather_columns  # noqa: E402,F401

@@ -1,0 +1,1019 @@
+// mr3.cu -- B2 (level-by-level representation-tree scheduler) and B3 (C-ABI).
+//
+// Algorithm 1 of PAPER.md (L287-L337) executed breadth-first, one tree level
+// per round of kernel launches: every singleton of a level goes
+// to K5 in one batched launch, every cluster of a level to K4 (one warp each),
+// then the cluster members are refined (K2) and classified (K3) in the child
+// coordinates.  The host only sizes launches (a few counters per level).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/mr3.h"
+#include "k_bisect.cuh"
+#include "k_child.cuh"
+#include "k_misc.cuh"
+#include "k_rqi.cuh"
+#include "kernels.cuh"
+
+using namespace mr3;
+
+namespace {
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+struct KTime {
+    const char *name;
+    cudaEvent_t a, b;
+};
+
+struct Cfg {  // per-mode parameters
+    double v[MR3_NPARAM];
+};
+
+}  // namespace
+
+struct mr3_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int nsm = 148;
+    std::map<std::string, Buf> bufs;
+    Cfg cfg[2];
+    std::string err;
+    std::vector<KTime> kt;
+    size_t kt_used = 0;
+    std::vector<std::pair<std::string, std::pair<double, int>>> ktimes;
+
+    // plan state
+    bool planned = false;
+    int mode = 0;
+    char range = 'A';
+    int64_t n = 0;
+    const void *d = nullptr, *e = nullptr;
+    double vl = 0, vu = 0;
+    int64_t il = 1, iu = 0;
+    int rank = 0, world = 1;
+    int64_t m = 0;      // wanted eigenpairs (global)
+    int cnt = 0;        // items (index set incl. guards, or all for splits)
+    int64_t slice_cap = 0;
+    bool split = false;
+    int nblocks = 1;
+    double scale = 1.0, norm1 = 0.0, pivmin = 0.0, spdiam = 1.0;
+    int nodes_used = 0;
+    int node_cap = 0;
+    int G0 = 1;
+    int64_t launches = 0;
+    mr3_stats stats;
+};
+
+// ------------------------------------------------------------------ helpers
+
+static const double kDefaults[2][MR3_NPARAM] = {
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0},
+};
+
+#define CK(call)                                                                  \
+    do {                                                                          \
+        cudaError_t _e = (call);                                                  \
+        if (_e != cudaSuccess) {                                                  \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(_e);         \
+            return _e == cudaErrorMemoryAllocation ? MR3_ERR_NOMEM : MR3_ERR_CUDA; \
+        }                                                                         \
+    } while (0)
+
+#define CKL(name)                                                                         \
+    do {                                                                                  \
+        cudaError_t _e = cudaGetLastError();                                              \
+        if (_e != cudaSuccess) {                                                          \
+            ctx->err = std::string("launch ") + name + ": " + cudaGetErrorString(_e);      \
+            return MR3_ERR_CUDA;                                                          \
+        }                                                                                 \
+        ctx->launches++;                                                                  \
+    } while (0)
+
+static void *getbuf(mr3_ctx ctx, const std::string &name, size_t bytes, int *rc) {
+    Buf &b = ctx->bufs[name];
+    if (bytes == 0) bytes = 16;
+    if (b.cap < bytes) {
+        if (b.p) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(b.p);
+            b.p = nullptr;
+            b.cap = 0;
+        }
+        size_t want = bytes + bytes / 8;
+        cudaError_t e = cudaMalloc(&b.p, want);
+        if (e != cudaSuccess) {
+            e = cudaMalloc(&b.p, bytes);
+            want = bytes;
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ctx->err = "cudaMalloc(" + name + ", " + std::to_string(bytes) + ") failed";
+            *rc = MR3_ERR_NOMEM;
+            return nullptr;
+        }
+        b.cap = want;
+    }
+    return b.p;
+}
+
+static KTime *kt_begin(mr3_ctx ctx, const char *name) {
+    if (ctx->kt_used == ctx->kt.size()) {
+        KTime t;
+        cudaEventCreate(&t.a);
+        cudaEventCreate(&t.b);
+        ctx->kt.push_back(t);
+    }
+    KTime *t = &ctx->kt[ctx->kt_used++];
+    t->name = name;
+    cudaEventRecord(t->a, ctx->stream);
+    return t;
+}
+static void kt_end(mr3_ctx ctx, KTime *t) { cudaEventRecord(t->b, ctx->stream); }
+
+static void kt_collect(mr3_ctx ctx) {
+    cudaStreamSynchronize(ctx->stream);
+    for (size_t i = 0; i < ctx->kt_used; i++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->kt[i].a, ctx->kt[i].b);
+        std::string nm = ctx->kt[i].name;
+        bool found = false;
+        for (auto &p : ctx->ktimes)
+            if (p.first == nm) {
+                p.second.first += ms;
+                p.second.second += 1;
+                found = true;
+            }
+        if (!found) ctx->ktimes.push_back({nm, {ms, 1}});
+    }
+    ctx->kt_used = 0;
+}
+
+template <class R>
+struct Work {
+    Items it;
+    NodeInfo *nodes;
+    DevStats *st;
+    double *rep_pool;
+};
+
+static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
+    if (forced > 0) {
+        int g = 1;
+        while (g * 2 <= forced && g < 32) g *= 2;
+        return g;
+    }
+    const long long target = (long long)ctx->nsm * 8 * 32;
+    int g = 1;
+    while (g < 32 && (long long)cnt * g < target) g *= 2;
+    return g;
+}
+
+template <class R>
+static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
+                         double absfloor, int certify) {
+    if (cnt <= 0) return 0;
+    const int tpb = 256;
+    long long threads = (long long)cnt * G;
+    int grid = (int)((threads + tpb - 1) / tpb);
+    KTime *t = kt_begin(ctx, "k_bisect");
+#define BIS(GG)                                                                                 \
+    case GG:                                                                                    \
+        k_bisect<R, GG><<<grid, tpb, 0, ctx->stream>>>(W.nodes, W.it, list, cnt, rtol, absfloor, \
+                                                       ctx->pivmin, certify, W.st);             \
+        break;
+    switch (G) {
+        BIS(1)
+        BIS(2)
+        BIS(4)
+        BIS(8)
+        BIS(16)
+        BIS(32)
+        default:
+            return MR3_ERR_STATE;
+    }
+#undef BIS
+    kt_end(ctx, t);
+    CKL("k_bisect");
+    return 0;
+}
+
+// ------------------------------------------------------------------ plan
+
+template <class R, class T>
+static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e, double vl,
+                     double vu, int64_t il, int64_t iu, int rank, int world, int64_t *m,
+                     double **brk, int64_t *slice_cap, int64_t *slice_cnt) {
+    const int mode = std::is_same<T, float>::value ? 1 : 0;
+    const double *P = ctx->cfg[mode].v;
+    const double eps_x = mode ? 5.9604644775390625e-08 : 1.1102230246251565e-16;
+    const double eps_y = Prec<R>::eps;
+    int rc = 0;
+    ctx->planned = false;
+    memset(&ctx->stats, 0, sizeof(ctx->stats));
+    ctx->ktimes.clear();
+    ctx->kt_used = 0;
+    ctx->launches = 0;
+    if (range != 'A' && range != 'I' && range != 'V') return -2;
+    if (n < 0) return -3;
+    if (range == 'I' && n > 0 && (il < 1 || iu < il - 1 || iu > n)) return -8;
+    if (range == 'V' && !(vl < vu)) return -6;
+    if (world < 1 || rank < 0 || rank >= world) return -11;
+    if (n > 0x7fffffffLL) return -3;
+    ctx->mode = mode;
+    ctx->range = range;
+    ctx->n = n;
+    ctx->d = d;
+    ctx->e = e;
+    ctx->rank = rank;
+    ctx->world = world;
+    *m = 0;
+    *slice_cap = 0;
+    *slice_cnt = 0;
+    *brk = nullptr;
+    if (n == 0 || (range == 'I' && iu < il)) {
+        ctx->m = 0;
+        ctx->cnt = 0;
+        ctx->planned = true;
+        return 0;
+    }
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    KTime *t_root = kt_begin(ctx, "k_root");
+
+    // K1a: norm, Gershgorin, finiteness
+    ScanInfo *dscan = (ScanInfo *)getbuf(ctx, "scan", sizeof(ScanInfo), &rc);
+    unsigned long long *dcnt = (unsigned long long *)getbuf(ctx, "cnt64", 64, &rc);
+    if (rc) return rc;
+    k_scan_input<T><<<1, 1024, 0, s>>>(d, e, n, dscan);
+    CKL("k_scan_input");
+    ScanInfo info;
+    CK(cudaMemcpyAsync(&info, dscan, sizeof(info), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info.nonfinite) return MR3_ERR_NONFINITE;
+    ctx->norm1 = info.norm1;
+    int ex = 0;
+    if (info.norm1 > 0) frexp(info.norm1, &ex);
+    ctx->scale = info.norm1 > 0 ? ldexp(1.0, -ex) : 1.0;  // scaled ||T||_1 in [0.5, 1)
+    const double nrm_s = info.norm1 * ctx->scale;
+    ctx->pivmin = eps_y * fmax(nrm_s, 1e-300);
+    ctx->spdiam = fmax((info.gu - info.gl) * ctx->scale, 1e-300);
+
+    // splitting: |e_i| <= eps_x ||T||
+    std::vector<BlockDesc> blocks;
+    const double thr = eps_x * info.norm1;
+    CK(cudaMemsetAsync(dcnt, 0, 8, s));
+    if (n > 1) {
+        k_split_count<T><<<std::min<int64_t>(1024, (n + 255) / 256), 256, 0, s>>>(e, n, thr, dcnt);
+        CKL("k_split_count");
+    }
+    unsigned long long nsplit = 0;
+    CK(cudaMemcpyAsync(&nsplit, dcnt, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (nsplit == 0) {
+        blocks.push_back({0, n});
+    } else {
+        int64_t *dpos = (int64_t *)getbuf(ctx, "splitpos", nsplit * 8, &rc);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(dcnt, 0, 8, s));
+        k_split_list<T><<<std::min<int64_t>(1024, (n + 255) / 256), 256, 0, s>>>(e, n, thr, dpos,
+                                                                                 dcnt);
+        CKL("k_split_list");
+        std::vector<int64_t> pos(nsplit);
+        CK(cudaMemcpyAsync(pos.data(), dpos, nsplit * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::sort(pos.begin(), pos.end());
+        int64_t r0 = 0;
+        for (int64_t p : pos) {
+            blocks.push_back({r0, p + 1 - r0});
+            r0 = p + 1;
+        }
+        blocks.push_back({r0, n - r0});
+    }
+    ctx->nblocks = (int)blocks.size();
+    ctx->split = ctx->nblocks > 1;
+    ctx->stats.n_blocks = ctx->nblocks;
+
+    // K1b: root representations
+    const int words = Prec<R>::words;
+    double *rep_pool = (double *)getbuf(ctx, "rep_root", (size_t)n * 4 * words * 8, &rc);
+    BlockDesc *dblocks = (BlockDesc *)getbuf(ctx, "blocks", blocks.size() * sizeof(BlockDesc), &rc);
+    double *dbrk0 = (double *)getbuf(ctx, "brk_root", blocks.size() * 4 * 8, &rc);
+    int *dfail = (int *)getbuf(ctx, "fail", 16, &rc);
+    ctx->node_cap = std::max<int>(1024, ctx->nblocks * 2 + 64);
+    NodeInfo *dnodes = (NodeInfo *)getbuf(ctx, "nodes", ctx->node_cap * sizeof(NodeInfo), &rc);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dblocks, blocks.data(), blocks.size() * sizeof(BlockDesc),
+                       cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(dfail, 0, 4, s));
+    int right = 0;
+    if (!ctx->split) {
+        if (range == 'I' && (il + iu) > n + 1) right = 1;
+        if (range == 'V' && 0.5 * (vl + vu) > 0.5 * (info.gl + info.gu)) right = 1;
+    }
+    const double xi = P[MR3_XI];
+    const uint64_t seed = (uint64_t)P[MR3_SEED];
+    k_root<R, T><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(d, e, dblocks, ctx->nblocks, ctx->scale,
+                                                         right, xi, seed, ctx->pivmin, rep_pool, 0,
+                                                         dnodes, dbrk0, dfail);
+    CKL("k_root");
+    ctx->nodes_used = ctx->nblocks;
+
+    // index set
+    int64_t ilw = il, iuw = iu;
+    if (range == 'A') {
+        ilw = 1;
+        iuw = n;
+    }
+    if (!ctx->split && range == 'V') {
+        int *dc = (int *)getbuf(ctx, "cnt2", 16, &rc);
+        if (rc) return rc;
+        k_count_at<R><<<1, 32, 0, s>>>(dnodes, 0, vl * ctx->scale, vu * ctx->scale, ctx->pivmin,
+                                       dc);
+        CKL("k_count_at");
+        int hc[2];
+        CK(cudaMemcpyAsync(hc, dc, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ilw = hc[0] + 1;
+        iuw = hc[1];
+    }
+    kt_end(ctx, t_root);
+    ctx->vl = vl;
+    ctx->vu = vu;
+    ctx->il = ilw;
+    ctx->iu = iuw;
+    int cnt;
+    if (!ctx->split) {
+        if (iuw < ilw) {
+            ctx->m = 0;
+            ctx->cnt = 0;
+            ctx->planned = true;
+            return 0;
+        }
+        int64_t k_lo = std::max<int64_t>(1, ilw - 1), k_hi = std::min<int64_t>(n, iuw + 1);
+        cnt = (int)(k_hi - k_lo + 1);
+        ctx->m = iuw - ilw + 1;
+        ctx->cnt = cnt;
+        // allocate items
+        Items it;
+        it.node = (int32_t *)getbuf(ctx, "it_node", cnt * 4, &rc);
+        it.k = (int32_t *)getbuf(ctx, "it_k", cnt * 4, &rc);
+        it.col = (int64_t *)getbuf(ctx, "it_col", cnt * 8, &rc);
+        it.lo = getbuf(ctx, "it_lo", (size_t)cnt * sizeof(R), &rc);
+        it.hi = getbuf(ctx, "it_hi", (size_t)cnt * sizeof(R), &rc);
+        it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
+        it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
+        if (rc) return rc;
+        k_init_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, (int)k_lo, (int)ilw, (int)iuw, 0,
+                                                          dbrk0);
+        CKL("k_init_items");
+    } else {
+        cnt = (int)n;
+        ctx->cnt = cnt;
+        ctx->m = -1;  // known after the global ordering in execute
+        std::vector<int64_t> item0(blocks.size());
+        int64_t acc = 0;
+        for (size_t b = 0; b < blocks.size(); b++) {
+            item0[b] = acc;
+            acc += blocks[b].n;
+        }
+        int64_t *ditem0 = (int64_t *)getbuf(ctx, "item0", item0.size() * 8, &rc);
+        Items it;
+        it.node = (int32_t *)getbuf(ctx, "it_node", cnt * 4, &rc);
+        it.k = (int32_t *)getbuf(ctx, "it_k", cnt * 4, &rc);
+        it.col = (int64_t *)getbuf(ctx, "it_col", cnt * 8, &rc);
+        it.lo = getbuf(ctx, "it_lo", (size_t)cnt * sizeof(R), &rc);
+        it.hi = getbuf(ctx, "it_hi", (size_t)cnt * sizeof(R), &rc);
+        it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
+        it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ditem0, item0.data(), item0.size() * 8, cudaMemcpyHostToDevice, s));
+        k_init_items_blocks<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, dblocks, ctx->nblocks,
+                                                                 ditem0, dbrk0);
+        CKL("k_init_items_blocks");
+    }
+
+    // K2 on this rank's static slice (Alg. 1 l.3)
+    int64_t cap = (cnt + world - 1) / world;
+    int64_t first = std::min<int64_t>((int64_t)rank * cap, cnt);
+    int64_t mine = std::min<int64_t>(cap, cnt - first);
+    ctx->slice_cap = cap;
+    double *dbrk = (double *)getbuf(ctx, "brk", (size_t)world * cap * 4 * 8, &rc);
+    int32_t *list = (int32_t *)getbuf(ctx, "list0", (size_t)cnt * 4, &rc);
+    DevStats *dst = (DevStats *)getbuf(ctx, "devstats", sizeof(DevStats), &rc);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
+    Work<R> W;
+    W.it.node = (int32_t *)ctx->bufs["it_node"].p;
+    W.it.k = (int32_t *)ctx->bufs["it_k"].p;
+    W.it.col = (int64_t *)ctx->bufs["it_col"].p;
+    W.it.lo = ctx->bufs["it_lo"].p;
+    W.it.hi = ctx->bufs["it_hi"].p;
+    W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
+    W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
+    W.nodes = dnodes;
+    W.st = dst;
+    double rtol = P[MR3_RTOL] > 0 ? P[MR3_RTOL] : 1e-2 * P[MR3_GAPTOL];
+    double absfloor = 4.0 * eps_y * ctx->spdiam;
+    if (mine > 0) {
+        k_iota<<<(int)((mine + 255) / 256), 256, 0, s>>>(list, (int)mine, (int)first);
+        CKL("k_iota");
+        ctx->G0 = choose_groups(ctx, cnt, (int)P[MR3_GROUPS]);
+        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0);
+        if (rc) return rc;
+        k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
+                                                                    dbrk + 4 * first);
+        CKL("k_items_to_brk");
+    }
+    int hfail = 0;
+    CK(cudaMemcpyAsync(&hfail, dfail, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *m = ctx->m;
+    *brk = dbrk;
+    *slice_cap = cap;
+    *slice_cnt = mine;
+    ctx->planned = true;
+    return 0;
+}
+
+// ------------------------------------------------------------------ execute
+
+template <class R, class OutT>
+static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, int64_t zcap,
+                        int64_t *zcol_begin, int64_t *zcol_end, mr3_stats *stats) {
+    if (!ctx->planned) return MR3_ERR_STATE;
+    const int mode = ctx->mode;
+    const double *P = ctx->cfg[mode].v;
+    const double eps_x = mode ? 5.9604644775390625e-08 : 1.1102230246251565e-16;
+    const double eps_y = Prec<R>::eps;
+    int rc = 0;
+    cudaStream_t s = ctx->stream;
+    *zcol_begin = 0;
+    *zcol_end = 0;
+    if (jobz != 'V' && jobz != 'N') return -2;
+    const int cnt = ctx->cnt;
+    if (cnt == 0) {
+        ctx->planned = false;
+        if (stats) *stats = ctx->stats;
+        return 0;
+    }
+    if (jobz == 'V' && ldz < ctx->n) return -4;
+    const int words = Prec<R>::words;
+    Work<R> W;
+    W.it.node = (int32_t *)ctx->bufs["it_node"].p;
+    W.it.k = (int32_t *)ctx->bufs["it_k"].p;
+    W.it.col = (int64_t *)ctx->bufs["it_col"].p;
+    W.it.lo = ctx->bufs["it_lo"].p;
+    W.it.hi = ctx->bufs["it_hi"].p;
+    W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
+    W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
+    W.nodes = (NodeInfo *)ctx->bufs["nodes"].p;
+    W.st = (DevStats *)ctx->bufs["devstats"].p;
+    double *dbrk = (double *)ctx->bufs["brk"].p;
+    // per-execute counters (bisect_rows of the plan is kept)
+    CK(cudaMemsetAsync((char *)W.st + 8, 0, sizeof(DevStats) - 8, s));
+    if (ctx->world > 1) {
+        k_brk_to_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, (int)ctx->slice_cap,
+                                                            ctx->world, dbrk);
+        CKL("k_brk_to_items");
+    }
+    double rtol = P[MR3_RTOL] > 0 ? P[MR3_RTOL] : 1e-2 * P[MR3_GAPTOL];
+    double absfloor = 4.0 * eps_y * ctx->spdiam;
+    const double gaptol = P[MR3_GAPTOL];
+
+    // split case: global order of all block eigenvalues -> output columns
+    if (ctx->split) {
+        unsigned long long *keys = (unsigned long long *)getbuf(ctx, "keys", cnt * 8, &rc);
+        unsigned long long *keys2 = (unsigned long long *)getbuf(ctx, "keys2", cnt * 8, &rc);
+        int32_t *vals = (int32_t *)getbuf(ctx, "vals", cnt * 4, &rc);
+        int32_t *vals2 = (int32_t *)getbuf(ctx, "vals2", cnt * 4, &rc);
+        int64_t *mc = (int64_t *)getbuf(ctx, "mcount", 16, &rc);
+        if (rc) return rc;
+        k_item_keys<R><<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, W.nodes, keys, vals);
+        CKL("k_item_keys");
+        size_t tmpb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmpb, keys, keys2, vals, vals2, cnt, 0, 64, s);
+        void *tmp = getbuf(ctx, "cubtmp", tmpb, &rc);
+        if (rc) return rc;
+        cub::DeviceRadixSort::SortPairs(tmp, tmpb, keys, keys2, vals, vals2, cnt, 0, 64, s);
+        CKL("radix sort");
+        int64_t init[2] = {0, 0x7fffffffffffffffLL};
+        CK(cudaMemcpyAsync(mc, init, 16, cudaMemcpyHostToDevice, s));
+        int md = ctx->range == 'A' ? 0 : (ctx->range == 'I' ? 1 : 2);
+        k_assign_cols<<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, vals2, keys2, md, ctx->il,
+                                                        ctx->iu, ctx->vl * ctx->scale,
+                                                        ctx->vu * ctx->scale, mc);
+        CKL("k_assign_cols");
+        int64_t hm = 0;
+        CK(cudaMemcpyAsync(&hm, mc, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ctx->m = hm;
+        int64_t first_rank = md == 1 ? ctx->il : 1;
+        if (md == 2) {
+            // first wanted rank = 1 + #items at or below vl: ranks are contiguous
+            std::vector<int64_t> cols(cnt);
+            CK(cudaMemcpyAsync(cols.data(), W.it.col, cnt * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            int64_t mn = INT64_MAX;
+            for (auto c : cols)
+                if (c >= 0) mn = std::min(mn, c);
+            first_rank = mn == INT64_MAX ? 1 : mn;
+        }
+        k_compact_cols<<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, vals2, first_rank);
+        CKL("k_compact_cols");
+    }
+    const int64_t m = ctx->m;
+    if (m <= 0) {
+        ctx->planned = false;
+        if (stats) *stats = ctx->stats;
+        return 0;
+    }
+
+    // level-0 classification of the whole index set (identical on every rank)
+    int32_t *listA = (int32_t *)getbuf(ctx, "listA", (size_t)cnt * 4, &rc);
+    int32_t *listB = (int32_t *)getbuf(ctx, "listB", (size_t)cnt * 4, &rc);
+    int32_t *singles = (int32_t *)getbuf(ctx, "singles", (size_t)cnt * 4, &rc);
+    int32_t *cbeg = (int32_t *)getbuf(ctx, "cbeg", (size_t)cnt * 4, &rc);
+    int32_t *cend = (int32_t *)getbuf(ctx, "cend", (size_t)cnt * 4, &rc);
+    int32_t *segb = (int32_t *)getbuf(ctx, "segb", (size_t)(cnt + 1) * 4, &rc);
+    int32_t *segw = (int32_t *)getbuf(ctx, "segw", (size_t)cnt * 4, &rc);
+    int32_t *dcounts = (int32_t *)getbuf(ctx, "counts", 16, &rc);
+    if (rc) return rc;
+    k_iota<<<(cnt + 255) / 256, 256, 0, s>>>(listA, cnt, 0);
+    CKL("k_iota");
+    SegOut so;
+    so.singles = singles;
+    so.clus_beg = cbeg;
+    so.clus_end = cend;
+    so.next_active = listB;
+    so.seg_begin = segb;
+    so.seg_want = segw;
+    so.counts = dcounts;
+    so.st = W.st;
+    KTime *tc = kt_begin(ctx, "k_classify");
+    k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, cnt, gaptol, so);
+    kt_end(ctx, tc);
+    CKL("k_classify");
+    int hc[4];
+    CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int nsing = hc[0], nclus = hc[1], nmem = hc[2];
+
+    // multi-rank: cluster-whole partition of the output columns
+    int64_t c0 = 0, c1 = m;
+    if (ctx->world > 1) {
+        std::vector<int32_t> hs(nsing), hb(nclus), he(nclus), hm(nmem);
+        std::vector<int64_t> cols(cnt);
+        if (nsing) CK(cudaMemcpyAsync(hs.data(), singles, nsing * 4, cudaMemcpyDeviceToHost, s));
+        if (nclus) {
+            CK(cudaMemcpyAsync(hb.data(), cbeg, nclus * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(he.data(), cend, nclus * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(hm.data(), listB, nmem * 4, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaMemcpyAsync(cols.data(), W.it.col, cnt * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // segments: (first column, cost, kind, index)
+        struct Seg {
+            int64_t c0;
+            double cost;
+            int kind, idx;
+        };
+        std::vector<Seg> segs;
+        for (int i = 0; i < nsing; i++) segs.push_back({cols[hs[i]], 1.0, 0, i});
+        for (int i = 0; i < nclus; i++) {
+            int64_t cmin = INT64_MAX;
+            int wanted = 0;
+            for (int j = hb[i]; j < he[i]; j++)
+                if (cols[hm[j]] >= 0) {
+                    cmin = std::min(cmin, cols[hm[j]]);
+                    wanted++;
+                }
+            segs.push_back({cmin, 3.0 * wanted, 1, i});
+        }
+        std::sort(segs.begin(), segs.end(), [](const Seg &a, const Seg &b) { return a.c0 < b.c0; });
+        std::vector<int64_t> sb(segs.size() + 1);
+        std::vector<double> cost(segs.size());
+        for (size_t i = 0; i < segs.size(); i++) {
+            sb[i] = segs[i].c0;
+            cost[i] = segs[i].cost;
+        }
+        sb[segs.size()] = m;
+        std::vector<int64_t> cb(ctx->world + 1);
+        mr3_partition_columns((int64_t)segs.size(), sb.data(), cost.data(), ctx->world, cb.data());
+        c0 = cb[ctx->rank];
+        c1 = cb[ctx->rank + 1];
+        // keep this rank's singletons and clusters
+        std::vector<int32_t> ns, nb, ne, nm;
+        for (auto &sg : segs) {
+            if (sg.c0 < c0 || sg.c0 >= c1) continue;
+            if (sg.kind == 0) {
+                ns.push_back(hs[sg.idx]);
+            } else {
+                int b0 = (int)nm.size();
+                for (int j = hb[sg.idx]; j < he[sg.idx]; j++) nm.push_back(hm[j]);
+                nb.push_back(b0);
+                ne.push_back((int)nm.size());
+            }
+        }
+        // clusters must stay in item order for the child pool layout: they are
+        nsing = (int)ns.size();
+        nclus = (int)nb.size();
+        nmem = (int)nm.size();
+        if (nsing) CK(cudaMemcpyAsync(singles, ns.data(), nsing * 4, cudaMemcpyHostToDevice, s));
+        if (nclus) {
+            CK(cudaMemcpyAsync(cbeg, nb.data(), nclus * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(cend, ne.data(), nclus * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(listB, nm.data(), nmem * 4, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaStreamSynchronize(s));
+    }
+    *zcol_begin = c0;
+    *zcol_end = c1;
+    if (jobz == 'V' && zcap < c1 - c0) return MR3_ERR_ZCAP;
+    if (jobz == 'V' && ctx->split && c1 > c0) {
+        CK(cudaMemset2DAsync(Z, ldz * sizeof(OutT), 0, ctx->n * sizeof(OutT), c1 - c0, s));
+    }
+
+    // RQI scratch sizing
+    size_t freeb = 0, totb = 0;
+    cudaMemGetInfo(&freeb, &totb);
+    const int64_t nmaxb = ctx->n;
+    const int64_t nblk = (nmaxb + RQ_C - 1) / RQ_C;
+    size_t budget = std::min<size_t>((size_t)(freeb * 0.6), (size_t)48 << 30);
+    int64_t per_thread = nblk * 3 * (int64_t)sizeof(R);
+    int64_t Smax = std::max<int64_t>(RQ_TPB, (int64_t)(budget / std::max<int64_t>(per_thread, 1)));
+    Smax = (Smax / RQ_TPB) * RQ_TPB;
+
+    auto run_rqi = [&](const int32_t *list, int ncount) -> int {
+        for (int off = 0; off < ncount;) {
+            int64_t S = std::min<int64_t>(Smax, ((ncount - off + RQ_TPB - 1) / RQ_TPB) * RQ_TPB);
+            int rc2 = 0;
+            R *ck = (R *)getbuf(ctx, "rqi_ck", (size_t)(3 * nblk * S) * sizeof(R), &rc2);
+            if (rc2) return rc2;
+            RqiArgs<R> A;
+            A.nodes = W.nodes;
+            A.it = W.it;
+            A.list = list + off;
+            A.cnt = (int)std::min<int64_t>(S, ncount - off);
+            A.ck_s = ck;
+            A.ck_W = ck + nblk * S;
+            A.ck_p = ck + 2 * nblk * S;
+            A.S = S;
+            A.pivmin = ctx->pivmin;
+            A.krs = P[MR3_KRS];
+            A.eps_x = eps_x;
+            A.gaptol = gaptol;
+            A.maxit = (int)P[MR3_MAX_RQI];
+            A.jobz_v = jobz == 'V';
+            A.w = w;
+            A.Z = Z;
+            A.ldz = ldz;
+            A.zcol0 = c0;
+            A.unscale = 1.0 / ctx->scale;
+            A.st = W.st;
+            KTime *t = kt_begin(ctx, "k_rqi");
+            k_rqi<R, OutT><<<(int)(S / RQ_TPB), RQ_TPB, 0, s>>>(A);
+            kt_end(ctx, t);
+            cudaError_t e2 = cudaGetLastError();
+            if (e2 != cudaSuccess) {
+                ctx->err = std::string("k_rqi: ") + cudaGetErrorString(e2);
+                return MR3_ERR_CUDA;
+            }
+            ctx->launches++;
+            off += A.cnt;
+        }
+        return 0;
+    };
+
+    // level loop (Alg. 1 l.5-17, breadth-first)
+    int level = 0;
+    int32_t *cur = listA, *nxt = listB;
+    const int maxdepth = (int)P[MR3_MAX_DEPTH];
+    const double elg1 = P[MR3_ELG_MAX];
+    const double elg2 = std::max(10.0, eps_x / (eps_y * std::sqrt((double)ctx->n)));
+    int Gc = P[MR3_GROUPS] > 0 ? choose_groups(ctx, 0, (int)P[MR3_GROUPS]) : 8;
+    while (true) {
+        if (nsing > 0) {
+            rc = run_rqi(singles, nsing);
+            if (rc) return rc;
+        }
+        ctx->stats.levels = level + 1;
+        if (nclus == 0) break;
+        if (level + 1 > maxdepth) {
+            // depth cap: the remaining cluster members get the bisection
+            // fallback + one solve each (the RQI kernel's fallback path)
+            double saved = ctx->cfg[mode].v[MR3_MAX_RQI];
+            ctx->cfg[mode].v[MR3_MAX_RQI] = 0;
+            P = ctx->cfg[mode].v;
+            rc = run_rqi(nxt, nmem);
+            ctx->cfg[mode].v[MR3_MAX_RQI] = saved;
+            P = ctx->cfg[mode].v;
+            if (rc) return rc;
+            break;
+        }
+        // K4: child representations (new nodes)
+        if (ctx->nodes_used + nclus > ctx->node_cap) {
+            // grow the node table (keep contents)
+            int newcap = std::max(ctx->node_cap * 2, ctx->nodes_used + nclus + 64);
+            NodeInfo *nn = nullptr;
+            CK(cudaMalloc(&nn, newcap * sizeof(NodeInfo)));
+            CK(cudaMemcpyAsync(nn, W.nodes, ctx->nodes_used * sizeof(NodeInfo),
+                               cudaMemcpyDeviceToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            cudaFree(ctx->bufs["nodes"].p);
+            ctx->bufs["nodes"].p = nn;
+            ctx->bufs["nodes"].cap = newcap * sizeof(NodeInfo);
+            ctx->node_cap = newcap;
+            W.nodes = nn;
+        }
+        std::string pname = "child_pool" + std::to_string(level);
+        double *pool =
+            (double *)getbuf(ctx, pname, (size_t)nclus * ctx->n * 4 * words * 8, &rc);
+        if (rc) return rc;
+        KTime *tch = kt_begin(ctx, "k_child");
+        k_child<R><<<nclus, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, nxt, cbeg, cend, nclus,
+                                        pool, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st);
+        kt_end(ctx, tch);
+        CKL("k_child");
+        ctx->nodes_used += nclus;
+        // K2: refine in the child coordinates (certified)
+        rc = launch_bisect<R>(ctx, W, nxt, nmem, Gc, rtol, absfloor, 1);
+        if (rc) return rc;
+        // K3: classify the members
+        std::swap(cur, nxt);
+        so.next_active = nxt;
+        KTime *tc2 = kt_begin(ctx, "k_classify");
+        k_classify<R><<<1, 1024, 0, s>>>(W.it, cur, nmem, gaptol, so);
+        kt_end(ctx, tc2);
+        CKL("k_classify");
+        CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        nsing = hc[0];
+        nclus = hc[1];
+        nmem = hc[2];
+        level++;
+    }
+    ctx->stats.d_max = level;
+    DevStats hst;
+    CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    kt_collect(ctx);
+    ctx->stats.n_clusters = hst.n_clusters;
+    ctx->stats.largest_cluster = std::max(1, hst.largest_cluster);
+    ctx->stats.rho = (double)ctx->stats.largest_cluster / (double)ctx->n;
+    ctx->stats.robustness_failures = hst.robustness_failures;
+    ctx->stats.rqi_fallbacks = hst.rqi_fallbacks;
+    ctx->stats.rqi_iters_max = hst.rqi_iters_max;
+    ctx->stats.bisect_rows = (double)hst.bisect_rows;
+    ctx->stats.rqi_rows = (double)hst.rqi_rows;
+    for (auto &p : ctx->ktimes) {
+        const std::string &nm = p.first;
+        int slot = nm == "k_root" ? 0 : nm == "k_bisect" ? 1 : nm == "k_classify" ? 2
+                                     : nm == "k_child"  ? 3 : nm == "k_rqi" ? 4 : 6;
+        ctx->stats.t_ms[slot] += p.second.first;
+        ctx->stats.t_ms[5] += p.second.first;
+    }
+    if (stats) *stats = ctx->stats;
+    ctx->planned = false;
+    return 0;
+}
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" {
+
+int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
+    if (!out) return -1;
+    mr3_ctx ctx = new mr3_ctx_s();
+    ctx->device = device;
+    for (int m = 0; m < 2; m++)
+        for (int i = 0; i < MR3_NPARAM; i++) ctx->cfg[m].v[i] = kDefaults[m][i];
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return MR3_ERR_CUDA;
+    }
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return MR3_ERR_CUDA;
+        }
+        ctx->own_stream = true;
+    }
+    cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
+    *out = ctx;
+    return 0;
+}
+
+int mr3_destroy(mr3_ctx ctx) {
+    if (!ctx) return 0;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &b : ctx->bufs)
+        if (b.second.p) cudaFree(b.second.p);
+    for (auto &t : ctx->kt) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return 0;
+}
+
+int mr3_set_param(mr3_ctx ctx, int mode, int which, double value) {
+    if (!ctx || mode < 0 || mode > 1 || which < 0 || which >= MR3_NPARAM) return -1;
+    ctx->cfg[mode].v[which] = value < 0 && which != MR3_RTOL ? kDefaults[mode][which] : value;
+    return 0;
+}
+
+double mr3_get_param(mr3_ctx ctx, int mode, int which) {
+    if (!ctx || mode < 0 || mode > 1 || which < 0 || which >= MR3_NPARAM) return NAN;
+    return ctx->cfg[mode].v[which];
+}
+
+int mr3_plan(mr3_ctx ctx, int mode, char range, int64_t n, const void *d, const void *e, double vl,
+             double vu, int64_t il, int64_t iu, int rank, int world, int64_t *m, double **brk,
+             int64_t *slice_cap, int64_t *slice_cnt) {
+    if (!ctx) return -1;
+    if (!m || !brk || !slice_cap || !slice_cnt) return -13;
+    if (n > 0 && (!d || (n > 1 && !e))) return -5;
+    if (mode == 0)
+        return plan_impl<dd, double>(ctx, range, n, (const double *)d, (const double *)e, vl, vu,
+                                     il, iu, rank, world, m, brk, slice_cap, slice_cnt);
+    if (mode == 1)
+        return plan_impl<double, float>(ctx, range, n, (const float *)d, (const float *)e, vl, vu,
+                                        il, iu, rank, world, m, brk, slice_cap, slice_cnt);
+    return -2;
+}
+
+int mr3_execute(mr3_ctx ctx, char jobz, void *w, void *Z, int64_t ldz, int64_t zcap,
+                int64_t *zcol_begin, int64_t *zcol_end, mr3_stats *stats) {
+    if (!ctx) return -1;
+    if (!zcol_begin || !zcol_end) return -7;
+    if (ctx->mode == 0)
+        return execute_impl<dd, double>(ctx, jobz, (double *)w, (double *)Z, ldz, zcap, zcol_begin,
+                                        zcol_end, stats);
+    return execute_impl<double, float>(ctx, jobz, (float *)w, (float *)Z, ldz, zcap, zcol_begin,
+                                       zcol_end, stats);
+}
+
+static int solve_common(mr3_ctx ctx, int mode, char jobz, char range, int64_t n, const void *d,
+                        const void *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
+                        void *w, void *Z, int64_t ldz, mr3_stats *stats) {
+    if (!ctx) return -1;
+    if (jobz != 'V' && jobz != 'N') return -2;
+    if (range != 'A' && range != 'I' && range != 'V') return -3;
+    if (n < 0) return -4;
+    if (!m) return -11;
+    if (n > 0 && !w) return -12;
+    if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -14;
+    double *brk = nullptr;
+    int64_t cap = 0, cntm = 0;
+    int rc = mr3_plan(ctx, mode, range, n, d, e, vl, vu, il, iu, 0, 1, m, &brk, &cap, &cntm);
+    if (rc) {
+        if (stats) *stats = ctx->stats;
+        return rc;
+    }
+    int64_t zb = 0, ze = 0;
+    rc = mr3_execute(ctx, jobz, w, Z, ldz, n, &zb, &ze, stats);
+    *m = ctx->m < 0 ? 0 : ctx->m;
+    return rc;
+}
+
+int mr3_dstemr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d, const double *e,
+                  double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
+                  int64_t ldz, mr3_stats *stats) {
+    return solve_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+}
+
+int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, const float *e,
+                 float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
+                 int64_t ldz, mr3_stats *stats) {
+    return solve_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+}
+
+int mr3_partition_columns(int64_t nseg, const int64_t *seg_begin, const double *cost, int world,
+                          int64_t *col_begin) {
+    if (world < 1 || nseg < 0 || !seg_begin || !col_begin || (nseg > 0 && !cost)) return -1;
+    const int64_t m = seg_begin[nseg];
+    double total = 0;
+    for (int64_t i = 0; i < nseg; i++) total += cost[i];
+    col_begin[0] = 0;
+    int r = 1;
+    double acc = 0;
+    for (int64_t i = 0; i < nseg && r < world; i++) {
+        acc += cost[i];
+        // cut after segment i once this rank's share is reached
+        while (r < world && acc >= total * r / world) {
+            col_begin[r] = (i + 1 < nseg) ? seg_begin[i + 1] : m;
+            r++;
+        }
+    }
+    for (; r < world; r++) col_begin[r] = m;
+    col_begin[world] = m;
+    for (int i = 1; i <= world; i++)
+        if (col_begin[i] < col_begin[i - 1]) col_begin[i] = col_begin[i - 1];
+    return 0;
+}
+
+int mr3_fp64_peak(mr3_ctx ctx, double *fp64_inst_per_s, double *dd_step_ns) {
+    if (!ctx) return -1;
+    cudaSetDevice(ctx->device);
+    int rc = 0;
+    double *out = (double *)getbuf(ctx, "peak_out", 64, &rc);
+    double *rep = (double *)getbuf(ctx, "peak_rep", 4096 * 64, &rc);
+    if (rc) return rc;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int iters = 4096, grid = ctx->nsm * 8, tpb = 256;
+    k_fp64_peak<<<grid, tpb, 0, ctx->stream>>>(out, 64, 1.0000001, 1e-9);  // warm-up
+    cudaEventRecord(a, ctx->stream);
+    k_fp64_peak<<<grid, tpb, 0, ctx->stream>>>(out, iters, 1.0000001, 1e-9);
+    cudaEventRecord(b, ctx->stream);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    if (fp64_inst_per_s)
+        *fp64_inst_per_s = (double)grid * tpb * iters * 64.0 / (ms * 1e-3);
+    k_fill_rep_test<<<16, 256, 0, ctx->stream>>>(rep, 4096);
+    int *ic = (int *)out;
+    const int reps = 8;
+    k_dd_latency<<<1, 1, 0, ctx->stream>>>(rep, 4096, 1, ic);
+    cudaEventRecord(a, ctx->stream);
+    k_dd_latency<<<1, 1, 0, ctx->stream>>>(rep, 4096, reps, ic);
+    cudaEventRecord(b, ctx->stream);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (dd_step_ns) *dd_step_ns = ms * 1e6 / (4096.0 * reps);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        ctx->err = cudaGetErrorString(e);
+        return MR3_ERR_CUDA;
+    }
+    return 0;
+}
+
+int mr3_last_kernel_times(mr3_ctx ctx, int *count, const char **names, double *ms,
+                          int *launches) {
+    if (!ctx || !count) return -1;
+    int c = 0;
+    for (auto &p : ctx->ktimes) {
+        if (c >= 16) break;
+        if (names) names[c] = p.first.c_str();
+        if (ms) ms[c] = p.second.first;
+        if (launches) launches[c] = p.second.second;
+        c++;
+    }
+    *count = c;
+    return 0;
+}
+
+int64_t mr3_last_launch_count(mr3_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+const char *mr3_strerror(int code) {
+    switch (code) {
+        case 0:
+            return "ok";
+        case MR3_ERR_NONFINITE:
+            return "NaN or Inf in d or e";
+        case MR3_ERR_CUDA:
+            return "CUDA error";
+        case MR3_ERR_NOMEM:
+            return "device allocation failed";
+        case MR3_ERR_NOCONV:
+            return "no convergence";
+        case MR3_ERR_ZCAP:
+            return "Z has too few columns";
+        case MR3_ERR_STATE:
+            return "execute without plan";
+        default:
+            return code < 0 ? "invalid argument" : "unknown error";
+    }
+}
+
+const char *mr3_last_error_string(mr3_ctx ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+const char *mr3_version(void) {
+    return "mr3-b200 sm_100a; dd (fp64 I/O) and fp64 (fp32 I/O) internal precision";
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the binary128 oracle.
+
+Sizes: small matrices the oracle finishes in seconds that still span several
+checkpoint blocks / output tiles and a ragged tail, edge cases, and the
+BASELINE.json configurations at full size on sampled outputs (oracle per index)
+plus size-independent properties (residuals of every column, exact
+orthogonality of every pair, eigenvalue ordering).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1304_1864_b200 as mr3
+import synth
+from mr3check import assert_parity, check_solution, exact_gram, exact_orthogonality
+
+pytestmark = pytest.mark.gpu
+
+
+def run(p, jobz="V", rng=None, il=1, iu=0, vl=0.0, vu=0.0):
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    rng = rng or p.range
+    if p.io == "f32":
+        w, Z, st = mr3.mr3_sstemr_d(d, e, jobz, rng, il or p.il, iu or p.iu, vl, vu)
+    else:
+        w, Z, st = mr3.mr3_dstemr_dd(d, e, jobz, rng, il or p.il, iu or p.iu, vl, vu)
+    torch.cuda.synchronize()
+    return w.cpu().numpy(), (Z.cpu().numpy() if Z is not None else None), st
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 9, 31, 33, 100, 257])
+@pytest.mark.parametrize("kind", ["uniform", "graded", "integer"])
+def test_small_random_full(n, kind):
+    p = synth.random_small(n, n + 7, kind)
+    w, Z, st = run(p)
+    assert w.shape == (n,) and Z.shape == (n, n)
+    assert np.all(np.diff(w) >= 0)
+    res = check_solution(p, w, Z, np.arange(1, n + 1))
+    assert_parity(res)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_uniform_1200(seed):
+    """Several checkpoint blocks, 10 output tiles, ragged tail (1200 = 37*32 + 16)."""
+    p = synth.random_uniform(1200, seed)
+    w, Z, st = run(p)
+    res = check_solution(p, w, Z, np.arange(1, p.n + 1), verbose=True)
+    assert_parity(res)
+    assert st["d_max"] == 0 and st["largest_cluster"] == 1
+
+
+def test_config1_121_full():
+    """BASELINE config 1 at full size, every pair against the oracle."""
+    p = synth.config(1)
+    w, Z, st = run(p)
+    res = check_solution(p, w, Z, np.arange(1, p.n + 1), verbose=True)
+    assert_parity(res)
+    assert st["d_max"] == 0  # d_max = 0 for non-Wilkinson types
+    k = np.arange(1, p.n + 1)
+    assert np.max(np.abs(w - (2 - 2 * np.cos(k * np.pi / (p.n + 1))))) < 4e-16 * 4 + 1e-15
+
+
+@pytest.mark.parametrize("copies", [2, 5, 12])
+def test_glued_wilkinson_small(copies):
+    """Clustered spectrum: child representations (tree depth >= 1)."""
+    p = synth.glued_wilkinson(copies, 21)
+    w, Z, st = run(p)
+    res = check_solution(p, w, Z, np.arange(1, p.n + 1), verbose=True)
+    assert_parity(res)
+    assert st["d_max"] >= 1
+
+
+def test_index_and_value_ranges():
+    p = synth.random_uniform(500, 4)
+    w, Z, st = run(p, rng="I", il=37, iu=211)
+    assert w.shape == (175,)
+    assert_parity(check_solution(p, w, Z, np.arange(37, 212)))
+    lh, _ = oracle.eigvals(p.d, p.e)
+    vl, vu = 0.5 * (lh[99] + lh[100]), 0.5 * (lh[299] + lh[300])
+    w2, Z2, _ = run(p, rng="V", vl=vl, vu=vu)
+    assert w2.shape == (200,)
+    assert_parity(check_solution(p, w2, Z2, np.arange(101, 301)))
+    # upper-half subset uses the right-end root
+    w3, Z3, _ = run(p, rng="I", il=450, iu=500)
+    assert_parity(check_solution(p, w3, Z3, np.arange(450, 501)))
+
+
+def test_values_only_matches_vectors_run():
+    p = synth.random_uniform(300, 9)
+    wn, Zn, _ = run(p, jobz="N")
+    wv, Zv, _ = run(p, jobz="V")
+    assert Zn is None
+    np.testing.assert_array_equal(wn, wv)
+    assert_parity(check_solution(p, wn, None, np.arange(1, 301)))
+
+
+def test_split_matrix():
+    """Exact zeros in e split T into blocks."""
+    p = synth.split_matrix(90, 3, split_at=(20, 21, 60))
+    w, Z, st = run(p)
+    assert st["n_blocks"] == 4
+    assert np.all(np.diff(w) >= 0)
+    assert_parity(check_solution(p, w, Z, np.arange(1, p.n + 1)))
+    w2, Z2, _ = run(p, rng="I", il=10, iu=70)
+    assert_parity(check_solution(p, w2, Z2, np.arange(10, 71)))
+
+
+def test_degenerate_inputs():
+    # n = 1
+    p = synth.Problem("one", np.array([3.5]), np.zeros(0))
+    w, Z, _ = run(p)
+    assert w.tolist() == [3.5] and Z.tolist() == [[1.0]]
+    # diagonal (all splits) with repeated values
+    p = synth.Problem("diag", np.array([3.0, 1.0, 2.0, 1.0]), np.zeros(3))
+    w, Z, _ = run(p)
+    np.testing.assert_array_equal(w, [1.0, 1.0, 2.0, 3.0])
+    assert np.allclose(np.abs(Z).sum(0), 1.0) and exact_orthogonality(torch.from_numpy(Z))[0] == 0
+    # zero matrix
+    p = synth.Problem("zero", np.zeros(5), np.zeros(4))
+    w, Z, _ = run(p)
+    assert np.all(w == 0) and exact_orthogonality(torch.from_numpy(Z))[0] == 0
+    # n = 0
+    w, Z, _ = mr3.mr3_dstemr_dd(torch.zeros(0, dtype=torch.float64, device="cuda"),
+                                torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert w.numel() == 0
+
+
+def test_error_codes():
+    d = torch.ones(10, dtype=torch.float64, device="cuda")
+    e = torch.ones(9, dtype=torch.float64, device="cuda")
+    d[3] = float("nan")
+    with pytest.raises(mr3.MR3Error) as ex:
+        mr3.mr3_dstemr_dd(d, e)
+    assert ex.value.code == 1
+    d[3] = 1.0
+    with pytest.raises(mr3.MR3Error) as ex:
+        mr3.mr3_dstemr_dd(d, e, "V", "I", 5, 3)
+    assert ex.value.code < 0
+    with pytest.raises(mr3.MR3Error):
+        mr3.mr3_dstemr_dd(d, e, "V", "V", 1, 1, 2.0, 1.0)
+
+
+def test_fp32_small_full():
+    p = synth.random_normal_f32(1000, 5, 1, 1000)
+    p.range = "A"
+    w, Z, st = run(p)
+    res = check_solution(p, w, Z, np.arange(1, 1001), io="f32")
+    assert_parity(res, io="f32")
+
+
+def test_fp32_subset():
+    p = synth.random_normal_f32(3000, 1, 1, 300)
+    w, Z, st = run(p)
+    res = check_solution(p, w, Z, np.arange(1, 301), io="f32")
+    assert_parity(res, io="f32")
+
+
+def test_deterministic_repeat():
+    p = synth.glued_wilkinson(4, 21)
+    w1, Z1, _ = run(p)
+    w2, Z2, _ = run(p)
+    np.testing.assert_array_equal(w1, w2)
+    np.testing.assert_array_equal(Z1, Z2)
+
+
+def test_two_phase_world_emulation_bitwise():
+    """Ranks of the plan/execute form emulated one after another on one GPU: the
+    union of their columns equals the world=1 solve bit for bit."""
+    import ctypes
+    p = synth.glued_wilkinson(8, 21)
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    w1, Z1, _ = mr3.mr3_dstemr_dd(d, e)
+    w1, Z1 = w1.cpu().numpy(), Z1.cpu().numpy()
+    L = mr3.lib()
+    world = 3
+    ctxs, bufs, caps = [], [], []
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for r in range(world):
+        h = ctypes.c_void_p()
+        assert L.mr3_create(ctypes.byref(h), 0, ctypes.c_void_p(streams[r].cuda_stream)) == 0
+        ctxs.append(h)
+        m = ctypes.c_int64()
+        brk = ctypes.c_void_p()
+        cap, cnt = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.mr3_plan(h, 0, b"A", p.n, ctypes.c_void_p(d.data_ptr()),
+                        ctypes.c_void_p(e.data_ptr()), 0.0, 0.0, 1, p.n, r, world,
+                        ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap), ctypes.byref(cnt))
+        assert rc == 0
+        torch.cuda.synchronize()
+        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * 4, d.device))
+        caps.append(cap.value)
+    rec = 4 * caps[0]
+    full = torch.cat([bufs[r][r * rec:(r + 1) * rec] for r in range(world)])
+    for r in range(world):
+        bufs[r][:world * rec].copy_(full)
+    torch.cuda.synchronize()
+    wall = np.zeros(p.n)
+    Zall = np.zeros((p.n, p.n))
+    for r in range(world):
+        w = torch.zeros(p.n, dtype=torch.float64, device="cuda")
+        Zs = torch.zeros((p.n, p.n), dtype=torch.float64, device="cuda")
+        zb, ze = ctypes.c_int64(), ctypes.c_int64()
+        st = mr3.Stats()
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
+                           ctypes.c_void_p(Zs.data_ptr()), p.n, p.n, ctypes.byref(zb),
+                           ctypes.byref(ze), ctypes.byref(st))
+        assert rc == 0
+        torch.cuda.synchronize()
+        a, b = zb.value, ze.value
+        wall[a:b] = w.cpu().numpy()[a:b]
+        Zall[:, a:b] = Zs[:b - a].T.cpu().numpy()
+    for h in ctxs:
+        L.mr3_destroy(h)
+    np.testing.assert_array_equal(wall, w1)
+    np.testing.assert_array_equal(Zall, Z1)
+
+
+def test_fp64_peak_microbenchmark():
+    ips, lat = mr3.fp64_peak()
+    assert 1e12 < ips < 1e14, ips
+    assert 1.0 < lat < 1e4, lat
+
+
+# ------------------------------------------------------------ full-size configs
+
+def _sample_indices(n, m, k=24, seed=0):
+    rng = np.random.default_rng(seed)
+    base = [1, 2, 3, m - 2, m - 1, m]
+    rest = rng.choice(np.arange(4, m - 2), size=k - len(base), replace=False)
+    return np.unique(np.concatenate([base, rest]))
+
+
+@pytest.mark.slow
+def test_config2_full_size():
+    p = synth.config(2)
+    w, Z, st = run(p)
+    assert np.all(np.diff(w) >= 0)
+    o, dd = exact_orthogonality(torch.from_numpy(Z).cuda())
+    assert o <= 1e-14 and dd <= 1e-14
+    r1, r2, _ = oracle.residuals(p.d, p.e, w, Z)
+    assert r2.max() <= 1e-15
+    idx = _sample_indices(p.n, p.n)
+    res = check_solution(p, w[idx - 1], Z[:, idx - 1], idx, full_orth=False, verbose=True)
+    assert_parity(res)
+
+
+@pytest.mark.slow
+def test_config3_full_size():
+    p = synth.config(3)
+    w, Z, st = run(p)
+    assert st["d_max"] >= 1
+    o, dd = exact_orthogonality(torch.from_numpy(Z).cuda())
+    assert o <= 1e-14 and dd <= 1e-14, (o, dd)
+    r1, r2, _ = oracle.residuals(p.d, p.e, w, Z)
+    assert r2.max() <= 1e-15
+    # Weyl: eigenvalues within 2^-26 of the W21 multiset (test_oracle_pins pins the oracle)
+    db, eb = synth.wilkinson_block(21)
+    jh, jl, _, _ = oracle.jacobi(db, eb)
+    ref = np.sort(np.repeat(jh + jl, 200))
+    assert np.max(np.abs(w - ref)) <= 2.0 ** -26 * 1.0001
+    idx = np.array([1, 2, 200, 201, 2100, 2101, 4000, 4199, 4200])
+    lh, ll = oracle.eigvals(p.d, p.e, idx)
+    assert np.max(np.abs(w[idx - 1] - lh)) <= 4e-16 * oracle.norm1(p.d, p.e)
+
+
+@pytest.mark.slow
+def test_config4_full_size():
+    p = synth.config(4)
+    w, Z, st = run(p)
+    assert w.shape == (2000,)
+    o, dd = exact_orthogonality(torch.from_numpy(Z).cuda())
+    assert o <= 5e-6 and dd <= 5e-6
+    idx = _sample_indices(p.n, 2000, k=16)
+    res = check_solution(p, w[idx - 1], Z[:, idx - 1], idx, io="f32", full_orth=False,
+                         verbose=True)
+    assert_parity(res, io="f32")
+
+
+@pytest.mark.slow
+def test_config5_full_size_sampled():
+    """Legendre n = 50000 (Z = 20 GB): the bench workload, sampled against the oracle."""
+    p = synth.config(5)
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    w, Z, st = mr3.mr3_dstemr_dd(d, e)
+    torch.cuda.synchronize()
+    assert st["d_max"] == 0 and st["largest_cluster"] == 1  # rho = 1/n (Table 2)
+    wc = w.cpu().numpy()
+    assert np.all(np.diff(wc) > 0)
+    idx = _sample_indices(p.n, p.n, k=12)
+    Zs = Z[:, torch.from_numpy(idx - 1).cuda()]
+    res = check_solution(p, wc[idx - 1], Zs.cpu().numpy(), idx, full_orth=True, verbose=True)
+    assert_parity(res)
+    # orthogonality of the sample against every column, exactly (c7)
+    G = exact_gram(Zs, Z)
+    G[torch.arange(idx.size, device="cuda"), torch.from_numpy(idx - 1).cuda()] -= 1.0
+    assert float(G.abs().max()) <= 1e-14
+    del G, Z
+    torch.cuda.empty_cache()
