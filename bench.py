@@ -118,7 +118,7 @@ def run_reference(args, p, rank, world):
     import oracle
     oracle.build()
     cores = oracle.num_threads()
-    per_step = args.cpu_sample or max(2 * cores, 8)
+    per_step = args.cpu_sample or max(8 * cores, 16)
     for _ in range(args.warmup):
         cpu_baseline_run(p, min(per_step, 4))
     tot_n, tot_t = 0, 0.0
@@ -298,7 +298,7 @@ def main():
     if rank == 0 and not args.no_cpu:
         import oracle
         oracle.build()
-        k = args.cpu_sample or max(2 * oracle.num_threads(), 8)
+        k = args.cpu_sample or max(32 * oracle.num_threads(), 64)
         cnt, dt_cpu, cores = cpu_baseline_run(p, k)
         result["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
                                   "kind": "oracle",

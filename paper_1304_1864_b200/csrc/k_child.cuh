@@ -50,9 +50,16 @@ __device__ void dstqds_write(const double *__restrict__ rep, int64_t n, R tau, d
 // end lambda_p - delta or right end lambda_q + delta -- and back-off level q >> 1,
 // delta geometric from just outside the end bracket to half the outer gap;
 // PAPER.md L1047-L1054 "back off further away than usual").
-// Accept the first candidate (priority = lane) whose growth <= elg1 * spdiam,
-// else <= elg2 * spdiam (relaxed k_elg, Eq. (3.5)), else the
-// smallest growth (L567-L572, counted as a robustness failure).
+// Acceptance (nearest candidate first, priority = lane):
+//   1. growth <= elg1 * spdiam among the four nearest back-off levels;
+//   2. growth <= elg2 * spdiam, elg2 = max(10, eps_x / (eps_y sqrt(n))): the
+//      relaxed k_elg of the mixed-precision setting (Eq. (3.5)),
+//      which costs no accuracy; preferring a near shift under the relaxed bound
+//      over a far one under the strict bound keeps the child eigenvalues small,
+//      so the cluster actually splits (glued matrices: localized vectors make
+//      max|d+| large exactly where the cluster's vectors are negligible --
+//      "conditional" growth, Def. 2.4);
+//   3. else the smallest growth (L567-L572), counted as a robustness failure.
 template <class R>
 __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, Items it,
                                               const int32_t *__restrict__ next_active,
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
                                               const int32_t *__restrict__ cend, int nclus,
                                               double *child_pool, int64_t pool_stride_rows,
                                               double spdiam, double elg1, double elg2,
-                                              double pivmin, DevStats *st) {
+                                              double pivmin, DevStats *st, double *dbg) {
     const int c = blockIdx.x;
     if (c >= nclus) return;
     const int lane = threadIdx.x;
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     double delta = d0 * pow(cap / d0, (double)lev / 15.0);
     R tau = side ? add(lamR, mk<R>(delta)) : sub(lamL, mk<R>(delta));
     double growth = dstqds_growth<R>(P.rep, P.n, tau, pivmin);
-    unsigned ok1 = __ballot_sync(0xffffffffu, growth <= elg1 * spdiam);
+    unsigned ok1 = __ballot_sync(0xffffffffu, growth <= elg1 * spdiam) & 0xffu;
     unsigned ok2 = __ballot_sync(0xffffffffu, growth <= elg2 * spdiam);
     int win;
     bool fail = false;
@@ -116,6 +123,12 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
         ch.depth = P.depth + 1;
         nodes[node_base + c] = ch;
         if (fail) atomicAdd(&st->robustness_failures, 1);
+        if (dbg) {
+            dbg[4 * c + 0] = win;
+            dbg[4 * c + 1] = growth;
+            dbg[4 * c + 2] = delta;
+            dbg[4 * c + 3] = hi(t);
+        }
     }
     __syncwarp();
     // translate the member brackets into the child's coordinates (Alg. 1 l.16)

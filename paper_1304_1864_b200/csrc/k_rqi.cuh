@@ -180,8 +180,15 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
         const double tol = A.krs * gap * A.eps_x * sqrt((double)nd.n);
         bool done = false;
+        if (nd.n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
+            lam_out = load_row4<R>(nd.rep, 0).d;
+            r = 0;
+            nz2 = mk<R>(1.0);
+            done = true;
+            iters = 0;
+        }
 #pragma unroll 1
-        for (iters = 1; iters <= A.maxit && !done; iters++) {
+        for (iters = 1; !done && iters <= A.maxit; iters++) {
             int c = rq_forward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.S, slot);
             rq_backward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.ck_p, A.S, slot, r, gr,
                            nz2);
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
             if (!(lt(a, lam_new) && lt(lam_new, b))) lam_new = half(add(a, b));
             lam = lam_new;
         }
-        if (!done) {
+        if (!done && nd.n > 1) {
             // fallback: bisection to relative eps_x sqrt(n) gaptol, one more solve
             fallback = true;
             double rtol = A.eps_x * sqrt((double)nd.n) * A.gaptol;

@@ -268,31 +268,52 @@ __global__ void k_split_list(const T *__restrict__ e, int64_t n, double thr, int
 }
 
 // ---------------------------------------------------------------------------
-// K1b: root representation, one thread per irreducible block (Alg. 1 l.1-2).
-// mu just outside the Gershgorin interval of the block (left: all d > 0,
-// right: all d < 0: a definite LDL^T, L1022-L1025), then
-//   d_1 = a_1 - mu ; l_i = e_i / d_i ; d_{i+1} = (a_{i+1} - mu) - l_i e_i
-// in R, the random relative perturbation x <- x (1 + xi u) of all 2n-1 data
-// (L901-L909), derived ld, lld, and certified root brackets.
+// K1b: root representations (Alg. 1 l.1-2), chunk-parallel.
+//
+// mu just outside the Gershgorin interval of each block (left: T - mu I positive
+// definite, all d > 0; right: negative definite; L1022-L1025), then the LDL^T of
+// T - mu I: d_1 = c_1, d_{r} = c_r - e_{r-1}^2 / d_{r-1}, l_r = e_r / d_r, with
+// c_r = a_r - mu.  The pivot recurrence is a continued fraction: with the state
+// (p, q) (d_{r-1} = p/q) row r maps it by A_r = [[c_r, -e_{r-1}^2], [1, 0]].
+// Chunks of RT_CH rows form their transfer matrices in R (k_root_chunkmat), one
+// thread per block scans them (k_root_scan), and every chunk then runs the
+// plain recurrence from its incoming pivot (k_root_factor).  The incoming pivot
+// of a chunk differs from the sequential one only by the rounding of the 2x2
+// products (relative ~ eps_y * O(n)), i.e. a relative perturbation of T far
+// below the xi = eps_x perturbation that follows (reading R3).
+// Then every datum d_i, l_i is perturbed x <- x (1 + xi u) (L901-L909), and the
+// derived ld = d l, lld = d l^2 are formed.  A 1x1 block is left unperturbed
+// (its eigenvalue is exactly d).
 // ---------------------------------------------------------------------------
 struct BlockDesc {
     int64_t row0, n;
 };
+struct ChunkDesc {
+    int64_t row0;   // first row (global)
+    int32_t len;    // rows in the chunk
+    int32_t block;  // owning block
+};
+constexpr int RT_CH = 32;
+
+template <class R>
+struct Mat2 {
+    R a, b, c, d;
+};
+
+template <class R>
+__device__ __forceinline__ R scale2(R x, int e) {
+    return mk2<R>(ldexp(hi(x), e), ldexp(lo_part(x), e));
+}
 
 template <class R, class T>
-__global__ void k_root(const T *__restrict__ d, const T *__restrict__ e, const BlockDesc *blocks,
-                       int nblocks, double scale, int right_side, double xi, uint64_t seed,
-                       double pivmin, double *rep_pool, int64_t rep_stride_rows,
-                       NodeInfo *nodes, double *brk /* per block: lo(R) hi(R) as 4 doubles */,
-                       int *fail) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nblocks) return;
+__global__ void k_root_gersh(const T *__restrict__ d, const T *__restrict__ e,
+                             const BlockDesc *blocks, double scale, int right, double padmul,
+                             double pivmin, double *mu_out, double *brk) {
+    const int b = blockIdx.x;
     const int64_t r0 = blocks[b].row0, n = blocks[b].n;
-    double *rep = rep_pool + r0 * 4 * Prec<R>::words;  // blocks own disjoint rows
-    (void)rep_stride_rows;
-    // block Gershgorin (scaled)
+    __shared__ double sg[32], su[32], sn[32];
     double gl = INFINITY, gu = -INFINITY, nrm = 0.0;
-    for (int64_t i = 0; i < n; i++) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         double di = (double)d[r0 + i] * scale;
         double r = (i > 0 ? fabs((double)e[r0 + i - 1]) * scale : 0.0) +
                    (i < n - 1 ? fabs((double)e[r0 + i]) * scale : 0.0);
@@ -300,77 +321,167 @@ __global__ void k_root(const T *__restrict__ d, const T *__restrict__ e, const B
         gu = fmax(gu, di + r);
         nrm = fmax(nrm, fabs(di) + r);
     }
-    double pad = 4.0 * 1.1102230246251565e-16 * fmax(fmax(fabs(gl), fabs(gu)), nrm) + pivmin;
-    bool right = right_side != 0;
-    double mu = 0.0;
-    bool ok = false;
-    for (int attempt = 0; attempt < 40 && !ok; attempt++) {
-        mu = right ? gu + pad : gl - pad;
-        ok = true;
-        // factor T_b - mu I
-        R dcur = sub(mk<R>((double)d[r0] * scale), mk<R>(mu));
-        for (int64_t i = 0; i < n; i++) {
-            bool good = right ? (hi(dcur) < 0.0) : (hi(dcur) > 0.0);
-            if (!good || !isfinite(hi(dcur))) {
-                ok = false;
-                break;
-            }
-            R li = mk<R>(0.0);
-            R dnext = mk<R>(0.0);
-            if (i < n - 1) {
-                double ei = (double)e[r0 + i] * scale;
-                li = div(mk<R>(ei), dcur);
-                R a = sub(mk<R>((double)d[r0 + i + 1] * scale), mk<R>(mu));
-                dnext = sub(a, mul(li, ei));
-            }
-            // perturb the data d_i, l_i (global row index keys the generator)
-            uint64_t grow = (uint64_t)(r0 + i);
-            R dp = mul(dcur, mk<R>(1.0));
-            {
-                double u = uniform_pm1(seed, grow, 0);
-                dp = add(dcur, mul(dcur, xi * u));
-            }
-            R lp = li;
-            if (i < n - 1) {
-                double u = uniform_pm1(seed, grow, 1);
-                lp = add(li, mul(li, xi * u));
-            }
-            R ldv = mul(dp, lp);
-            R lldv = mul(ldv, lp);
-            store_row4<R>(rep, i, dp, lldv, lp, ldv);
-            dcur = dnext;
-        }
-        pad *= 16.0;
+    for (int o = 16; o > 0; o >>= 1) {
+        gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+        gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+        nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
     }
-    if (!ok) atomicExch(fail, 1);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sg[w] = gl;
+        su[w] = gu;
+        sn[w] = nrm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
+            gl = fmin(gl, sg[i]);
+            gu = fmax(gu, su[i]);
+            nrm = fmax(nrm, sn[i]);
+        }
+        double pad = (4.0 * 1.1102230246251565e-16 * fmax(fmax(fabs(gl), fabs(gu)), nrm) + pivmin) *
+                     padmul;
+        double mu = right ? gu + pad : gl - pad;
+        mu_out[b] = mu;
+        // certified enclosure of the root's eigenvalues: the data are perturbed by
+        // at most (1 + xi)^(2n) ~ 1 + 2 n xi relative, far inside the 1e-3 margin
+        double lo, hi_;
+        if (right) {
+            lo = (gl - mu) * (1.0 + 1e-3) - pad;
+            hi_ = 0.0;
+        } else {
+            lo = 0.0;
+            hi_ = (gu - mu) * (1.0 + 1e-3) + pad;
+        }
+        brk[4 * b + 0] = lo;
+        brk[4 * b + 1] = 0.0;
+        brk[4 * b + 2] = hi_;
+        brk[4 * b + 3] = 0.0;
+    }
+}
+
+template <class R>
+__device__ __forceinline__ R shifted_diag(double dv, double mu) {  // c = d - mu, exact in dd
+    return sub(mk<R>(dv), mk<R>(mu));
+}
+
+template <class R, class T>
+__global__ void k_root_chunkmat(const T *__restrict__ d, const T *__restrict__ e,
+                                const ChunkDesc *chunks, int nch, const BlockDesc *blocks,
+                                double scale, const double *mu, Mat2<R> *mats) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nch) return;
+    const ChunkDesc ch = chunks[k];
+    const int64_t b0 = blocks[ch.block].row0;
+    const double m = mu[ch.block];
+    Mat2<R> M;
+    M.a = mk<R>(1.0);
+    M.b = mk<R>(0.0);
+    M.c = mk<R>(0.0);
+    M.d = mk<R>(1.0);
+    for (int j = 0; j < ch.len; j++) {
+        const int64_t r = ch.row0 + j;
+        R c = shifted_diag<R>((double)d[r] * scale, m);
+        R na, nb;
+        if (r > b0) {
+            double ev = (double)e[r - 1] * scale;
+            R e2 = mul(mk<R>(ev), ev);
+            na = sub(mul(c, M.a), mul(e2, M.c));
+            nb = sub(mul(c, M.b), mul(e2, M.d));
+        } else {
+            na = mul(c, M.a);
+            nb = mul(c, M.b);
+        }
+        M.c = M.a;
+        M.d = M.b;
+        M.a = na;
+        M.b = nb;
+        if ((j & 7) == 7 || j == ch.len - 1) {  // projective: rescale by a power of 2
+            double mx = fmax(fmax(fabs(hi(M.a)), fabs(hi(M.b))), fmax(fabs(hi(M.c)), fabs(hi(M.d))));
+            int ex = 0;
+            if (mx > 0) frexp(mx, &ex);
+            M.a = scale2(M.a, -ex);
+            M.b = scale2(M.b, -ex);
+            M.c = scale2(M.c, -ex);
+            M.d = scale2(M.d, -ex);
+        }
+    }
+    mats[k] = M;
+}
+
+// one thread per block: incoming state of every chunk, (p, q) = (1, 0) at the top
+template <class R>
+__global__ void k_root_scan(const int *blk_chunk0, int nblocks, const Mat2<R> *mats,
+                            R *states) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    R p = mk<R>(1.0), q = mk<R>(0.0);
+    for (int k = blk_chunk0[b]; k < blk_chunk0[b + 1]; k++) {
+        states[2 * k] = p;
+        states[2 * k + 1] = q;
+        const Mat2<R> M = mats[k];
+        R np = add(mul(M.a, p), mul(M.b, q));
+        R nq = add(mul(M.c, p), mul(M.d, q));
+        double mx = fmax(fabs(hi(np)), fabs(hi(nq)));
+        int ex = 0;
+        if (mx > 0) frexp(mx, &ex);
+        p = scale2(np, -ex);
+        q = scale2(nq, -ex);
+    }
+}
+
+template <class R, class T>
+__global__ void k_root_factor(const T *__restrict__ d, const T *__restrict__ e,
+                              const ChunkDesc *chunks, int nch, const BlockDesc *blocks,
+                              double scale, const double *mu, const R *states, int right,
+                              double xi, uint64_t seed, double *rep_pool, int *fail) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nch) return;
+    const ChunkDesc ch = chunks[k];
+    const int64_t b0 = blocks[ch.block].row0, bn = blocks[ch.block].n;
+    const double m = mu[ch.block];
+    R dprev = mk<R>(0.0);
+    if (ch.row0 > b0) dprev = div(states[2 * k], states[2 * k + 1]);
+    bool bad = false;
+    for (int j = 0; j < ch.len; j++) {
+        const int64_t r = ch.row0 + j;
+        R c = shifted_diag<R>((double)d[r] * scale, m);
+        R dr = c;
+        if (r > b0) {
+            double ev = (double)e[r - 1] * scale;
+            R lprev = div(mk<R>(ev), dprev);
+            dr = sub(c, mul(lprev, ev));
+        }
+        bool good = right ? (hi(dr) < 0.0) : (hi(dr) > 0.0);
+        if (!good || !isfinite(hi(dr))) bad = true;
+        R lr = mk<R>(0.0);
+        if (r < b0 + bn - 1) lr = div(mk<R>((double)e[r] * scale), dr);
+        R dp = dr, lp = lr;
+        if (bn > 1) {
+            dp = add(dr, mul(dr, xi * uniform_pm1(seed, (uint64_t)r, 0)));
+            if (r < b0 + bn - 1) lp = add(lr, mul(lr, xi * uniform_pm1(seed, (uint64_t)r, 1)));
+        }
+        R ldv = mul(dp, lp);
+        store_row4<R>(rep_pool + r * 4 * Prec<R>::words, 0, dp, mul(ldv, lp), lp, ldv);
+        dprev = dr;
+    }
+    if (bad) atomicExch(fail, 1);
+}
+
+template <class R>
+__global__ void k_root_nodes(const BlockDesc *blocks, int nblocks, const double *mu,
+                             double *rep_pool, NodeInfo *nodes) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
     NodeInfo ni;
-    ni.rep = rep;
-    ni.n = n;
-    ni.row0 = r0;
-    ni.sig_hi = mu;
+    ni.rep = rep_pool + blocks[b].row0 * 4 * Prec<R>::words;
+    ni.n = blocks[b].n;
+    ni.row0 = blocks[b].row0;
+    ni.sig_hi = mu[b];
     ni.sig_lo = 0.0;
     ni.depth = 0;
     ni.block = b;
     nodes[b] = ni;
-    // certified bracket for all eigenvalues of the block in root coordinates
-    double span = gu - gl;
-    double lo = right ? (gl - mu) - pad - 1e-3 * span : -pad;
-    double hiv = right ? pad : (gu - mu) + pad + 1e-3 * span;
-    if (!right) lo = -fmax(pad, pivmin * 4.0);
-    for (int it = 0; it < 60; it++) {
-        int c = negcount<R>(rep, n, mk<R>(lo), pivmin);
-        if (c == 0) break;
-        lo -= fmax(span, 1.0) * (double)(1 << (it < 20 ? it : 20));
-    }
-    for (int it = 0; it < 60; it++) {
-        int c = negcount<R>(rep, n, mk<R>(hiv), pivmin);
-        if (c == n) break;
-        hiv += fmax(span, 1.0) * (double)(1 << (it < 20 ? it : 20));
-    }
-    brk[4 * b + 0] = lo;
-    brk[4 * b + 1] = 0.0;
-    brk[4 * b + 2] = hiv;
-    brk[4 * b + 3] = 0.0;
 }
 
 // counts of the root at two shifts (value range -> index range)

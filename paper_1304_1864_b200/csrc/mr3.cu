@@ -75,6 +75,7 @@ struct mr3_ctx_s {
     int node_cap = 0;
     int G0 = 1;
     int64_t launches = 0;
+    int debug = 0;
     mr3_stats stats;
 };
 
@@ -163,6 +164,11 @@ static void kt_collect(mr3_ctx ctx) {
     }
     ctx->kt_used = 0;
 }
+
+static inline double hi_of(double x) { return x; }
+static inline double lo_of(double) { return 0.0; }
+static inline double hi_of(const dd &x) { return x.hi; }
+static inline double lo_of(const dd &x) { return x.lo; }
 
 template <class R>
 struct Work {
@@ -271,7 +277,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     if (info.norm1 > 0) frexp(info.norm1, &ex);
     ctx->scale = info.norm1 > 0 ? ldexp(1.0, -ex) : 1.0;  // scaled ||T||_1 in [0.5, 1)
     const double nrm_s = info.norm1 * ctx->scale;
-    ctx->pivmin = eps_y * fmax(nrm_s, 1e-300);
+    ctx->pivmin = eps_y * (info.norm1 > 0 ? nrm_s : 1.0);
     ctx->spdiam = fmax((info.gu - info.gl) * ctx->scale, 1e-300);
 
     // splitting: |e_i| <= eps_x ||T||
@@ -309,10 +315,25 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     ctx->split = ctx->nblocks > 1;
     ctx->stats.n_blocks = ctx->nblocks;
 
-    // K1b: root representations
+    // K1b: root representations (chunk-parallel LDL^T + perturbation)
     const int words = Prec<R>::words;
+    std::vector<ChunkDesc> chunks;
+    std::vector<int> blk_chunk0(blocks.size() + 1);
+    for (size_t bi = 0; bi < blocks.size(); bi++) {
+        blk_chunk0[bi] = (int)chunks.size();
+        for (int64_t r = 0; r < blocks[bi].n; r += RT_CH)
+            chunks.push_back({blocks[bi].row0 + r, (int32_t)std::min<int64_t>(RT_CH, blocks[bi].n - r),
+                              (int32_t)bi});
+    }
+    blk_chunk0[blocks.size()] = (int)chunks.size();
+    const int nch = (int)chunks.size();
     double *rep_pool = (double *)getbuf(ctx, "rep_root", (size_t)n * 4 * words * 8, &rc);
     BlockDesc *dblocks = (BlockDesc *)getbuf(ctx, "blocks", blocks.size() * sizeof(BlockDesc), &rc);
+    ChunkDesc *dchunks = (ChunkDesc *)getbuf(ctx, "chunks", chunks.size() * sizeof(ChunkDesc), &rc);
+    int *dbc0 = (int *)getbuf(ctx, "blk_chunk0", blk_chunk0.size() * 4, &rc);
+    Mat2<R> *dmats = (Mat2<R> *)getbuf(ctx, "root_mats", (size_t)nch * sizeof(Mat2<R>), &rc);
+    R *dstates = (R *)getbuf(ctx, "root_states", (size_t)nch * 2 * sizeof(R), &rc);
+    double *dmu = (double *)getbuf(ctx, "root_mu", blocks.size() * 8, &rc);
     double *dbrk0 = (double *)getbuf(ctx, "brk_root", blocks.size() * 4 * 8, &rc);
     int *dfail = (int *)getbuf(ctx, "fail", 16, &rc);
     ctx->node_cap = std::max<int>(1024, ctx->nblocks * 2 + 64);
@@ -320,7 +341,9 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     if (rc) return rc;
     CK(cudaMemcpyAsync(dblocks, blocks.data(), blocks.size() * sizeof(BlockDesc),
                        cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(dfail, 0, 4, s));
+    CK(cudaMemcpyAsync(dchunks, chunks.data(), chunks.size() * sizeof(ChunkDesc),
+                       cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dbc0, blk_chunk0.data(), blk_chunk0.size() * 4, cudaMemcpyHostToDevice, s));
     int right = 0;
     if (!ctx->split) {
         if (range == 'I' && (il + iu) > n + 1) right = 1;
@@ -328,10 +351,33 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     }
     const double xi = P[MR3_XI];
     const uint64_t seed = (uint64_t)P[MR3_SEED];
-    k_root<R, T><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(d, e, dblocks, ctx->nblocks, ctx->scale,
-                                                         right, xi, seed, ctx->pivmin, rep_pool, 0,
-                                                         dnodes, dbrk0, dfail);
-    CKL("k_root");
+    double padmul = 1.0;
+    for (int attempt = 0; attempt < 12; attempt++, padmul *= 16.0) {
+        CK(cudaMemsetAsync(dfail, 0, 4, s));
+        k_root_gersh<R, T><<<ctx->nblocks, 256, 0, s>>>(d, e, dblocks, ctx->scale, right, padmul,
+                                                         ctx->pivmin, dmu, dbrk0);
+        CKL("k_root_gersh");
+        k_root_chunkmat<R, T><<<(nch + 127) / 128, 128, 0, s>>>(d, e, dchunks, nch, dblocks,
+                                                                 ctx->scale, dmu, dmats);
+        CKL("k_root_chunkmat");
+        k_root_scan<R><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(dbc0, ctx->nblocks, dmats, dstates);
+        CKL("k_root_scan");
+        k_root_factor<R, T><<<(nch + 127) / 128, 128, 0, s>>>(d, e, dchunks, nch, dblocks,
+                                                               ctx->scale, dmu, dstates, right, xi,
+                                                               seed, rep_pool, dfail);
+        CKL("k_root_factor");
+        int hfail = 0;
+        CK(cudaMemcpyAsync(&hfail, dfail, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!hfail) break;
+        if (attempt == 11) {
+            ctx->err = "root representation: no definite shift found";
+            return MR3_ERR_CUDA;
+        }
+    }
+    k_root_nodes<R><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(dblocks, ctx->nblocks, dmu, rep_pool,
+                                                             dnodes);
+    CKL("k_root_nodes");
     ctx->nodes_used = ctx->nblocks;
 
     // index set
@@ -440,8 +486,6 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                                                                     dbrk + 4 * first);
         CKL("k_items_to_brk");
     }
-    int hfail = 0;
-    CK(cudaMemcpyAsync(&hfail, dfail, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *m = ctx->m;
     *brk = dbrk;
@@ -573,6 +617,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int nsing = hc[0], nclus = hc[1], nmem = hc[2];
+    if (ctx->debug) fprintf(stderr, "[mr3] level 0: %d singles %d clusters %d members\n", nsing, nclus, nmem);
 
     // multi-rank: cluster-whole partition of the output columns
     int64_t c0 = 0, c1 = m;
@@ -700,6 +745,32 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         return 0;
     };
 
+    auto dump = [&](const char *tag, const int32_t *list, int cntl, int lvl) {
+        if (!ctx->debug) return;
+        cudaStreamSynchronize(ctx->stream);
+        std::vector<int32_t> ids(cntl);
+        std::vector<R> lo(cnt), hi(cnt);
+        std::vector<int32_t> nodev(cnt), kv(cnt);
+        std::vector<double> lg(cnt), rg(cnt);
+        cudaMemcpy(ids.data(), list, cntl * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(lo.data(), W.it.lo, cnt * sizeof(R), cudaMemcpyDeviceToHost);
+        cudaMemcpy(hi.data(), W.it.hi, cnt * sizeof(R), cudaMemcpyDeviceToHost);
+        cudaMemcpy(nodev.data(), W.it.node, cnt * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(kv.data(), W.it.k, cnt * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(lg.data(), W.it.lgap, cnt * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(rg.data(), W.it.rgap, cnt * 8, cudaMemcpyDeviceToHost);
+        std::vector<NodeInfo> nds(ctx->nodes_used);
+        cudaMemcpy(nds.data(), W.nodes, ctx->nodes_used * sizeof(NodeInfo), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[mr3] level %d %s: %d items\n", lvl, tag, cntl);
+        for (int i = 0; i < cntl && i < ctx->debug; i++) {
+            int id = ids[i];
+            const NodeInfo &nd = nds[nodev[id]];
+            fprintf(stderr, "  id %d k %d node %d depth %d sig %.17g lo %.17g%+.3g hi %.17g%+.3g w %.3g lg %.3g rg %.3g\n",
+                    id, kv[id], nodev[id], nd.depth, nd.sig_hi, hi_of(lo[id]), lo_of(lo[id]),
+                    hi_of(hi[id]), lo_of(hi[id]), hi_of(hi[id]) - hi_of(lo[id]), lg[id], rg[id]);
+        }
+    };
+
     // level loop (Alg. 1 l.5-17, breadth-first)
     int level = 0;
     int32_t *cur = listA, *nxt = listB;
@@ -745,15 +816,28 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         double *pool =
             (double *)getbuf(ctx, pname, (size_t)nclus * ctx->n * 4 * words * 8, &rc);
         if (rc) return rc;
+        double *cdbg = nullptr;
+        if (ctx->debug) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
         k_child<R><<<nclus, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, nxt, cbeg, cend, nclus,
-                                        pool, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st);
+                                        pool, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st,
+                                        cdbg);
         kt_end(ctx, tch);
         CKL("k_child");
+        if (ctx->debug) {
+            std::vector<double> hd(4 * nclus);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(hd.data(), cdbg, nclus * 32, cudaMemcpyDeviceToHost);
+            for (int c = 0; c < nclus && c < ctx->debug; c++)
+                fprintf(stderr, "[mr3] child %d: lane %g growth %.3g delta %.3g tau %.17g\n", c,
+                        hd[4 * c], hd[4 * c + 1], hd[4 * c + 2], hd[4 * c + 3]);
+        }
         ctx->nodes_used += nclus;
+        dump("after child", nxt, nmem, level + 1);
         // K2: refine in the child coordinates (certified)
         rc = launch_bisect<R>(ctx, W, nxt, nmem, Gc, rtol, absfloor, 1);
         if (rc) return rc;
+        dump("after refine", nxt, nmem, level + 1);
         // K3: classify the members
         std::swap(cur, nxt);
         so.next_active = nxt;
@@ -767,6 +851,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         nclus = hc[1];
         nmem = hc[2];
         level++;
+        if (ctx->debug)
+            fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
+                    nclus, nmem);
     }
     ctx->stats.d_max = level;
     DevStats hst;
@@ -817,6 +904,8 @@ int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
         ctx->own_stream = true;
     }
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
+    const char *dbg = getenv("MR3_DEBUG");
+    ctx->debug = dbg ? atoi(dbg) : 0;
     *out = ctx;
     return 0;
 }
