@@ -16,7 +16,6 @@ N > 1  : launched by torchrun, one rank per GPU; the index set is partitioned
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -31,7 +30,7 @@ import synth  # noqa: E402
 # SASS-counted FP64-pipe instructions (DADD/DMUL/DFMA/DSETP; MUFU.RCP64H is on the XU) per row of
 # the dd negcount loop of k_bisect<dd,1> (recount
 # with tools/count_sass.py after every change of the loop body).
-FP64_INST_PER_BISECT_ROW = {"dd": 46, "f64": 12}
+FP64_INST_PER_BISECT_ROW = {"dd": 46, "f64": 12, "x": 11}  # "x": binary_x phase rows
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 
 
@@ -49,26 +48,36 @@ def parse():
 
 
 class Clocks:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region (in-process NVML,
+    every 200 ms; nvidia-smi in a subprocess would fork this large process)."""
 
     def __init__(self, dev):
         self.dev = dev
         self.samples = []
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        except Exception:
+            self.nvml = None
 
     def run(self):
+        nv = self.nvml
+        if nv is None:
+            return
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.samples.append((sm, mx, rs, pw))
             except Exception:
                 pass
             self.stop.wait(0.2)
@@ -80,21 +89,35 @@ class Clocks:
     def __exit__(self, *a):
         self.stop.set()
         self.t.join(timeout=10)
+        if self.nvml is not None and not self.samples:
+            self.sample_once()
+
+    def sample_once(self):
+        self.stop.clear()
+        self.stop.set()
+        try:
+            nv = self.nvml
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h),
+                                 nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
+        except Exception:
+            pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
         reasons = set()
-        for s in self.samples:
-            for nm, v in zip(names, s[5:9]):
-                if v.strip().lower() == "active":
+        for _, _, rs, _ in self.samples:
+            for nm, bit in bits.items():
+                if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": float(max(s[1] for s in self.samples)),
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "power_w_max": float(max(s[3] for s in self.samples))}
 
 
 def cpu_baseline_run(p, n_idx, seed=0):
@@ -226,8 +249,10 @@ def main():
     kb_ms, kb_n = ktot.get("k_bisect", (0.0, 0))
     mode = "f64" if p.io == "f32" else "dd"
     rows = stats["bisect_rows"] if stats else 0.0
-    # bisect_rows counts plan + cluster refinement of the last step; per launch:
-    achieved = rows * FP64_INST_PER_BISECT_ROW[mode] / (kb_ms / args.steps * 1e-3) if kb_ms else 0
+    rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
+    # bisect_rows(_x) count plan + cluster refinement of the last step:
+    inst = rows * FP64_INST_PER_BISECT_ROW[mode] + rows_x * FP64_INST_PER_BISECT_ROW["x"]
+    achieved = inst / (kb_ms / args.steps * 1e-3) if kb_ms else 0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -255,8 +280,10 @@ def main():
                          "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz",
                          "measured_peak_same_run": peak_ips / 1e12,
                          "frac_of_measured": achieved / peak_ips if peak_ips else None,
-                         "inst_per_row": FP64_INST_PER_BISECT_ROW[mode],
-                         "rows_per_launch": rows / max(kb_n / args.steps, 1)},
+                         "inst_per_row": {"binary_y": FP64_INST_PER_BISECT_ROW[mode],
+                                          "binary_x": FP64_INST_PER_BISECT_ROW["x"]},
+                         "rows_per_step": {"binary_y": rows, "binary_x": rows_x},
+                         "launches_per_step": kb_n / args.steps},
             "kernels": kt,
             "dd_step_latency_ns": dd_step_ns,
             "gpu_launches": launches,

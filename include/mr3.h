@@ -63,6 +63,7 @@ typedef struct {
     double rho;                  /* clustering: largest cluster / n, in [1/n, 1] */
     double bisect_rows;          /* Sturm-count rows executed (dstqds steps) */
     double rqi_rows;             /* twisted-factorisation rows executed */
+    double bisect_rows_x;        /* Sturm-count rows executed in binary_x (fp64 phase) */
     double t_ms[8];
 } mr3_stats;
 
@@ -77,7 +78,8 @@ enum mr3_param {
     MR3_ELG_MAX = 6,   /* element-growth acceptance k_elg (first pass); default 8 */
     MR3_RTOL = 7,      /* bisection relative tolerance; default 1e-2 * gaptol (L1294-L1295) */
     MR3_GROUPS = 8,    /* lanes per eigenvalue in the multisection (0 = automatic) */
-    MR3_NPARAM = 9
+    MR3_XPHASE = 9,    /* fp64 I/O: approximate eigenvalues in binary_x first (L1064-L1111); 1 */
+    MR3_NPARAM = 10
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

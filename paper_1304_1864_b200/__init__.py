@@ -31,7 +31,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
-          "RTOL": 7, "GROUPS": 8}
+          "RTOL": 7, "GROUPS": 8, "XPHASE": 9}
 ERRORS = {1: "NONFINITE", 2: "CUDA", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 
@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
                 ("rqi_fallbacks", ctypes.c_int32), ("n_blocks", ctypes.c_int32),
                 ("rqi_iters_max", ctypes.c_int32), ("levels", ctypes.c_int32),
                 ("rho", ctypes.c_double), ("bisect_rows", ctypes.c_double),
-                ("rqi_rows", ctypes.c_double), ("t_ms", ctypes.c_double * 8)]
+                ("rqi_rows", ctypes.c_double), ("bisect_rows_x", ctypes.c_double),
+                ("t_ms", ctypes.c_double * 8)]
 
     def asdict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "t_ms"}

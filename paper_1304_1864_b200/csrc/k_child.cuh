@@ -30,7 +30,7 @@ __device__ double dstqds_growth(const double *__restrict__ rep, int64_t n, R tau
 
 template <class R>
 __device__ void dstqds_write(const double *__restrict__ rep, int64_t n, R tau, double pivmin,
-                             double *__restrict__ child) {
+                             double *__restrict__ child, double *__restrict__ childx) {
     R s = neg(tau);
 #pragma unroll 1
     for (int64_t i = 0; i < n; i++) {
@@ -42,7 +42,9 @@ __device__ void dstqds_write(const double *__restrict__ rep, int64_t n, R tau, d
             s = sub(mul(mul(lp, r.l), s), tau);
         }
         R ldp = mul(dp, lp);
-        store_row4<R>(child, i, dp, mul(ldp, lp), lp, ldp);
+        R lldp = mul(ldp, lp);
+        store_row4<R>(child, i, dp, lldp, lp, ldp);
+        reinterpret_cast<double2 *>(childx)[i] = make_double2(hi(dp), hi(lldp));
     }
 }
 
@@ -65,7 +67,8 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
                                               const int32_t *__restrict__ next_active,
                                               const int32_t *__restrict__ cbeg,
                                               const int32_t *__restrict__ cend, int nclus,
-                                              double *child_pool, int64_t pool_stride_rows,
+                                              double *child_pool, double *childx_pool,
+                                              int64_t pool_stride_rows,
                                               double spdiam, double elg1, double elg2,
                                               double pivmin, DevStats *st, double *dbg) {
     const int c = blockIdx.x;
@@ -113,10 +116,12 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     }
     R t = shfl_R<R>(0xffffffffu, tau, win, 32);
     double *child = child_pool + (int64_t)c * pool_stride_rows * 4 * Prec<R>::words;
+    double *childx = childx_pool + (int64_t)c * pool_stride_rows * 2;
     if (lane == win) {
-        dstqds_write<R>(P.rep, P.n, t, pivmin, child);
+        dstqds_write<R>(P.rep, P.n, t, pivmin, child, childx);
         NodeInfo ch = P;
         ch.rep = child;
+        ch.repx = childx;
         R sig = add(mk2<R>(P.sig_hi, P.sig_lo), t);
         ch.sig_hi = hi(sig);
         ch.sig_lo = lo_part(sig);

@@ -16,6 +16,7 @@ namespace mr3 {
 
 struct NodeInfo {
     const double *rep;  // rows of 4 R values {d, lld, l, ld}
+    const double *repx; // M_x: {d, lld} rounded to binary64, 2 per row
     int64_t n;          // rows (irreducible block size)
     int64_t row0;       // first row of the block in T
     double sig_hi, sig_lo;  // accumulated shift sigma (scaled units), Alg.1 l.19/29
@@ -32,7 +33,8 @@ struct Items {  // eigenvalue slots, SoA over the requested index set (+ guards)
 };
 
 struct DevStats {
-    unsigned long long bisect_rows;
+    unsigned long long bisect_rows;    // binary_y Sturm rows
+    unsigned long long bisect_rows_x;  // binary_x Sturm rows (fp64 phase)
     unsigned long long rqi_rows;
     int rqi_fallbacks;
     int rqi_iters_max;
@@ -138,6 +140,28 @@ __device__ __forceinline__ int negcount(const double *__restrict__ rep, int64_t 
     }
     R dp = guard(add(cur.d, s), pivmin);
     cnt += is_neg(dp) ? 1 : 0;
+    return cnt;
+}
+
+// negcount in binary_x arithmetic on the narrowed copy M_x (§3.2,
+// "Arithmetic used to approximate eigenvalues", L1064-L1111)
+__device__ __forceinline__ int negcount_x(const double *__restrict__ repx, int64_t n, double x,
+                                          double pivmin) {
+    double s = -x;
+    int cnt = 0;
+    double2 cur = __ldg(reinterpret_cast<const double2 *>(repx));
+#pragma unroll 1
+    for (int64_t j = 0; j < n - 1; j++) {
+        double2 nxt = __ldg(reinterpret_cast<const double2 *>(repx) + j + 1);
+        double dp = cur.x + s;
+        dp = fabs(dp) < pivmin ? -pivmin : dp;
+        cnt += dp < 0.0 ? 1 : 0;
+        s = fma_rn(cur.y, div(s, dp), -x);
+        cur = nxt;
+    }
+    double dp = cur.x + s;
+    dp = fabs(dp) < pivmin ? -pivmin : dp;
+    cnt += dp < 0.0 ? 1 : 0;
     return cnt;
 }
 
@@ -434,7 +458,8 @@ template <class R, class T>
 __global__ void k_root_factor(const T *__restrict__ d, const T *__restrict__ e,
                               const ChunkDesc *chunks, int nch, const BlockDesc *blocks,
                               double scale, const double *mu, const R *states, int right,
-                              double xi, uint64_t seed, double *rep_pool, int *fail) {
+                              double xi, uint64_t seed, double *rep_pool, double *repx_pool,
+                              int *fail) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nch) return;
     const ChunkDesc ch = chunks[k];
@@ -462,7 +487,9 @@ __global__ void k_root_factor(const T *__restrict__ d, const T *__restrict__ e,
             if (r < b0 + bn - 1) lp = add(lr, mul(lr, xi * uniform_pm1(seed, (uint64_t)r, 1)));
         }
         R ldv = mul(dp, lp);
-        store_row4<R>(rep_pool + r * 4 * Prec<R>::words, 0, dp, mul(ldv, lp), lp, ldv);
+        R lldv = mul(ldv, lp);
+        store_row4<R>(rep_pool + r * 4 * Prec<R>::words, 0, dp, lldv, lp, ldv);
+        reinterpret_cast<double2 *>(repx_pool)[r] = make_double2(hi(dp), hi(lldv));
         dprev = dr;
     }
     if (bad) atomicExch(fail, 1);
@@ -470,11 +497,12 @@ __global__ void k_root_factor(const T *__restrict__ d, const T *__restrict__ e,
 
 template <class R>
 __global__ void k_root_nodes(const BlockDesc *blocks, int nblocks, const double *mu,
-                             double *rep_pool, NodeInfo *nodes) {
+                             double *rep_pool, double *repx_pool, NodeInfo *nodes) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
     NodeInfo ni;
     ni.rep = rep_pool + blocks[b].row0 * 4 * Prec<R>::words;
+    ni.repx = repx_pool + blocks[b].row0 * 2;
     ni.n = blocks[b].n;
     ni.row0 = blocks[b].row0;
     ni.sig_hi = mu[b];

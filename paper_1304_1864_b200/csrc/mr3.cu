@@ -82,9 +82,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0},
 };
 
 #define CK(call)                                                                  \
@@ -178,13 +178,17 @@ struct Work {
     double *rep_pool;
 };
 
+// lanes per eigenvalue of the multisection: enough independent Sturm chains to
+// cover the dependent-step latency (about 16 warps per SM), as few as possible
+// beyond that (a round of G points buys log2(G+1) bits).  A function of the
+// global item count only, so every rank takes the same path (determinism).
 static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
     if (forced > 0) {
         int g = 1;
         while (g * 2 <= forced && g < 32) g *= 2;
         return g;
     }
-    const long long target = (long long)ctx->nsm * 8 * 32;
+    const long long target = (long long)ctx->nsm * 16 * 32;
     int g = 1;
     while (g < 32 && (long long)cnt * g < target) g *= 2;
     return g;
@@ -192,16 +196,23 @@ static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
 
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
-                         double absfloor, int certify) {
+                         double absfloor, int certify, bool xphase, double eps_x) {
     if (cnt <= 0) return 0;
-    const int tpb = 256;
+    const int tpb = 128;
     long long threads = (long long)cnt * G;
     int grid = (int)((threads + tpb - 1) / tpb);
+    const double pivmin_x = 0x1p-900;
     KTime *t = kt_begin(ctx, "k_bisect");
-#define BIS(GG)                                                                                 \
-    case GG:                                                                                    \
-        k_bisect<R, GG><<<grid, tpb, 0, ctx->stream>>>(W.nodes, W.it, list, cnt, rtol, absfloor, \
-                                                       ctx->pivmin, certify, W.st);             \
+#define BIS(GG)                                                                               \
+    case GG:                                                                                  \
+        if (xphase)                                                                           \
+            k_bisect<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                             \
+                W.nodes, W.it, list, cnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x,       \
+                certify, W.st);                                                               \
+        else                                                                                  \
+            k_bisect<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                            \
+                W.nodes, W.it, list, cnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x,       \
+                certify, W.st);                                                               \
         break;
     switch (G) {
         BIS(1)
@@ -328,6 +339,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     blk_chunk0[blocks.size()] = (int)chunks.size();
     const int nch = (int)chunks.size();
     double *rep_pool = (double *)getbuf(ctx, "rep_root", (size_t)n * 4 * words * 8, &rc);
+    double *repx_pool = (double *)getbuf(ctx, "repx_root", (size_t)n * 16, &rc);
     BlockDesc *dblocks = (BlockDesc *)getbuf(ctx, "blocks", blocks.size() * sizeof(BlockDesc), &rc);
     ChunkDesc *dchunks = (ChunkDesc *)getbuf(ctx, "chunks", chunks.size() * sizeof(ChunkDesc), &rc);
     int *dbc0 = (int *)getbuf(ctx, "blk_chunk0", blk_chunk0.size() * 4, &rc);
@@ -364,7 +376,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_root_scan");
         k_root_factor<R, T><<<(nch + 127) / 128, 128, 0, s>>>(d, e, dchunks, nch, dblocks,
                                                                ctx->scale, dmu, dstates, right, xi,
-                                                               seed, rep_pool, dfail);
+                                                               seed, rep_pool, repx_pool, dfail);
         CKL("k_root_factor");
         int hfail = 0;
         CK(cudaMemcpyAsync(&hfail, dfail, 4, cudaMemcpyDeviceToHost, s));
@@ -376,7 +388,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         }
     }
     k_root_nodes<R><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(dblocks, ctx->nblocks, dmu, rep_pool,
-                                                             dnodes);
+                                                             repx_pool, dnodes);
     CKL("k_root_nodes");
     ctx->nodes_used = ctx->nblocks;
 
@@ -480,7 +492,8 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         k_iota<<<(int)((mine + 255) / 256), 256, 0, s>>>(list, (int)mine, (int)first);
         CKL("k_iota");
         ctx->G0 = choose_groups(ctx, cnt, (int)P[MR3_GROUPS]);
-        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0);
+        const bool xphase = words == 2 && P[MR3_XPHASE] != 0;
+        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x);
         if (rc) return rc;
         k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
                                                                     dbrk + 4 * first);
@@ -530,7 +543,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.st = (DevStats *)ctx->bufs["devstats"].p;
     double *dbrk = (double *)ctx->bufs["brk"].p;
     // per-execute counters (bisect_rows of the plan is kept)
-    CK(cudaMemsetAsync((char *)W.st + 8, 0, sizeof(DevStats) - 8, s));
+    CK(cudaMemsetAsync((char *)W.st + 16, 0, sizeof(DevStats) - 16, s));
     if (ctx->world > 1) {
         k_brk_to_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, (int)ctx->slice_cap,
                                                             ctx->world, dbrk);
@@ -815,13 +828,14 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         std::string pname = "child_pool" + std::to_string(level);
         double *pool =
             (double *)getbuf(ctx, pname, (size_t)nclus * ctx->n * 4 * words * 8, &rc);
+        double *poolx = (double *)getbuf(ctx, pname + "x", (size_t)nclus * ctx->n * 16, &rc);
         if (rc) return rc;
         double *cdbg = nullptr;
         if (ctx->debug) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
         k_child<R><<<nclus, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, nxt, cbeg, cend, nclus,
-                                        pool, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st,
-                                        cdbg);
+                                        pool, poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin,
+                                        W.st, cdbg);
         kt_end(ctx, tch);
         CKL("k_child");
         if (ctx->debug) {
@@ -835,7 +849,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         ctx->nodes_used += nclus;
         dump("after child", nxt, nmem, level + 1);
         // K2: refine in the child coordinates (certified)
-        rc = launch_bisect<R>(ctx, W, nxt, nmem, Gc, rtol, absfloor, 1);
+        rc = launch_bisect<R>(ctx, W, nxt, nmem, Gc, rtol, absfloor, 1,
+                              words == 2 && P[MR3_XPHASE] != 0, eps_x);
         if (rc) return rc;
         dump("after refine", nxt, nmem, level + 1);
         // K3: classify the members
@@ -867,6 +882,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     ctx->stats.rqi_fallbacks = hst.rqi_fallbacks;
     ctx->stats.rqi_iters_max = hst.rqi_iters_max;
     ctx->stats.bisect_rows = (double)hst.bisect_rows;
+    ctx->stats.bisect_rows_x = (double)hst.bisect_rows_x;
     ctx->stats.rqi_rows = (double)hst.rqi_rows;
     for (auto &p : ctx->ktimes) {
         const std::string &nm = p.first;
