@@ -127,7 +127,7 @@ __device__ __forceinline__ void certify_bracket(const NodeInfo &nd, R &a, R &b, 
 }
 
 template <class R, int G, bool XPHASE>
-__global__ void __launch_bounds__(256) k_bisect(const NodeInfo *__restrict__ nodes, Items it,
+__global__ void __launch_bounds__(128, 6) k_bisect(const NodeInfo *__restrict__ nodes, Items it,
                                                 const int32_t *__restrict__ list, int cnt,
                                                 double rtol, double absfloor, double pivmin,
                                                 double pivmin_x, double eps_x, int certify,

@@ -11,7 +11,11 @@
 //   gamma_k = s_k + p_k + lam ; r = argmin |gamma_k| (ties: smallest k)
 //   ||z||^2 for twist k = 1 + W_k + V_k with the prefix norms
 //       W_{k+1} = (l+_k)^2 (1 + W_k),  V_{k-1} = (u-_{k-1})^2 (1 + V_k)
-//   (exact identities for z_r = 1, z_i = -l+_i z_{i+1} (i < r), z_{i+1} = -u-_i z_i)
+//   (exact identities for z_r = 1, z_i = -l+_i z_{i+1} (i < r), z_{i+1} = -u-_i z_i),
+//   kept in binary64: they only feed the RQ correction and the stopping test.
+//   The output is normalised with that estimate and the exact ||z|| is summed
+//   (pair arithmetic) while the column is written; k_fixnorm rescales the few
+//   columns whose estimate was off by more than 2^-54.
 //   lam <- lam + gamma_r / ||z||^2          (RQ correction, L714-L717)
 //   stop: |gamma_r|/||z|| <= k_rs gap eps_x sqrt(n)   (Eq. (3.6))
 //         or |gamma_r|/||z||^2 <= 8 eps_y |lam|        (stagnation, L720-L723)
@@ -39,7 +43,9 @@ struct RqiArgs {
     Items it;
     const int32_t *list;
     int cnt;
-    R *ck_s, *ck_W, *ck_p;  // [nblk][S]
+    R *ck_s, *ck_p;         // [nblk][S]
+    double *ck_W;           // [nblk][S]
+    double *fac;            // per local column: 1/||written column|| (fp64 output), 0 = exact
     int64_t S;              // checkpoint stride (threads in this launch)
     double pivmin, krs, eps_x, gaptol;
     int maxit;
@@ -51,18 +57,25 @@ struct RqiArgs {
     DevStats *st;
 };
 
-template <class R>
-__device__ __forceinline__ R clampbig(R x) {
-    return hi(x) > 1e250 ? mk<R>(1e250) : x;
+__device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
+
+// ss += x^2 in pair arithmetic (two-prod + two-sum)
+__device__ __forceinline__ void accum_sq(double x, double &sh, double &sl) {
+    double p = x * x;
+    double pe = fma(x, x, -p);
+    double e;
+    double sn = two_sum(sh, p, e);
+    sl += e + pe;
+    sh = sn;
 }
 
 // F sweep with checkpoints; returns count(lam)
 template <class R>
 __device__ __forceinline__ int rq_forward(const double *__restrict__ rep, int64_t n, R lam,
-                                          double pivmin, R *ck_s, R *ck_W, int64_t S,
+                                          double pivmin, R *ck_s, double *ck_W, int64_t S,
                                           int64_t slot) {
     R s = neg(lam);
-    R W = mk<R>(0.0);
+    double W = 0.0;
     int negc = 0;
 #pragma unroll 1
     for (int64_t b0 = 0; b0 < n; b0 += RQ_C) {
@@ -77,7 +90,8 @@ __device__ __forceinline__ int rq_forward(const double *__restrict__ rep, int64_
                 negc += is_neg(dp) ? 1 : 0;
                 if (k < n - 1) {
                     R lp = div(r.ld, dp);
-                    W = clampbig(mul(mul(lp, lp), add(W, 1.0)));
+                    double l2 = hi(lp) * hi(lp);
+                    W = clampbig(fma(l2, W, l2));
                     s = sub(mul(lp, mul(r.l, s)), lam);
                 }
             }
@@ -89,22 +103,24 @@ __device__ __forceinline__ int rq_forward(const double *__restrict__ rep, int64_
 // B sweep: recompute each forward block, argmin |gamma_k|, norms, p checkpoints
 template <class R>
 __device__ __forceinline__ void rq_backward(const double *__restrict__ rep, int64_t n, R lam,
-                                            double pivmin, const R *ck_s, const R *ck_W, R *ck_p,
-                                            int64_t S, int64_t slot, int64_t &r_out, R &g_out,
-                                            R &nz2_out) {
+                                            double pivmin, const R *ck_s, const double *ck_W,
+                                            R *ck_p, int64_t S, int64_t slot, int64_t &r_out,
+                                            R &g_out, double &nz2_out) {
     Row4<R> rl = load_row4<R>(rep, n - 1);
     R p = sub(rl.d, lam);
-    R V = mk<R>(0.0);
+    double V = 0.0;
     double best = INFINITY;
     int64_t r = n - 1;
-    R gr = mk<R>(0.0), nz2 = mk<R>(1.0);
+    R gr = mk<R>(0.0);
+    double nz2 = 1.0;
     const int64_t nblk = (n + RQ_C - 1) / RQ_C;
 #pragma unroll 1
     for (int64_t blk = nblk - 1; blk >= 0; blk--) {
         const int64_t b0 = blk * RQ_C;
-        R sbuf[RQ_C], wbuf[RQ_C];
+        R sbuf[RQ_C];
+        double wbuf[RQ_C];
         R s = ck_s[blk * S + slot];
-        R W = ck_W[blk * S + slot];
+        double W = ck_W[blk * S + slot];
 #pragma unroll
         for (int j = 0; j < RQ_C; j++) {
             int64_t k = b0 + j;
@@ -114,7 +130,8 @@ __device__ __forceinline__ void rq_backward(const double *__restrict__ rep, int6
                 Row4<R> r4 = load_row4<R>(rep, k);
                 R dp = guard(add(r4.d, s), pivmin);
                 R lp = div(r4.ld, dp);
-                W = clampbig(mul(mul(lp, lp), add(W, 1.0)));
+                double l2 = hi(lp) * hi(lp);
+                W = clampbig(fma(l2, W, l2));
                 s = sub(mul(lp, mul(r4.l, s)), lam);
             }
         }
@@ -129,14 +146,15 @@ __device__ __forceinline__ void rq_backward(const double *__restrict__ rep, int6
                     best = ga;
                     r = k;
                     gr = g;
-                    nz2 = add(add(wbuf[j], V), 1.0);
+                    nz2 = 1.0 + wbuf[j] + V;
                 }
                 if (k > 0) {
                     Row4<R> r4 = load_row4<R>(rep, k - 1);
                     R Dm = guard(add(r4.lld, p), pivmin);
                     R t = div(r4.d, Dm);
-                    R um = mul(r4.l, t);
-                    V = clampbig(mul(mul(um, um), add(V, 1.0)));
+                    double u2 = hi(r4.l) * hi(t);
+                    u2 *= u2;
+                    V = clampbig(fma(u2, V, u2));
                     p = sub(mul(p, t), lam);
                 }
             }
@@ -162,7 +180,8 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
     nd.rep = nullptr;
     nd.row0 = 0;
     int k = 0;
-    R lam = mk<R>(0.0), a = lam, b = lam, gr = lam, nz2 = mk<R>(1.0), lam_out = lam;
+    R lam = mk<R>(0.0), a = lam, b = lam, gr = lam, lam_out = lam;
+    double nz2 = 1.0;
     int64_t r = 0;
     double gap = INFINITY;
     unsigned long long rows = 0;
@@ -183,7 +202,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         if (nd.n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
             lam_out = load_row4<R>(nd.rep, 0).d;
             r = 0;
-            nz2 = mk<R>(1.0);
+            nz2 = 1.0;
             done = true;
             iters = 0;
         }
@@ -198,7 +217,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
             } else {
                 if (lt(a, lam)) a = lam;
             }
-            double g = hi(gr), z2 = hi(nz2);
+            double g = hi(gr), z2 = nz2;
             double corr = g / z2;
             R lam_new = add(lam, mk<R>(corr));
             if (fabs(g) / sqrt(z2) <= tol ||
@@ -231,7 +250,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
             rq_backward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.ck_p, A.S, slot, r, gr,
                            nz2);
             rows += 3 * nd.n;
-            R lam_new = add(lam, mk<R>(hi(gr) / hi(nz2)));
+            R lam_new = add(lam, mk<R>(hi(gr) / nz2));
             lam_out = (lt(a, lam_new) && lt(lam_new, b)) ? lam_new : lam;
             atomicAdd(&A.st->rqi_fallbacks, 1);
             iters = A.maxit + 1;
@@ -265,8 +284,10 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
     __syncthreads();
     const int64_t nmax = s_nmax;
     const bool mine = active && col >= 0;
-    // 1/||z|| in R
-    R inv = div(mk<R>(1.0), sqrt_r(nz2));
+    // 1/||z|| from the binary64 norm estimate; the exact norm of what is written
+    // is summed in pair arithmetic (ss) and checked at the end
+    const double inv = 1.0 / sqrt(nz2);
+    double ss_hi = 0.0, ss_lo = 0.0;
     const double tiny = 1e-250;
     OutT *Zo = reinterpret_cast<OutT *>(A.Z);
     const int warp = tid >> 5, lane = tid & 31;
@@ -313,7 +334,9 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
                             z = neg(mul(lpb[j], z1));
                         }
                         if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
-                        tile[kk - t0][tid] = (OutT)hi(mul(z, inv));
+                        OutT zo = (OutT)hi(mul(z, inv));
+                        tile[kk - t0][tid] = zo;
+                        accum_sq((double)zo, ss_hi, ss_lo);
                         z2 = z1;
                         z1 = z;
                     }
@@ -381,7 +404,9 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
                                     z = neg(mul(uprev, z1));
                                 }
                                 if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
-                                tile[kk - t0][tid] = (OutT)hi(mul(z, inv));
+                                OutT zo = (OutT)hi(mul(z, inv));
+                                tile[kk - t0][tid] = zo;
+                                accum_sq((double)zo, ss_hi, ss_lo);
                                 z2 = z1;
                                 z1 = z;
                             }
@@ -400,7 +425,25 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         }
         if (mine) rows += nd.n - r;
     }
+    if (mine && A.fac) {
+        // exact sum of squares of the written column vs 1 (fp64 output only)
+        double dev = (ss_hi - 1.0) + ss_lo;
+        A.fac[col - A.zcol0] = fabs(dev) > 0x1p-54 ? 1.0 / sqrt(ss_hi + ss_lo) : 0.0;
+    }
     if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
+}
+
+// rescale the columns whose binary64 norm estimate missed by more than 2^-54
+// (one CTA per column; columns with fac == 0 are already unit vectors)
+template <class OutT>
+__global__ void k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols, const double *fac,
+                          const int64_t *row0n /* unused: whole column */, int64_t n) {
+    const int64_t c = blockIdx.x;
+    if (c >= ncols) return;
+    const double f = fac[c];
+    if (f == 0.0) return;
+    OutT *col = Z + c * ldz;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) col[i] = (OutT)((double)col[i] * f);
 }
 
 }  // namespace mr3

@@ -123,43 +123,99 @@ __device__ __forceinline__ R guard(R x, double pivmin) {
 //   s_1 = -x ; d+_j = d_j + s_j ; s_{j+1} = lld_j * (s_j / d+_j) - x
 // ("special forms of ... qd"; Sturm count S:182-188).
 // ---------------------------------------------------------------------------
+constexpr int PF = 4;   // binary_x rows prefetched ahead of the Sturm recurrence (L2 latency)
+constexpr int PFY = 2;  // binary_y rows prefetched ahead (32 B each)
+
 template <class R>
 __device__ __forceinline__ int negcount(const double *__restrict__ rep, int64_t n, R x,
                                         double pivmin) {
     R s = neg(x);
     int cnt = 0;
+    Row2<R> ring[PFY];
+#pragma unroll
+    for (int u = 0; u < PFY; u++) ring[u] = load_row2<R>(rep, u < n ? u : n - 1);
     int64_t j = 0;
-    Row2<R> cur = load_row2<R>(rep, 0);
 #pragma unroll 1
-    for (; j < n - 1; j++) {
-        Row2<R> nxt = load_row2<R>(rep, j + 1);  // prefetch one row ahead
-        R dp = guard(add(cur.d, s), pivmin);
-        cnt += is_neg(dp) ? 1 : 0;
-        s = sub(mul(cur.lld, div(s, dp)), x);
-        cur = nxt;
+    for (; j + PFY <= n - 1; j += PFY) {
+#pragma unroll
+        for (int u = 0; u < PFY; u++) {
+            Row2<R> cur = ring[u];
+            int64_t nx = j + u + PFY;
+            ring[u] = load_row2<R>(rep, nx < n ? nx : n - 1);
+            R dp = guard(add(cur.d, s), pivmin);
+            cnt += is_neg(dp) ? 1 : 0;
+            s = sub(mul(cur.lld, div(s, dp)), x);
+        }
     }
-    R dp = guard(add(cur.d, s), pivmin);
+    // tail rows j .. n-2 (fewer than PFY), then the last pivot
+#pragma unroll
+    for (int u = 0; u < PFY; u++) {
+        if (j + u < n - 1) {
+            Row2<R> cur = ring[u];
+            R dp = guard(add(cur.d, s), pivmin);
+            cnt += is_neg(dp) ? 1 : 0;
+            s = sub(mul(cur.lld, div(s, dp)), x);
+        }
+    }
+    Row2<R> last = load_row2<R>(rep, n - 1);
+    R dp = guard(add(last.d, s), pivmin);
     cnt += is_neg(dp) ? 1 : 0;
     return cnt;
 }
 
 // negcount in binary_x arithmetic on the narrowed copy M_x (§3.2,
-// "Arithmetic used to approximate eigenvalues", L1064-L1111)
+// "Arithmetic used to approximate eigenvalues", L1064-L1111).
+// Fast path per row: d+ = d + s ; count the sign bit ; s = (lld s) * rcp(d+) - x
+// (lld*s is off the dependency chain; rcp to 1 ulp).  No pivot guard: a zero
+// (or subnormal) pivot turns s into NaN, which is checked once per PF rows and
+// the block is then redone with the guard |d+| < pivmin -> -pivmin.
+__device__ __forceinline__ int sign_bit(double v) {
+    return (int)((unsigned)__double2hiint(v) >> 31);
+}
+__device__ __forceinline__ void nc_row_guarded(double d, double lld, double x, double pivmin,
+                                               double &s, int &cnt) {
+    double dp = d + s;
+    dp = fabs(dp) < pivmin ? -pivmin : dp;
+    cnt += dp < 0.0 ? 1 : 0;
+    s = fma_rn(lld * s, rcp(dp), -x);
+}
 __device__ __forceinline__ int negcount_x(const double *__restrict__ repx, int64_t n, double x,
                                           double pivmin) {
+    const double2 *rx = reinterpret_cast<const double2 *>(repx);
     double s = -x;
     int cnt = 0;
-    double2 cur = __ldg(reinterpret_cast<const double2 *>(repx));
+    double2 ring[PF];
+#pragma unroll
+    for (int u = 0; u < PF; u++) ring[u] = __ldg(rx + (u < n ? u : n - 1));
+    int64_t j = 0;
 #pragma unroll 1
-    for (int64_t j = 0; j < n - 1; j++) {
-        double2 nxt = __ldg(reinterpret_cast<const double2 *>(repx) + j + 1);
-        double dp = cur.x + s;
-        dp = fabs(dp) < pivmin ? -pivmin : dp;
-        cnt += dp < 0.0 ? 1 : 0;
-        s = fma_rn(cur.y, div(s, dp), -x);
-        cur = nxt;
+    for (; j + PF <= n - 1; j += PF) {
+        const double s0 = s;
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < PF; u++) {
+            const double2 cur = ring[u];
+            int64_t nx = j + u + PF;
+            ring[u] = __ldg(rx + (nx < n ? nx : n - 1));
+            double dp = cur.x + s;
+            c += sign_bit(dp);
+            s = fma_rn(cur.y * s, rcp(dp), -x);
+        }
+        if (isnan(s)) {  // a (near-)zero pivot in this block: redo it guarded (rare)
+            s = s0;
+            c = 0;
+            for (int u = 0; u < PF; u++) {
+                const double2 cur = __ldg(rx + j + u);
+                nc_row_guarded(cur.x, cur.y, x, pivmin, s, c);
+            }
+        }
+        cnt += c;
     }
-    double dp = cur.x + s;
+#pragma unroll
+    for (int u = 0; u < PF; u++)
+        if (j + u < n - 1) nc_row_guarded(ring[u].x, ring[u].y, x, pivmin, s, cnt);
+    double2 last = __ldg(rx + (n - 1));
+    double dp = last.x + s;
     dp = fabs(dp) < pivmin ? -pivmin : dp;
     cnt += dp < 0.0 ? 1 : 0;
     return cnt;

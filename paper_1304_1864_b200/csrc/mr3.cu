@@ -707,30 +707,37 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         CK(cudaMemset2DAsync(Z, ldz * sizeof(OutT), 0, ctx->n * sizeof(OutT), c1 - c0, s));
     }
 
-    // RQI scratch sizing
+    // RQI scratch sizing: checkpoints of (s, W, p) every RQ_C rows per eigenpair
     size_t freeb = 0, totb = 0;
     cudaMemGetInfo(&freeb, &totb);
     const int64_t nmaxb = ctx->n;
     const int64_t nblk = (nmaxb + RQ_C - 1) / RQ_C;
     size_t budget = std::min<size_t>((size_t)(freeb * 0.6), (size_t)48 << 30);
-    int64_t per_thread = nblk * 3 * (int64_t)sizeof(R);
+    int64_t per_thread = nblk * (2 * (int64_t)sizeof(R) + 8);
     int64_t Smax = std::max<int64_t>(RQ_TPB, (int64_t)(budget / std::max<int64_t>(per_thread, 1)));
     Smax = (Smax / RQ_TPB) * RQ_TPB;
+    double *dfac = nullptr;
+    if (jobz == 'V' && sizeof(OutT) == 8 && c1 > c0) {
+        dfac = (double *)getbuf(ctx, "fac", (size_t)(c1 - c0) * 8, &rc);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(dfac, 0, (size_t)(c1 - c0) * 8, s));
+    }
 
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
         for (int off = 0; off < ncount;) {
             int64_t S = std::min<int64_t>(Smax, ((ncount - off + RQ_TPB - 1) / RQ_TPB) * RQ_TPB);
             int rc2 = 0;
-            R *ck = (R *)getbuf(ctx, "rqi_ck", (size_t)(3 * nblk * S) * sizeof(R), &rc2);
+            char *ck = (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc2);
             if (rc2) return rc2;
             RqiArgs<R> A;
             A.nodes = W.nodes;
             A.it = W.it;
             A.list = list + off;
             A.cnt = (int)std::min<int64_t>(S, ncount - off);
-            A.ck_s = ck;
-            A.ck_W = ck + nblk * S;
-            A.ck_p = ck + 2 * nblk * S;
+            A.ck_s = (R *)ck;
+            A.ck_p = (R *)(ck + nblk * S * sizeof(R));
+            A.ck_W = (double *)(ck + 2 * nblk * S * sizeof(R));
+            A.fac = dfac;
             A.S = S;
             A.pivmin = ctx->pivmin;
             A.krs = P[MR3_KRS];
@@ -869,6 +876,12 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if (ctx->debug)
             fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
                     nclus, nmem);
+    }
+    if (dfac) {
+        KTime *tf = kt_begin(ctx, "k_fixnorm");
+        k_fixnorm<OutT><<<(unsigned)(c1 - c0), 256, 0, s>>>(Z, ldz, c1 - c0, dfac, nullptr, ctx->n);
+        kt_end(ctx, tf);
+        CKL("k_fixnorm");
     }
     ctx->stats.d_max = level;
     DevStats hst;
