@@ -3,7 +3,13 @@
 // coalesced store of the Z column (Alg. 1 l.11-12, PAPER.md L652-L727,
 // L1140-L1173; memory contract L1199-L1226).
 //
-// One thread per eigenpair.  Iteration j at shift lam:
+// One thread per eigenpair; every CTA holds eigenpairs of ONE representation
+// (the host groups the singletons by node), so the rows of that representation
+// are staged through shared memory: tiles of RQ_TR rows (plus a halo below) are
+// loaded cooperatively with cp.async into a double buffer while the previous
+// tile is consumed, and all four sweeps read their rows from smem.
+//
+// Iteration j at shift lam:
 //   F (stationary, top-down):   s_1 = -lam ; d+_i = d_i + s_i ; l+_i = ld_i / d+_i ;
 //                               s_{i+1} = l+_i l_i s_i - lam ; count #{d+_i < 0}
 //   B (progressive, bottom-up): p_n = d_n - lam ; D-_{i+1} = lld_i + p_{i+1} ;
@@ -13,9 +19,6 @@
 //       W_{k+1} = (l+_k)^2 (1 + W_k),  V_{k-1} = (u-_{k-1})^2 (1 + V_k)
 //   (exact identities for z_r = 1, z_i = -l+_i z_{i+1} (i < r), z_{i+1} = -u-_i z_i),
 //   kept in binary64: they only feed the RQ correction and the stopping test.
-//   The output is normalised with that estimate and the exact ||z|| is summed
-//   (pair arithmetic) while the column is written; k_fixnorm rescales the few
-//   columns whose estimate was off by more than 2^-54.
 //   lam <- lam + gamma_r / ||z||^2          (RQ correction, L714-L717)
 //   stop: |gamma_r|/||z|| <= k_rs gap eps_x sqrt(n)   (Eq. (3.6))
 //         or |gamma_r|/||z||^2 <= 8 eps_y |lam|        (stagnation, L720-L723)
@@ -23,30 +26,41 @@
 // iterate leaving it is replaced by the bracket midpoint (RQI "guarded by
 // bisection", L315); after max_rqi iterations: bisection to relative
 // eps_x sqrt(n) gaptol and one more twisted solve (L1154-L1163).
+// The output is normalised with the binary64 norm estimate and the exact norm
+// of what is written is summed in pair arithmetic; k_fixnorm rescales the few
+// columns whose estimate was off by more than 2^-54.
 //
 // Storage: the forward state (s, W) and backward state p are checkpointed every
-// C rows (6 B/row/eigenpair in dd) instead of storing whole sweeps; each block
-// of C rows is recomputed into registers when a sweep needs it in the other
-// direction (SURVEY.md §7 hard part 2, option (c)).
+// RQ_C rows (5 B/row/eigenpair in dd) instead of storing whole sweeps; each
+// block of RQ_C rows is recomputed into registers when a sweep needs it in the
+// other direction (SURVEY.md §7 hard part 2, option (c)).
 #pragma once
 #include "k_bisect.cuh"
 
 namespace mr3 {
 
-constexpr int RQ_C = 8;     // checkpoint block (rows)
-constexpr int RQ_TR = 32;   // output tile rows (4 checkpoint blocks)
-constexpr int RQ_TPB = 128; // threads per CTA
+constexpr int RQ_C = 8;      // checkpoint block (rows)
+constexpr int RQ_TR = 32;    // rows per staged tile = output tile rows (4 blocks)
+constexpr int RQ_HALO = 8;   // rows staged below a tile (the sweeps need row t0 - 1)
+constexpr int RQ_TPB = 128;  // threads per CTA
+
+struct RqiTask {
+    int32_t first;  // offset into the singleton list
+    int32_t cnt;    // eigenpairs (<= RQ_TPB)
+    int32_t node;
+    int32_t pad;
+};
 
 template <class R>
 struct RqiArgs {
     const NodeInfo *nodes;
     Items it;
-    const int32_t *list;
-    int cnt;
-    R *ck_s, *ck_p;         // [nblk][S]
-    double *ck_W;           // [nblk][S]
-    double *fac;            // per local column: 1/||written column|| (fp64 output), 0 = exact
-    int64_t S;              // checkpoint stride (threads in this launch)
+    const int32_t *list;   // singleton item ids
+    const RqiTask *tasks;  // one per CTA
+    R *ck_s, *ck_p;        // [nblk][S]
+    double *ck_W;          // [nblk][S]
+    double *fac;           // per local column: 1/||written column|| (fp64 output), 0 = exact
+    int64_t S;             // checkpoint stride (CTAs in this launch * RQ_TPB)
     double pivmin, krs, eps_x, gaptol;
     int maxit;
     int jobz_v;
@@ -69,195 +83,276 @@ __device__ __forceinline__ void accum_sq(double x, double &sh, double &sl) {
     sh = sn;
 }
 
-// F sweep with checkpoints; returns count(lam)
-template <class R>
-__device__ __forceinline__ int rq_forward(const double *__restrict__ rep, int64_t n, R lam,
-                                          double pivmin, R *ck_s, double *ck_W, int64_t S,
-                                          int64_t slot) {
-    R s = neg(lam);
-    double W = 0.0;
-    int negc = 0;
-#pragma unroll 1
-    for (int64_t b0 = 0; b0 < n; b0 += RQ_C) {
-        ck_s[(b0 / RQ_C) * S + slot] = s;
-        ck_W[(b0 / RQ_C) * S + slot] = W;
-#pragma unroll
-        for (int j = 0; j < RQ_C; j++) {
-            int64_t k = b0 + j;
-            if (k < n) {
-                Row4<R> r = load_row4<R>(rep, k);
-                R dp = guard(add(r.d, s), pivmin);
-                negc += is_neg(dp) ? 1 : 0;
-                if (k < n - 1) {
-                    R lp = div(r.ld, dp);
-                    double l2 = hi(lp) * hi(lp);
-                    W = clampbig(fma(l2, W, l2));
-                    s = sub(mul(lp, mul(r.l, s)), lam);
-                }
-            }
-        }
-    }
-    return negc;
+// ---------------------------------------------------------------- staging
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// B sweep: recompute each forward block, argmin |gamma_k|, norms, p checkpoints
 template <class R>
-__device__ __forceinline__ void rq_backward(const double *__restrict__ rep, int64_t n, R lam,
-                                            double pivmin, const R *ck_s, const double *ck_W,
-                                            R *ck_p, int64_t S, int64_t slot, int64_t &r_out,
-                                            R &g_out, double &nz2_out) {
-    Row4<R> rl = load_row4<R>(rep, n - 1);
-    R p = sub(rl.d, lam);
-    double V = 0.0;
-    double best = INFINITY;
-    int64_t r = n - 1;
-    R gr = mk<R>(0.0);
-    double nz2 = 1.0;
-    const int64_t nblk = (n + RQ_C - 1) / RQ_C;
-#pragma unroll 1
-    for (int64_t blk = nblk - 1; blk >= 0; blk--) {
-        const int64_t b0 = blk * RQ_C;
-        R sbuf[RQ_C];
-        double wbuf[RQ_C];
-        R s = ck_s[blk * S + slot];
-        double W = ck_W[blk * S + slot];
-#pragma unroll
-        for (int j = 0; j < RQ_C; j++) {
-            int64_t k = b0 + j;
-            sbuf[j] = s;
-            wbuf[j] = W;
-            if (k < n - 1) {
-                Row4<R> r4 = load_row4<R>(rep, k);
-                R dp = guard(add(r4.d, s), pivmin);
-                R lp = div(r4.ld, dp);
-                double l2 = hi(lp) * hi(lp);
-                W = clampbig(fma(l2, W, l2));
-                s = sub(mul(lp, mul(r4.l, s)), lam);
-            }
-        }
-#pragma unroll
-        for (int j = RQ_C - 1; j >= 0; j--) {
-            int64_t k = b0 + j;
-            if (k < n) {
-                if (j == 0) ck_p[blk * S + slot] = p;  // p at the block start
-                R g = add(add(sbuf[j], p), lam);
-                double ga = fabs(hi(g));
-                if (ga <= best) {
-                    best = ga;
-                    r = k;
-                    gr = g;
-                    nz2 = 1.0 + wbuf[j] + V;
-                }
-                if (k > 0) {
-                    Row4<R> r4 = load_row4<R>(rep, k - 1);
-                    R Dm = guard(add(r4.lld, p), pivmin);
-                    R t = div(r4.d, Dm);
-                    double u2 = hi(r4.l) * hi(t);
-                    u2 *= u2;
-                    V = clampbig(fma(u2, V, u2));
-                    p = sub(mul(p, t), lam);
-                }
-            }
-        }
+struct Stage {
+    static constexpr int ROWD = 4 * Prec<R>::words;  // doubles per row
+    static constexpr int ROWS = RQ_TR + RQ_HALO;     // staged rows per tile
+    static constexpr int TILE = ROWS * ROWD;         // doubles per tile buffer
+};
+
+// rows [t0 - HALO, t0 + TR) of rep (clamped to [0, n)) -> buf, asynchronously
+template <class R>
+__device__ __forceinline__ void stage_tile(double *buf, const double *rep, int64_t n, int64_t t0) {
+    constexpr int ROWD = Stage<R>::ROWD;
+    constexpr int CH = Stage<R>::ROWS * ROWD / 2;  // 16-byte chunks
+    for (int c = threadIdx.x; c < CH; c += RQ_TPB) {
+        int r = c / (ROWD / 2), off = (c % (ROWD / 2)) * 2;
+        int64_t g = t0 - RQ_HALO + r;
+        g = g < 0 ? 0 : (g >= n ? n - 1 : g);
+        cp_async16(buf + r * ROWD + off, rep + g * ROWD + off);
     }
-    r_out = r;
-    g_out = gr;
-    nz2_out = nz2;
+    cp_async_commit();
 }
 
+template <class R>
+__device__ __forceinline__ Row4<R> srow(const double *buf, int64_t t0, int64_t k);
+template <>
+__device__ __forceinline__ Row4<dd> srow<dd>(const double *buf, int64_t t0, int64_t k) {
+    const double2 *p = reinterpret_cast<const double2 *>(buf + (k - t0 + RQ_HALO) * 8);
+    double2 a = p[0], b = p[1], c = p[2], d = p[3];
+    Row4<dd> r;
+    r.d = mkdd(a.x, a.y);
+    r.lld = mkdd(b.x, b.y);
+    r.l = mkdd(c.x, c.y);
+    r.ld = mkdd(d.x, d.y);
+    return r;
+}
+template <>
+__device__ __forceinline__ Row4<double> srow<double>(const double *buf, int64_t t0, int64_t k) {
+    const double2 *p = reinterpret_cast<const double2 *>(buf + (k - t0 + RQ_HALO) * 4);
+    double2 a = p[0], b = p[1];
+    Row4<double> r;
+    r.d = a.x;
+    r.lld = a.y;
+    r.l = b.x;
+    r.ld = b.y;
+    return r;
+}
+
+// Run body(buf, t0) over all row tiles of the representation, ascending or
+// descending, with the next tile's rows in flight while the current one is used.
+// Every thread of the CTA must call this (barriers inside).
+template <class R, class Body>
+__device__ __forceinline__ void staged_pass(double *smem, const double *rep, int64_t n, bool desc,
+                                            Body body) {
+    constexpr int TILE = Stage<R>::TILE;
+    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+    auto t0_of = [&](int i) -> int64_t { return (int64_t)(desc ? ntile - 1 - i : i) * RQ_TR; };
+    stage_tile<R>(smem, rep, n, t0_of(0));
+    for (int i = 0; i < ntile; i++) {
+        if (i + 1 < ntile) {
+            stage_tile<R>(smem + ((i + 1) & 1) * TILE, rep, n, t0_of(i + 1));
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        body(smem + (i & 1) * TILE, t0_of(i));
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- kernel
 template <class R, class OutT>
 __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
+    __shared__ __align__(16) double sstage[2 * Stage<R>::TILE];
     __shared__ OutT tile[RQ_TR][RQ_TPB + 1];
-    __shared__ int64_t s_r[RQ_TPB], s_n[RQ_TPB], s_row0[RQ_TPB], s_col[RQ_TPB];
-    __shared__ int64_t s_nmax;
+    __shared__ int64_t s_r[RQ_TPB], s_col[RQ_TPB];
 
     const int tid = threadIdx.x;
+    const RqiTask task = A.tasks[blockIdx.x];
+    const NodeInfo nd = A.nodes[task.node];
+    const int64_t n = nd.n;
     const int64_t slot = (int64_t)blockIdx.x * RQ_TPB + tid;
-    const bool active = slot < A.cnt;
-    int id = -1;
-    NodeInfo nd;
-    nd.n = 0;
-    nd.rep = nullptr;
-    nd.row0 = 0;
-    int k = 0;
+    const bool active = tid < task.cnt;
+    int id = -1, k = 0;
     R lam = mk<R>(0.0), a = lam, b = lam, gr = lam, lam_out = lam;
-    double nz2 = 1.0;
+    double nz2 = 1.0, gap = INFINITY;
     int64_t r = 0;
-    double gap = INFINITY;
     unsigned long long rows = 0;
     int iters = 0;
-    bool fallback = false;
-
+    bool done = !active;
     if (active) {
-        id = A.list[slot];
-        nd = A.nodes[A.it.node[id]];
+        id = A.list[task.first + tid];
         k = A.it.k[id];
         a = reinterpret_cast<const R *>(A.it.lo)[id];
         b = reinterpret_cast<const R *>(A.it.hi)[id];
         lam = half(add(a, b));
         gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
-        const double tol = A.krs * gap * A.eps_x * sqrt((double)nd.n);
-        bool done = false;
-        if (nd.n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
+        if (n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
             lam_out = load_row4<R>(nd.rep, 0).d;
-            r = 0;
-            nz2 = 1.0;
             done = true;
-            iters = 0;
         }
+    }
+    const double tol = A.krs * gap * A.eps_x * sqrt((double)n);
+
+    // one twisted factorization at lam for the threads with `need`
+    auto twisted = [&](bool need) -> int {
+        // F: top-down, checkpoints (s, W) at every block start
+        R s = neg(lam);
+        double W = 0.0;
+        int negc = 0;
+        staged_pass<R>(sstage, nd.rep, n, false, [&](const double *buf, int64_t t0) {
+            if (!need) return;
+#pragma unroll
+            for (int q = 0; q < RQ_TR / RQ_C; q++) {
+                const int64_t b0 = t0 + q * RQ_C;
+                if (b0 < n) {
+                    A.ck_s[(b0 / RQ_C) * A.S + slot] = s;
+                    A.ck_W[(b0 / RQ_C) * A.S + slot] = W;
+                }
+#pragma unroll
+                for (int j = 0; j < RQ_C; j++) {
+                    const int64_t kk = b0 + j;
+                    if (kk < n) {
+                        Row4<R> rw = srow<R>(buf, t0, kk);
+                        R dp = guard(add(rw.d, s), A.pivmin);
+                        negc += is_neg(dp) ? 1 : 0;
+                        if (kk < n - 1) {
+                            R lp = div(rw.ld, dp);
+                            double l2 = hi(lp) * hi(lp);
+                            W = clampbig(fma(l2, W, l2));
+                            s = sub(mul(lp, mul(rw.l, s)), lam);
+                        }
+                    }
+                }
+            }
+        });
+        // B: bottom-up, argmin |gamma_k|, p checkpoints
+        R p = mk<R>(0.0);
+        double V = 0.0, best = INFINITY;
+        int64_t rr = n - 1;
+        R g_r = mk<R>(0.0);
+        double z2 = 1.0;
+        if (need) p = sub(load_row4<R>(nd.rep, n - 1).d, lam);
+        staged_pass<R>(sstage, nd.rep, n, true, [&](const double *buf, int64_t t0) {
+            if (!need) return;
 #pragma unroll 1
-        for (iters = 1; !done && iters <= A.maxit; iters++) {
-            int c = rq_forward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.S, slot);
-            rq_backward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.ck_p, A.S, slot, r, gr,
-                           nz2);
-            rows += 3 * nd.n;
+            for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
+                const int64_t b0 = t0 + q * RQ_C;
+                if (b0 >= n) continue;
+                const int64_t blk = b0 / RQ_C;
+                R sb[RQ_C];
+                double wb[RQ_C];
+                R s2 = A.ck_s[blk * A.S + slot];
+                double W2 = A.ck_W[blk * A.S + slot];
+#pragma unroll
+                for (int j = 0; j < RQ_C; j++) {
+                    const int64_t kk = b0 + j;
+                    sb[j] = s2;
+                    wb[j] = W2;
+                    if (kk < n - 1) {
+                        Row4<R> rw = srow<R>(buf, t0, kk);
+                        R dp = guard(add(rw.d, s2), A.pivmin);
+                        R lp = div(rw.ld, dp);
+                        double l2 = hi(lp) * hi(lp);
+                        W2 = clampbig(fma(l2, W2, l2));
+                        s2 = sub(mul(lp, mul(rw.l, s2)), lam);
+                    }
+                }
+#pragma unroll
+                for (int j = RQ_C - 1; j >= 0; j--) {
+                    const int64_t kk = b0 + j;
+                    if (kk < n) {
+                        if (j == 0) A.ck_p[blk * A.S + slot] = p;  // p at the block start
+                        R g = add(add(sb[j], p), lam);
+                        double ga = fabs(hi(g));
+                        if (ga <= best) {
+                            best = ga;
+                            rr = kk;
+                            g_r = g;
+                            z2 = 1.0 + wb[j] + V;
+                        }
+                        if (kk > 0) {
+                            Row4<R> rw = srow<R>(buf, t0, kk - 1);
+                            R Dm = guard(add(rw.lld, p), A.pivmin);
+                            R t = div(rw.d, Dm);
+                            double u2 = hi(rw.l) * hi(t);
+                            u2 *= u2;
+                            V = clampbig(fma(u2, V, u2));
+                            p = sub(mul(p, t), lam);
+                        }
+                    }
+                }
+            }
+        });
+        if (need) {
+            r = rr;
+            gr = g_r;
+            nz2 = z2;
+            rows += 3 * n;
+        }
+        return negc;
+    };
+
+#pragma unroll 1
+    for (iters = 1; iters <= A.maxit; iters++) {
+        const bool need = !done;
+        if (!__syncthreads_or(need)) break;
+        int c = twisted(need);
+        if (need) {
             if (c >= k) {
                 if (lt(lam, b)) b = lam;
             } else {
                 if (lt(a, lam)) a = lam;
             }
-            double g = hi(gr), z2 = nz2;
-            double corr = g / z2;
+            double g = hi(gr);
+            double corr = g / nz2;
             R lam_new = add(lam, mk<R>(corr));
-            if (fabs(g) / sqrt(z2) <= tol ||
-                fabs(corr) <= 8.0 * Prec<R>::eps * fabs(hi(lam)) || g == 0.0) {
+            if (fabs(g) / sqrt(nz2) <= tol || fabs(corr) <= 8.0 * Prec<R>::eps * fabs(hi(lam)) ||
+                g == 0.0) {
                 lam_out = lam_new;
                 done = true;
-                break;
+            } else {
+                if (!(lt(a, lam_new) && lt(lam_new, b))) lam_new = half(add(a, b));
+                lam = lam_new;
             }
-            if (!(lt(a, lam_new) && lt(lam_new, b))) lam_new = half(add(a, b));
-            lam = lam_new;
         }
-        if (!done && nd.n > 1) {
-            // fallback: bisection to relative eps_x sqrt(n) gaptol, one more solve
-            fallback = true;
-            double rtol = A.eps_x * sqrt((double)nd.n) * A.gaptol;
+    }
+    // fallback: bisection to relative eps_x sqrt(n) gaptol, then one more solve
+    const bool fb = !done;
+    if (__syncthreads_or(fb)) {
+        if (fb) {
+            double rtol = A.eps_x * sqrt((double)n) * A.gaptol;
 #pragma unroll 1
             for (int it2 = 0; it2 < 400; it2++) {
                 R w = sub(b, a);
                 if (hi(w) <= fmax(2.0 * rtol * fmax(fabs(hi(a)), fabs(hi(b))), 1e-300)) break;
                 R mid = half(add(a, b));
                 if (!(lt(a, mid) && lt(mid, b))) break;
-                if (negcount<R>(nd.rep, nd.n, mid, A.pivmin) >= k)
+                if (negcount<R>(nd.rep, n, mid, A.pivmin) >= k)
                     b = mid;
                 else
                     a = mid;
-                rows += nd.n;
+                rows += n;
             }
             lam = half(add(a, b));
-            rq_forward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.S, slot);
-            rq_backward<R>(nd.rep, nd.n, lam, A.pivmin, A.ck_s, A.ck_W, A.ck_p, A.S, slot, r, gr,
-                           nz2);
-            rows += 3 * nd.n;
+        }
+        twisted(fb);
+        if (fb) {
             R lam_new = add(lam, mk<R>(hi(gr) / nz2));
             lam_out = (lt(a, lam_new) && lt(lam_new, b)) ? lam_new : lam;
             atomicAdd(&A.st->rqi_fallbacks, 1);
             iters = A.maxit + 1;
         }
+    }
+    int64_t col = -1;
+    if (active) {
         // eigenvalue output: w = (lambda[M] + sigma) * 2^-scale  (Alg. 1 l.12)
         R lt_ = add(lam_out, mk2<R>(nd.sig_hi, nd.sig_lo));
-        int64_t col = A.it.col[id];
+        col = A.it.col[id];
         if (col >= 0) {
             if (sizeof(OutT) == 4)
                 reinterpret_cast<float *>(A.w)[col] = (float)(hi(lt_) * A.unscale);
@@ -273,63 +368,51 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
     }
 
     // ---------------- final stage: z from the twisted factorization at lam -----
-    int64_t col = active ? A.it.col[id] : -1;
-    s_r[tid] = r;
-    s_n[tid] = active ? nd.n : 0;
-    s_row0[tid] = nd.row0;
-    s_col[tid] = col - A.zcol0;
-    if (tid == 0) s_nmax = 0;
-    __syncthreads();
-    if (active && col >= 0) atomicMax((unsigned long long *)&s_nmax, (unsigned long long)nd.n);
-    __syncthreads();
-    const int64_t nmax = s_nmax;
     const bool mine = active && col >= 0;
-    // 1/||z|| from the binary64 norm estimate; the exact norm of what is written
-    // is summed in pair arithmetic (ss) and checked at the end
+    s_r[tid] = mine ? r : -1;
+    s_col[tid] = mine ? col - A.zcol0 : -1;
     const double inv = 1.0 / sqrt(nz2);
     double ss_hi = 0.0, ss_lo = 0.0;
     const double tiny = 1e-250;
     OutT *Zo = reinterpret_cast<OutT *>(A.Z);
     const int warp = tid >> 5, lane = tid & 31;
+    __syncthreads();
 
-    // D sweep: rows k <= r, top-down tiles from the last one, z_r = 1,
-    // z_k = -l+_k z_{k+1}  (z_k = -(ld_{k+1}/ld_k) z_{k+2} if z_{k+1} == 0)
+    // D sweep: rows k <= r, top-down, z_r = 1, z_k = -l+_k z_{k+1}
+    // (z_k = -(ld_{k+1}/ld_k) z_{k+2} if z_{k+1} == 0)
     {
-        R z1 = mk<R>(0.0), z2 = mk<R>(0.0);  // z_{k+1}, z_{k+2}
-        const int64_t ntile = (nmax + RQ_TR - 1) / RQ_TR;
-#pragma unroll 1
-        for (int64_t tt = ntile - 1; tt >= 0; tt--) {
-            const int64_t t0 = tt * RQ_TR;
+        R z1 = mk<R>(0.0), z2v = mk<R>(0.0);  // z_{k+1}, z_{k+2}
+        R ldn = mk<R>(0.0);                   // ld_{k+1}
+        staged_pass<R>(sstage, nd.rep, n, true, [&](const double *buf, int64_t t0) {
             if (mine && t0 <= r) {
 #pragma unroll 1
                 for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
                     const int64_t b0 = t0 + q * RQ_C;
-                    if (b0 > r || b0 >= nd.n) continue;
+                    if (b0 > r || b0 >= n) continue;
                     R lpb[RQ_C];
                     R s = A.ck_s[(b0 / RQ_C) * A.S + slot];
 #pragma unroll
                     for (int j = 0; j < RQ_C; j++) {
-                        int64_t kk = b0 + j;
+                        const int64_t kk = b0 + j;
                         lpb[j] = mk<R>(0.0);
-                        if (kk < nd.n - 1 && kk < r) {
-                            Row4<R> r4 = load_row4<R>(nd.rep, kk);
-                            R dp = guard(add(r4.d, s), A.pivmin);
-                            R lp = div(r4.ld, dp);
+                        if (kk < n - 1 && kk < r) {
+                            Row4<R> rw = srow<R>(buf, t0, kk);
+                            R dp = guard(add(rw.d, s), A.pivmin);
+                            R lp = div(rw.ld, dp);
                             lpb[j] = lp;
-                            s = sub(mul(lp, mul(r4.l, s)), lam);
+                            s = sub(mul(lp, mul(rw.l, s)), lam);
                         }
                     }
 #pragma unroll
                     for (int j = RQ_C - 1; j >= 0; j--) {
-                        int64_t kk = b0 + j;
-                        if (kk > r || kk >= nd.n) continue;
+                        const int64_t kk = b0 + j;
+                        if (kk > r || kk >= n) continue;
+                        Row4<R> rw = srow<R>(buf, t0, kk);
                         R z;
                         if (kk == r) {
                             z = mk<R>(1.0);
-                        } else if (hi(z1) == 0.0 && fabs(hi(z2)) > tiny) {
-                            Row4<R> ra = load_row4<R>(nd.rep, kk);
-                            Row4<R> rb = load_row4<R>(nd.rep, kk + 1);
-                            z = neg(mul(div(rb.ld, ra.ld), z2));
+                        } else if (hi(z1) == 0.0 && fabs(hi(z2v)) > tiny) {
+                            z = neg(mul(div(ldn, rw.ld), z2v));
                         } else {
                             z = neg(mul(lpb[j], z1));
                         }
@@ -337,79 +420,82 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
                         OutT zo = (OutT)hi(mul(z, inv));
                         tile[kk - t0][tid] = zo;
                         accum_sq((double)zo, ss_hi, ss_lo);
-                        z2 = z1;
+                        z2v = z1;
                         z1 = z;
+                        ldn = rw.ld;
                     }
                 }
             }
             __syncthreads();
             for (int c = warp; c < RQ_TPB; c += RQ_TPB / 32) {
                 const int64_t row = t0 + lane;
-                if (s_col[c] >= 0 && s_n[c] > 0 && row < s_n[c] && row <= s_r[c])
-                    Zo[(s_row0[c] + row) + s_col[c] * A.ldz] = tile[lane][c];
+                if (s_col[c] >= 0 && row < n && row <= s_r[c])
+                    Zo[(nd.row0 + row) + s_col[c] * A.ldz] = tile[lane][c];
             }
-            __syncthreads();
-        }
+        });
         if (mine) rows += r + 1;
     }
-    // U sweep: rows k > r, bottom-up tiles, z_k = -u-_{k-1} z_{k-1}
+    // U sweep: rows k > r, bottom-up, z_k = -u-_{k-1} z_{k-1}
     // (z_k = -(ld_{k-2}/ld_{k-1}) z_{k-2} if z_{k-1} == 0)
     {
-        R z1 = mk<R>(0.0), z2 = mk<R>(0.0);  // z_{k-1}, z_{k-2}
-        R ucarry = mk<R>(0.0);              // u-_{b0-1}
-        const int64_t ntile = (nmax + RQ_TR - 1) / RQ_TR;
-#pragma unroll 1
-        for (int64_t tt = 0; tt < ntile; tt++) {
-            const int64_t t0 = tt * RQ_TR;
+        R z1 = mk<R>(0.0), z2v = mk<R>(0.0);     // z_{k-1}, z_{k-2}
+        R ldm1 = mk<R>(0.0), ldm2 = mk<R>(0.0);  // ld_{k-1}, ld_{k-2}
+        R ucarry = mk<R>(0.0);                   // u-_{b0-1}
+        staged_pass<R>(sstage, nd.rep, n, false, [&](const double *buf, int64_t t0) {
             if (mine && t0 + RQ_TR - 1 >= r) {
 #pragma unroll 1
                 for (int q = 0; q < RQ_TR / RQ_C; q++) {
                     const int64_t b0 = t0 + q * RQ_C;
-                    if (b0 + RQ_C - 1 < r || b0 >= nd.n) continue;
+                    if (b0 >= n) continue;
+                    if (b0 + RQ_C - 1 < r) {  // below the twist: only track ld
+                        ldm2 = srow<R>(buf, t0, b0 + RQ_C - 2).ld;
+                        ldm1 = srow<R>(buf, t0, b0 + RQ_C - 1).ld;
+                        continue;
+                    }
                     // recompute u-_k for k in [b0, e), e = min(b0 + C, n - 1)
                     R ub[RQ_C];
-                    const int64_t e = (b0 + RQ_C < nd.n - 1) ? b0 + RQ_C : nd.n - 1;
+                    const int64_t e = (b0 + RQ_C < n - 1) ? b0 + RQ_C : n - 1;
                     R p;
                     if (e == b0 + RQ_C)
                         p = A.ck_p[((b0 + RQ_C) / RQ_C) * A.S + slot];
                     else
-                        p = sub(load_row4<R>(nd.rep, nd.n - 1).d, lam);
+                        p = sub(srow<R>(buf, t0, n - 1).d, lam);
 #pragma unroll
                     for (int j = RQ_C - 1; j >= 0; j--) {
-                        int64_t kk = b0 + j;
+                        const int64_t kk = b0 + j;
                         ub[j] = mk<R>(0.0);
                         if (kk < e) {
-                            Row4<R> r4 = load_row4<R>(nd.rep, kk);
-                            R Dm = guard(add(r4.lld, p), A.pivmin);
-                            R t = div(r4.d, Dm);
-                            ub[j] = mul(r4.l, t);
+                            Row4<R> rw = srow<R>(buf, t0, kk);
+                            R Dm = guard(add(rw.lld, p), A.pivmin);
+                            R t = div(rw.d, Dm);
+                            ub[j] = mul(rw.l, t);
                             p = sub(mul(p, t), lam);
                         }
                     }
 #pragma unroll
                     for (int j = 0; j < RQ_C; j++) {
-                        int64_t kk = b0 + j;
+                        const int64_t kk = b0 + j;
                         R uprev = (j == 0) ? ucarry : ub[j == 0 ? 0 : j - 1];
-                        if (kk < nd.n) {
+                        if (kk < n) {
+                            R ldk = srow<R>(buf, t0, kk).ld;
                             if (kk == r) {
                                 z1 = mk<R>(1.0);
-                                z2 = mk<R>(0.0);
+                                z2v = mk<R>(0.0);
                             } else if (kk > r) {
                                 R z;
-                                if (hi(z1) == 0.0 && fabs(hi(z2)) > tiny) {
-                                    Row4<R> ra = load_row4<R>(nd.rep, kk - 2);
-                                    Row4<R> rb = load_row4<R>(nd.rep, kk - 1);
-                                    z = neg(mul(div(ra.ld, rb.ld), z2));
-                                } else {
+                                if (hi(z1) == 0.0 && fabs(hi(z2v)) > tiny)
+                                    z = neg(mul(div(ldm2, ldm1), z2v));
+                                else
                                     z = neg(mul(uprev, z1));
-                                }
                                 if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
                                 OutT zo = (OutT)hi(mul(z, inv));
                                 tile[kk - t0][tid] = zo;
                                 accum_sq((double)zo, ss_hi, ss_lo);
-                                z2 = z1;
+                                z2v = z1;
                                 z1 = z;
                             }
+                            ldm2 = ldm1;
+                            ldm1 = ldk;
                         }
                     }
                     ucarry = ub[RQ_C - 1];
@@ -418,12 +504,11 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
             __syncthreads();
             for (int c = warp; c < RQ_TPB; c += RQ_TPB / 32) {
                 const int64_t row = t0 + lane;
-                if (s_col[c] >= 0 && s_n[c] > 0 && row < s_n[c] && row > s_r[c])
-                    Zo[(s_row0[c] + row) + s_col[c] * A.ldz] = tile[lane][c];
+                if (s_col[c] >= 0 && row < n && row > s_r[c])
+                    Zo[(nd.row0 + row) + s_col[c] * A.ldz] = tile[lane][c];
             }
-            __syncthreads();
-        }
-        if (mine) rows += nd.n - r;
+        });
+        if (mine) rows += n - r;
     }
     if (mine && A.fac) {
         // exact sum of squares of the written column vs 1 (fp64 output only)
@@ -436,14 +521,64 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
 // rescale the columns whose binary64 norm estimate missed by more than 2^-54
 // (one CTA per column; columns with fac == 0 are already unit vectors)
 template <class OutT>
-__global__ void k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols, const double *fac,
-                          const int64_t *row0n /* unused: whole column */, int64_t n) {
+__global__ void k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols, const double *fac, int64_t n) {
     const int64_t c = blockIdx.x;
     if (c >= ncols) return;
     const double f = fac[c];
     if (f == 0.0) return;
-    OutT *col = Z + c * ldz;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) col[i] = (OutT)((double)col[i] * f);
+    OutT *colp = Z + c * ldz;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) colp[i] = (OutT)((double)colp[i] * f);
+}
+
+// CTA tasks for k_rqi: runs of <= RQ_TPB consecutive singletons of the same node
+// (one CTA of 1024 threads; two chunked scans).
+__global__ void __launch_bounds__(1024) k_rqi_tasks(const int32_t *__restrict__ singles, int cnt,
+                                                    const int32_t *__restrict__ item_node,
+                                                    int32_t *seg_begin /* cnt+1 */,
+                                                    RqiTask *tasks, int *ntasks) {
+    __shared__ int sh[33];
+    __shared__ int carry[2];
+    if (threadIdx.x < 2) carry[threadIdx.x] = 0;
+    __syncthreads();
+    // pass 1: node segments
+    for (int base = 0; base < cnt; base += blockDim.x) {
+        int p = base + threadIdx.x;
+        int start = 0;
+        if (p < cnt) start = (p == 0 || item_node[singles[p]] != item_node[singles[p - 1]]) ? 1 : 0;
+        int tot;
+        int ex = block_excl_scan(start, &tot, sh);
+        if (p < cnt && start) seg_begin[carry[0] + ex] = p;
+        __syncthreads();
+        if (threadIdx.x == 0) carry[0] += tot;
+        __syncthreads();
+    }
+    const int nseg = carry[0];
+    if (threadIdx.x == 0) seg_begin[nseg] = cnt;
+    __syncthreads();
+    // pass 2: per segment, ceil(len / TPB) tasks
+    for (int base = 0; base < nseg; base += blockDim.x) {
+        int sgi = base + threadIdx.x;
+        int nt = 0, b0 = 0, len = 0;
+        if (sgi < nseg) {
+            b0 = seg_begin[sgi];
+            len = seg_begin[sgi + 1] - b0;
+            nt = (len + RQ_TPB - 1) / RQ_TPB;
+        }
+        int tot;
+        int ex = block_excl_scan(nt, &tot, sh);
+        for (int q = 0; q < nt; q++) {
+            RqiTask t;
+            t.first = b0 + q * RQ_TPB;
+            t.cnt = min(RQ_TPB, len - q * RQ_TPB);
+            t.node = item_node[singles[b0]];
+            t.pad = 0;
+            tasks[carry[1] + ex + q] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry[1] += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *ntasks = carry[1];
 }
 
 }  // namespace mr3

@@ -724,16 +724,40 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     }
 
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
-        for (int off = 0; off < ncount;) {
-            int64_t S = std::min<int64_t>(Smax, ((ncount - off + RQ_TPB - 1) / RQ_TPB) * RQ_TPB);
-            int rc2 = 0;
+        if (ncount <= 0) return 0;
+        int rc2 = 0;
+        // CTA tasks: runs of <= RQ_TPB singletons of one node (smem staging)
+        RqiTask *dtasks = (RqiTask *)getbuf(ctx, "rqi_tasks", (size_t)(ncount + 1) * sizeof(RqiTask),
+                                            &rc2);
+        int32_t *dseg = (int32_t *)getbuf(ctx, "rqi_seg", (size_t)(ncount + 1) * 4, &rc2);
+        int *dnt = (int *)getbuf(ctx, "rqi_ntasks", 16, &rc2);
+        if (rc2) return rc2;
+        k_rqi_tasks<<<1, 1024, 0, s>>>(list, ncount, W.it.node, dseg, dtasks, dnt);
+        {
+            cudaError_t e2 = cudaGetLastError();
+            if (e2 != cudaSuccess) {
+                ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
+                return MR3_ERR_CUDA;
+            }
+            ctx->launches++;
+        }
+        int ntasks = 0;
+        if (cudaMemcpyAsync(&ntasks, dnt, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            ctx->err = "k_rqi_tasks: copy";
+            return MR3_ERR_CUDA;
+        }
+        const int64_t tmax = std::max<int64_t>(1, Smax / RQ_TPB);
+        for (int off = 0; off < ntasks;) {
+            const int nb = (int)std::min<int64_t>(tmax, ntasks - off);
+            const int64_t S = (int64_t)nb * RQ_TPB;
             char *ck = (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc2);
             if (rc2) return rc2;
             RqiArgs<R> A;
             A.nodes = W.nodes;
             A.it = W.it;
-            A.list = list + off;
-            A.cnt = (int)std::min<int64_t>(S, ncount - off);
+            A.list = list;
+            A.tasks = dtasks + off;
             A.ck_s = (R *)ck;
             A.ck_p = (R *)(ck + nblk * S * sizeof(R));
             A.ck_W = (double *)(ck + 2 * nblk * S * sizeof(R));
@@ -752,7 +776,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             A.unscale = 1.0 / ctx->scale;
             A.st = W.st;
             KTime *t = kt_begin(ctx, "k_rqi");
-            k_rqi<R, OutT><<<(int)(S / RQ_TPB), RQ_TPB, 0, s>>>(A);
+            k_rqi<R, OutT><<<nb, RQ_TPB, 0, s>>>(A);
             kt_end(ctx, t);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
@@ -760,7 +784,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 return MR3_ERR_CUDA;
             }
             ctx->launches++;
-            off += A.cnt;
+            off += nb;
         }
         return 0;
     };
@@ -879,7 +903,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     }
     if (dfac) {
         KTime *tf = kt_begin(ctx, "k_fixnorm");
-        k_fixnorm<OutT><<<(unsigned)(c1 - c0), 256, 0, s>>>(Z, ldz, c1 - c0, dfac, nullptr, ctx->n);
+        k_fixnorm<OutT><<<(unsigned)(c1 - c0), 256, 0, s>>>(Z, ldz, c1 - c0, dfac, ctx->n);
         kt_end(ctx, tf);
         CKL("k_fixnorm");
     }
