@@ -79,7 +79,9 @@ enum mr3_param {
     MR3_RTOL = 7,      /* bisection relative tolerance; default 1e-2 * gaptol (L1294-L1295) */
     MR3_GROUPS = 8,    /* lanes per eigenvalue in the multisection (0 = automatic) */
     MR3_XPHASE = 9,    /* fp64 I/O: approximate eigenvalues in binary_x first (L1064-L1111); 1 */
-    MR3_NPARAM = 10
+    MR3_REFINE = 10,   /* RQI start refinement constant C (0 = off): singletons whose bracket
+                          half-width exceeds gap*sqrt(eps_x sqrt(n)/C) get a binary_x start; 4 */
+    MR3_NPARAM = 11
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

@@ -173,6 +173,50 @@ __global__ void __launch_bounds__(128, 6) k_bisect(const NodeInfo *__restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// K2': starting points for RQI.  Each RQI step restarts inverse iteration from
+// e_r, so its error contracts like e1 ~ C e0^2 / gap; two iterations (one RQ
+// correction + the converged solve) need e0 <= gap sqrt(eps_x sqrt(n) / C).  A
+// singleton whose certified bracket is wider than that (small gaps near the
+// spectrum ends) gets x0 from a binary_x multisection on M_x to a few ulps; the
+// others keep x0 = NaN (bracket midpoint).  x0 needs no certification: the RQI
+// keeps the certified binary_y bracket as its guard.
+// ---------------------------------------------------------------------------
+template <class R, int G>
+__global__ void __launch_bounds__(128) k_refine_x0(const NodeInfo *__restrict__ nodes, Items it,
+                                                   const int32_t *__restrict__ list, int cnt,
+                                                   double eps_x, double pivmin_x, double cconv,
+                                                   DevStats *st) {
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = gtid / G;
+    const int lig = gtid % G;
+    if (item >= cnt) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask =
+        (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int id = list[item];
+    const NodeInfo nd = nodes[it.node[id]];
+    const int k = it.k[id];
+    const R a = reinterpret_cast<R *>(it.lo)[id];
+    const R b = reinterpret_cast<R *>(it.hi)[id];
+    const double gap = fmin(it.lgap[id], it.rgap[id]);
+    const double need = gap * sqrt(eps_x * sqrt((double)nd.n) / cconv);
+    if (!(0.5 * hi(sub(b, a)) > need) || nd.n < 2) {
+        if (lig == 0) it.x0[id] = NAN;
+        return;
+    }
+    double ax = hi(a), bx = hi(b);
+    unsigned long long rows_x = 0;
+    // to a few ulps: relative 4 eps_x (multisect's tol is 2 rtol max|.|)
+    multisect<double, G>(ax, bx, k, lig, lane, gmask, 2.0 * eps_x, 1e-300, 1.0, rows_x, nd.n,
+                         [&](double x) { return negcount_x(nd.repx, nd.n, x, pivmin_x); });
+    if (lig == 0) {
+        double x = 0.5 * (ax + bx);
+        it.x0[id] = (x > hi(a) && x < hi(b)) ? x : NAN;
+    }
+    if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
+}
+
+// ---------------------------------------------------------------------------
 // K3: classification (Alg. 1 l.7, L309-L310; reldist, L593-L612):
 //   reldist(j, j+1) = (lo_{j+1} - hi_j) / max(|lo_j|, |hi_j|, |lo_{j+1}|, |hi_{j+1}|)
 // >= gaptol separates j and j+1 (zero denominator: separated).

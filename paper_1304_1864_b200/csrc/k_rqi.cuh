@@ -69,6 +69,7 @@ struct RqiArgs {
     int64_t ldz, zcol0;
     double unscale;   // multiply eigenvalues by this (exact power of 2)
     DevStats *st;
+    int32_t *dbg_iters;  // optional (MR3_DEBUG): iterations per item
 };
 
 __device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
@@ -189,6 +190,8 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         a = reinterpret_cast<const R *>(A.it.lo)[id];
         b = reinterpret_cast<const R *>(A.it.hi)[id];
         lam = half(add(a, b));
+        const double x0 = A.it.x0[id];
+        if (!isnan(x0) && lt(a, mk<R>(x0)) && lt(mk<R>(x0), b)) lam = mk<R>(x0);
         gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
         if (n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
@@ -361,6 +364,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         }
         reinterpret_cast<R *>(A.it.lo)[id] = lam_out;  // keep lambda[M] for diagnostics
         atomicMax(&A.st->rqi_iters_max, iters);
+        if (A.dbg_iters) A.dbg_iters[id] = iters;
     }
     if (!A.jobz_v) {
         if (active && rows) atomicAdd(&A.st->rqi_rows, rows);

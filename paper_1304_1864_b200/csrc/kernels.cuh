@@ -30,6 +30,7 @@ struct Items {  // eigenvalue slots, SoA over the requested index set (+ guards)
     int64_t *col;    // output column (global), -1 = guard / not wanted
     void *lo, *hi;   // R brackets [lo, hi] in node coordinates
     double *lgap, *rgap;  // absolute gaps to the neighbours (node coordinates)
+    double *x0;           // RQI starting point (binary64, node coordinates) or NaN: midpoint
 };
 
 struct DevStats {

@@ -82,9 +82,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0},
 };
 
 #define CK(call)                                                                  \
@@ -179,7 +179,7 @@ struct Work {
 };
 
 // lanes per eigenvalue of the multisection: enough independent Sturm chains to
-// cover the dependent-step latency (about 16 warps per SM), as few as possible
+// cover the dependent-step latency (about 4 warps per SM; measured sweep), as few as possible
 // beyond that (a round of G points buys log2(G+1) bits).  A function of the
 // global item count only, so every rank takes the same path (determinism).
 static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
@@ -188,7 +188,7 @@ static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
         while (g * 2 <= forced && g < 32) g *= 2;
         return g;
     }
-    const long long target = (long long)ctx->nsm * 16 * 32;
+    const long long target = (long long)ctx->nsm * 4 * 32;
     int g = 1;
     while (g < 32 && (long long)cnt * g < target) g *= 2;
     return g;
@@ -436,6 +436,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.hi = getbuf(ctx, "it_hi", (size_t)cnt * sizeof(R), &rc);
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
+        it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
         if (rc) return rc;
         k_init_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, (int)k_lo, (int)ilw, (int)iuw, 0,
                                                           dbrk0);
@@ -459,6 +460,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.hi = getbuf(ctx, "it_hi", (size_t)cnt * sizeof(R), &rc);
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
+        it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
         if (rc) return rc;
         CK(cudaMemcpyAsync(ditem0, item0.data(), item0.size() * 8, cudaMemcpyHostToDevice, s));
         k_init_items_blocks<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, dblocks, ctx->nblocks,
@@ -484,6 +486,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     W.it.hi = ctx->bufs["it_hi"].p;
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
+    W.it.x0 = (double *)ctx->bufs["it_x0"].p;
     W.nodes = dnodes;
     W.st = dst;
     double rtol = P[MR3_RTOL] > 0 ? P[MR3_RTOL] : 1e-2 * P[MR3_GAPTOL];
@@ -539,6 +542,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.it.hi = ctx->bufs["it_hi"].p;
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
+    W.it.x0 = (double *)ctx->bufs["it_x0"].p;
     W.nodes = (NodeInfo *)ctx->bufs["nodes"].p;
     W.st = (DevStats *)ctx->bufs["devstats"].p;
     double *dbrk = (double *)ctx->bufs["brk"].p;
@@ -726,6 +730,21 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
         if (ncount <= 0) return 0;
         int rc2 = 0;
+        if (P[MR3_REFINE] > 0) {  // K2': binary_x starting points for small-gap singletons
+            const long long threads = (long long)ncount * 4;
+            KTime *tr = kt_begin(ctx, "k_refine_x0");
+            k_refine_x0<R, 4><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
+                W.nodes, W.it, list, ncount, eps_x, 0x1p-900, P[MR3_REFINE], W.st);
+            kt_end(ctx, tr);
+            cudaError_t e2 = cudaGetLastError();
+            if (e2 != cudaSuccess) {
+                ctx->err = std::string("k_refine_x0: ") + cudaGetErrorString(e2);
+                return MR3_ERR_CUDA;
+            }
+            ctx->launches++;
+        } else {
+            CK(cudaMemsetAsync(W.it.x0, 0xff, (size_t)cnt * 8, s));  // NaN: midpoints
+        }
         // CTA tasks: runs of <= RQ_TPB singletons of one node (smem staging)
         RqiTask *dtasks = (RqiTask *)getbuf(ctx, "rqi_tasks", (size_t)(ncount + 1) * sizeof(RqiTask),
                                             &rc2);
@@ -775,6 +794,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             A.zcol0 = c0;
             A.unscale = 1.0 / ctx->scale;
             A.st = W.st;
+            A.dbg_iters = nullptr;
+            if (ctx->debug) A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc2);
             KTime *t = kt_begin(ctx, "k_rqi");
             k_rqi<R, OutT><<<nb, RQ_TPB, 0, s>>>(A);
             kt_end(ctx, t);
@@ -900,6 +921,30 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if (ctx->debug)
             fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
                     nclus, nmem);
+    }
+    if (ctx->debug && ctx->bufs.count("dbg_iters")) {
+        cudaStreamSynchronize(s);
+        std::vector<int32_t> itv(cnt);
+        std::vector<double> lg(cnt), rg(cnt);
+        std::vector<R> lam(cnt);
+        cudaMemcpy(itv.data(), ctx->bufs["dbg_iters"].p, cnt * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(lg.data(), W.it.lgap, cnt * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(rg.data(), W.it.rgap, cnt * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(lam.data(), W.it.lo, cnt * sizeof(R), cudaMemcpyDeviceToHost);
+        int hist[16] = {0};
+        for (int i = 0; i < cnt; i++) hist[std::min(15, std::max(0, itv[i]))]++;
+        fprintf(stderr, "[mr3] rqi iteration histogram:");
+        for (int i = 0; i < 16; i++)
+            if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
+        fprintf(stderr, "\n");
+        int shown = 0;
+        for (int i = 0; i < cnt && shown < 40; i++)
+            if (itv[i] >= 4) {
+                fprintf(stderr, "  item %d iters %d lam %.17g lgap %.3g rgap %.3g\n", i, itv[i],
+                        hi_of(lam[i]), lg[i], rg[i]);
+                shown++;
+            }
+        cudaMemset(ctx->bufs["dbg_iters"].p, 0, cnt * 4);
     }
     if (dfac) {
         KTime *tf = kt_begin(ctx, "k_fixnorm");
