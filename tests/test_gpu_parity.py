@@ -165,7 +165,8 @@ def test_deterministic_repeat():
     np.testing.assert_array_equal(Z1, Z2)
 
 
-def test_two_phase_world_emulation_bitwise():
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_two_phase_world_emulation_bitwise(world):
     """Ranks of the plan/execute form emulated one after another on one GPU: the
     union of their columns equals the world=1 solve bit for bit."""
     import ctypes
@@ -175,7 +176,6 @@ def test_two_phase_world_emulation_bitwise():
     w1, Z1, _ = mr3.mr3_dstemr_dd(d, e)
     w1, Z1 = w1.cpu().numpy(), Z1.cpu().numpy()
     L = mr3.lib()
-    world = 3
     ctxs, bufs, caps = [], [], []
     streams = [torch.cuda.Stream() for _ in range(world)]
     for r in range(world):
