@@ -30,7 +30,7 @@ import synth  # noqa: E402
 # SASS-counted FP64-pipe instructions (DADD/DMUL/DFMA/DSETP; MUFU.RCP64H is on the XU) per row of
 # the dd negcount loop of k_bisect<dd,1> (recount
 # with tools/count_sass.py after every change of the loop body).
-FP64_INST_PER_BISECT_ROW = {"dd": 45.25, "f64": 12, "x": 6.25}  # "x": binary_x phase rows
+FP64_INST_PER_BISECT_ROW = {"dd": 45.25, "f64": 12, "x": 3.25}  # "x": binary_x phase rows (projective)
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 
 

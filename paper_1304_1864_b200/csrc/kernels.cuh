@@ -124,7 +124,6 @@ __device__ __forceinline__ R guard(R x, double pivmin) {
 //   s_1 = -x ; d+_j = d_j + s_j ; s_{j+1} = lld_j * (s_j / d+_j) - x
 // ("special forms of ... qd"; Sturm count S:182-188).
 // ---------------------------------------------------------------------------
-constexpr int PF = 4;   // binary_x rows prefetched ahead of the Sturm recurrence (L2 latency)
 constexpr int PFY = 2;  // binary_y rows prefetched ahead (32 B each)
 
 template <class R>
@@ -165,11 +164,21 @@ __device__ __forceinline__ int negcount(const double *__restrict__ rep, int64_t 
 }
 
 // negcount in binary_x arithmetic on the narrowed copy M_x (§3.2,
-// "Arithmetic used to approximate eigenvalues", L1064-L1111).
-// Fast path per row: d+ = d + s ; count the sign bit ; s = (lld s) * rcp(d+) - x
-// (lld*s is off the dependency chain; rcp to 1 ulp).  No pivot guard: a zero
-// (or subnormal) pivot turns s into NaN, which is checked once per PF rows and
-// the block is then redone with the guard |d+| < pivmin -> -pivmin.
+// "Arithmetic used to approximate eigenvalues", L1064-L1111), in projective
+// (division-free) form.  With s_j = p_j / q_j the dstqds step
+//   d+_j = d_j + s_j ,  s_{j+1} = lld_j s_j / d+_j - x
+// becomes  D_j = d_j q_j + p_j  (= d+_j q_j),  q_{j+1} = D_j,  p_{j+1} = lld_j p_j - x D_j,
+// and d+_j < 0  <=>  sign(D_j) != sign(q_j).  Per row: two FMAs and one MUL, no
+// reciprocal, and a dependent chain of two FMAs.  (p, q) is rescaled by a power of
+// two every XB rows (exact); a non-finite state (overflow; unreachable for XB = 8
+// unless |lld| > 1e38) redoes the block in the guarded ratio form.  A zero pivot
+// needs no guard: D_j = 0 makes q_{j+1} = 0 and s_{j+1} = +-inf, which the next
+// row absorbs exactly as IEEE arithmetic on the ratio form would.  The binary_x
+// counts only steer the search: every bracket is certified by binary_y (dstqds)
+// counts afterwards (k_bisect XPHASE), so this form needs no stability argument
+// of its own beyond producing counts of a nearby matrix.
+// The rows are read with a prefetch distance of XB rows; repx arrays carry XPAD
+// padding rows beyond the last row so the prefetch never needs a bound check.
 __device__ __forceinline__ int sign_bit(double v) {
     return (int)((unsigned)__double2hiint(v) >> 31);
 }
@@ -180,46 +189,63 @@ __device__ __forceinline__ void nc_row_guarded(double d, double lld, double x, d
     cnt += dp < 0.0 ? 1 : 0;
     s = fma_rn(lld * s, rcp(dp), -x);
 }
+constexpr int XB = 8;    // rows per block (prefetch distance, rescale period)
+constexpr int XPAD = 8;  // padding rows after every binary_x representation
+__device__ __forceinline__ void xrow(const double2 r, const double x, double &p, double &q,
+                                     unsigned &c) {
+    const double D = fma_rn(r.x, q, p);
+    c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+    p = fma_rn(-x, D, mul_rn(r.y, p));
+    q = D;
+}
 __device__ __forceinline__ int negcount_x(const double *__restrict__ repx, int64_t n, double x,
                                           double pivmin) {
     const double2 *rx = reinterpret_cast<const double2 *>(repx);
-    double s = -x;
-    int cnt = 0;
-    double2 ring[PF];
-#pragma unroll
-    for (int u = 0; u < PF; u++) ring[u] = __ldg(rx + (u < n ? u : n - 1));
+    double p = -x, q = 1.0;
+    unsigned c = 0;
     int64_t j = 0;
+    if (n - 1 >= XB) {
+        double2 r0 = __ldg(rx + 0), r1 = __ldg(rx + 1), r2 = __ldg(rx + 2), r3 = __ldg(rx + 3),
+                r4 = __ldg(rx + 4), r5 = __ldg(rx + 5), r6 = __ldg(rx + 6), r7 = __ldg(rx + 7);
 #pragma unroll 1
-    for (; j + PF <= n - 1; j += PF) {
-        const double s0 = s;
-        int c = 0;
-#pragma unroll
-        for (int u = 0; u < PF; u++) {
-            const double2 cur = ring[u];
-            int64_t nx = j + u + PF;
-            ring[u] = __ldg(rx + (nx < n ? nx : n - 1));
-            double dp = cur.x + s;
-            c += sign_bit(dp);
-            s = fma_rn(cur.y * s, rcp(dp), -x);
-        }
-        if (isnan(s)) {  // a (near-)zero pivot in this block: redo it guarded (rare)
-            s = s0;
-            c = 0;
-            for (int u = 0; u < PF; u++) {
-                const double2 cur = __ldg(rx + j + u);
-                nc_row_guarded(cur.x, cur.y, x, pivmin, s, c);
+        for (; j + XB <= n - 1; j += XB) {
+            const double p0 = p, q0 = q;
+            const unsigned c0 = c;
+            const double2 *nx = rx + j + XB;
+            xrow(r0, x, p, q, c); r0 = __ldg(nx + 0);
+            xrow(r1, x, p, q, c); r1 = __ldg(nx + 1);
+            xrow(r2, x, p, q, c); r2 = __ldg(nx + 2);
+            xrow(r3, x, p, q, c); r3 = __ldg(nx + 3);
+            xrow(r4, x, p, q, c); r4 = __ldg(nx + 4);
+            xrow(r5, x, p, q, c); r5 = __ldg(nx + 5);
+            xrow(r6, x, p, q, c); r6 = __ldg(nx + 6);
+            xrow(r7, x, p, q, c); r7 = __ldg(nx + 7);
+            const unsigned ep = (unsigned)__double2hiint(p) & 0x7ff00000u;
+            const unsigned eq = (unsigned)__double2hiint(q) & 0x7ff00000u;
+            const unsigned em = ep > eq ? ep : eq;
+            if (em == 0x7ff00000u) {  // overflow: redo the block in the guarded ratio form
+                double s = p0 / q0;
+                if (!(fabs(s) <= 1e300)) s = copysign(1e300, s);
+                int cc = 0;
+                for (int u = 0; u < XB; u++) {
+                    const double2 r = __ldg(rx + j + u);
+                    nc_row_guarded(r.x, r.y, x, pivmin, s, cc);
+                }
+                c = c0 + (unsigned)cc;
+                p = s;
+                q = 1.0;
+            } else {  // exact power-of-two rescale to max exponent 2^0
+                const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+                p = mul_rn(p, sc);
+                q = mul_rn(q, sc);
             }
         }
-        cnt += c;
     }
-#pragma unroll
-    for (int u = 0; u < PF; u++)
-        if (j + u < n - 1) nc_row_guarded(ring[u].x, ring[u].y, x, pivmin, s, cnt);
-    double2 last = __ldg(rx + (n - 1));
-    double dp = last.x + s;
-    dp = fabs(dp) < pivmin ? -pivmin : dp;
-    cnt += dp < 0.0 ? 1 : 0;
-    return cnt;
+#pragma unroll 1
+    for (; j < n - 1; j++) xrow(__ldg(rx + j), x, p, q, c);  // fewer than XB rows
+    const double D = fma_rn(__ldg(rx + (n - 1)).x, q, p);
+    c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+    return (int)c;
 }
 
 // two shifts through the same rows (ILP 2)

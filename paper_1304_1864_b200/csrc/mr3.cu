@@ -339,7 +339,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     blk_chunk0[blocks.size()] = (int)chunks.size();
     const int nch = (int)chunks.size();
     double *rep_pool = (double *)getbuf(ctx, "rep_root", (size_t)n * 4 * words * 8, &rc);
-    double *repx_pool = (double *)getbuf(ctx, "repx_root", (size_t)n * 16, &rc);
+    double *repx_pool = (double *)getbuf(ctx, "repx_root", (size_t)(n + XPAD) * 16, &rc);
     BlockDesc *dblocks = (BlockDesc *)getbuf(ctx, "blocks", blocks.size() * sizeof(BlockDesc), &rc);
     ChunkDesc *dchunks = (ChunkDesc *)getbuf(ctx, "chunks", chunks.size() * sizeof(ChunkDesc), &rc);
     int *dbc0 = (int *)getbuf(ctx, "blk_chunk0", blk_chunk0.size() * 4, &rc);
@@ -351,6 +351,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     ctx->node_cap = std::max<int>(1024, ctx->nblocks * 2 + 64);
     NodeInfo *dnodes = (NodeInfo *)getbuf(ctx, "nodes", ctx->node_cap * sizeof(NodeInfo), &rc);
     if (rc) return rc;
+    CK(cudaMemsetAsync(repx_pool + 2 * n, 0, XPAD * 16, s));  // prefetch padding (negcount_x)
     CK(cudaMemcpyAsync(dblocks, blocks.data(), blocks.size() * sizeof(BlockDesc),
                        cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dchunks, chunks.data(), chunks.size() * sizeof(ChunkDesc),
@@ -880,8 +881,10 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         std::string pname = "child_pool" + std::to_string(level);
         double *pool =
             (double *)getbuf(ctx, pname, (size_t)nclus * ctx->n * 4 * words * 8, &rc);
-        double *poolx = (double *)getbuf(ctx, pname + "x", (size_t)nclus * ctx->n * 16, &rc);
+        double *poolx =
+            (double *)getbuf(ctx, pname + "x", ((size_t)nclus * ctx->n + XPAD) * 16, &rc);
         if (rc) return rc;
+        CK(cudaMemsetAsync(poolx + 2 * (size_t)nclus * ctx->n, 0, XPAD * 16, s));
         double *cdbg = nullptr;
         if (ctx->debug) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
