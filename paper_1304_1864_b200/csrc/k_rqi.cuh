@@ -95,18 +95,21 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <class R>
-struct Stage {
-    static constexpr int ROWD = 4 * Prec<R>::words;  // doubles per row
-    static constexpr int ROWS = RQ_TR + RQ_HALO;     // staged rows per tile
-    static constexpr int TILE = ROWS * ROWD;         // doubles per tile buffer
+// rows of ROWD doubles (4 R values per row of a binary_y representation, {d, lld}
+// per row of the binary_x copy)
+template <int ROWD_>
+struct StageG {
+    static constexpr int ROWD = ROWD_;             // doubles per row
+    static constexpr int ROWS = RQ_TR + RQ_HALO;   // staged rows per tile
+    static constexpr int TILE = ROWS * ROWD;       // doubles per tile buffer
 };
+template <class R>
+struct Stage : StageG<4 * Prec<R>::words> {};
 
 // rows [t0 - HALO, t0 + TR) of rep (clamped to [0, n)) -> buf, asynchronously
-template <class R>
-__device__ __forceinline__ void stage_tile(double *buf, const double *rep, int64_t n, int64_t t0) {
-    constexpr int ROWD = Stage<R>::ROWD;
-    constexpr int CH = Stage<R>::ROWS * ROWD / 2;  // 16-byte chunks
+template <int ROWD>
+__device__ __forceinline__ void stage_tile_g(double *buf, const double *rep, int64_t n, int64_t t0) {
+    constexpr int CH = StageG<ROWD>::ROWS * ROWD / 2;  // 16-byte chunks
     for (int c = threadIdx.x; c < CH; c += RQ_TPB) {
         int r = c / (ROWD / 2), off = (c % (ROWD / 2)) * 2;
         int64_t g = t0 - RQ_HALO + r;
@@ -114,6 +117,34 @@ __device__ __forceinline__ void stage_tile(double *buf, const double *rep, int64
         cp_async16(buf + r * ROWD + off, rep + g * ROWD + off);
     }
     cp_async_commit();
+}
+
+// Run body(buf, t0) over all row tiles of the representation, ascending or
+// descending, with the next tile's rows in flight while the current one is used.
+// Every thread of the CTA must call this (barriers inside).
+template <int ROWD, class Body>
+__device__ __forceinline__ void staged_pass_g(double *smem, const double *rep, int64_t n, bool desc,
+                                              Body body) {
+    constexpr int TILE = StageG<ROWD>::TILE;
+    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+    auto t0_of = [&](int i) -> int64_t { return (int64_t)(desc ? ntile - 1 - i : i) * RQ_TR; };
+    stage_tile_g<ROWD>(smem, rep, n, t0_of(0));
+    for (int i = 0; i < ntile; i++) {
+        if (i + 1 < ntile) {
+            stage_tile_g<ROWD>(smem + ((i + 1) & 1) * TILE, rep, n, t0_of(i + 1));
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        body(smem + (i & 1) * TILE, t0_of(i));
+        __syncthreads();
+    }
+}
+template <class R, class Body>
+__device__ __forceinline__ void staged_pass(double *smem, const double *rep, int64_t n, bool desc,
+                                            Body body) {
+    staged_pass_g<Stage<R>::ROWD>(smem, rep, n, desc, body);
 }
 
 template <class R>
@@ -139,29 +170,6 @@ __device__ __forceinline__ Row4<double> srow<double>(const double *buf, int64_t 
     r.l = b.x;
     r.ld = b.y;
     return r;
-}
-
-// Run body(buf, t0) over all row tiles of the representation, ascending or
-// descending, with the next tile's rows in flight while the current one is used.
-// Every thread of the CTA must call this (barriers inside).
-template <class R, class Body>
-__device__ __forceinline__ void staged_pass(double *smem, const double *rep, int64_t n, bool desc,
-                                            Body body) {
-    constexpr int TILE = Stage<R>::TILE;
-    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
-    auto t0_of = [&](int i) -> int64_t { return (int64_t)(desc ? ntile - 1 - i : i) * RQ_TR; };
-    stage_tile<R>(smem, rep, n, t0_of(0));
-    for (int i = 0; i < ntile; i++) {
-        if (i + 1 < ntile) {
-            stage_tile<R>(smem + ((i + 1) & 1) * TILE, rep, n, t0_of(i + 1));
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        body(smem + (i & 1) * TILE, t0_of(i));
-        __syncthreads();
-    }
 }
 
 // ---------------------------------------------------------------- kernel
@@ -194,6 +202,8 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         if (!isnan(x0) && lt(a, mk<R>(x0)) && lt(mk<R>(x0), b)) lam = mk<R>(x0);
         gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
+        r = A.it.twist[id];
+        if (r < 0 || r >= n) r = n - 1;
         if (n == 1) {  // 1x1 block: the eigenpair is (d_1, e_1) exactly
             lam_out = load_row4<R>(nd.rep, 0).d;
             done = true;
@@ -300,11 +310,83 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         return negc;
     };
 
+    // One twisted factorization at lam with the twist index r fixed (from
+    // k_rqi_locate): F rows 0..r-1 top-down and B rows n-1..r+1 bottom-up only --
+    // n rows instead of the 3n of a full factorization with argmin.  Checkpoints:
+    // s at every block start b0 <= r, p at every block start >= r (what the z
+    // sweeps below need).  Returns the inertia of the twisted factorization
+    // N_r Delta_r N_r^T = M - lam I, Delta_r = diag(d+_0..d+_{r-1}, gamma_r,
+    // D-_{r+1}..D-_{n-1}), i.e. negcount(lam) (Sylvester).
+    auto twisted_fixed = [&](bool need) -> int {
+        R s = neg(lam);
+        double W = 0.0;
+        int negc = 0;
+        staged_pass<R>(sstage, nd.rep, n, false, [&](const double *buf, int64_t t0) {
+            if (!need || t0 > r) return;
+#pragma unroll
+            for (int q = 0; q < RQ_TR / RQ_C; q++) {
+                const int64_t b0 = t0 + q * RQ_C;
+                if (b0 <= r) {
+                    A.ck_s[(b0 / RQ_C) * A.S + slot] = s;
+                    A.ck_W[(b0 / RQ_C) * A.S + slot] = W;
+                }
+#pragma unroll
+                for (int j = 0; j < RQ_C; j++) {
+                    const int64_t kk = b0 + j;
+                    if (kk < r) {
+                        Row4<R> rw = srow<R>(buf, t0, kk);
+                        R dp = guard(add(rw.d, s), A.pivmin);
+                        negc += is_neg(dp) ? 1 : 0;
+                        R lp = div(rw.ld, dp);
+                        double l2 = hi(lp) * hi(lp);
+                        W = clampbig(fma(l2, W, l2));
+                        s = sub(mul(lp, mul(rw.l, s)), lam);
+                    }
+                }
+            }
+        });
+        R p = mk<R>(0.0);
+        double V = 0.0;
+        if (need) p = sub(load_row4<R>(nd.rep, n - 1).d, lam);
+        staged_pass<R>(sstage, nd.rep, n, true, [&](const double *buf, int64_t t0) {
+            if (!need || t0 + RQ_TR <= r) return;
+#pragma unroll 1
+            for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
+                const int64_t b0 = t0 + q * RQ_C;
+                if (b0 >= n || b0 + RQ_C <= r) continue;
+#pragma unroll
+                for (int j = RQ_C - 1; j >= 0; j--) {
+                    const int64_t kk = b0 + j;
+                    if (kk < n && kk >= r) {
+                        if (j == 0) A.ck_p[(b0 / RQ_C) * A.S + slot] = p;  // p_{b0}
+                        if (kk > r) {
+                            Row4<R> rw = srow<R>(buf, t0, kk - 1);
+                            R Dm = guard(add(rw.lld, p), A.pivmin);
+                            negc += is_neg(Dm) ? 1 : 0;
+                            R t = div(rw.d, Dm);
+                            double u2 = hi(rw.l) * hi(t);
+                            u2 *= u2;
+                            V = clampbig(fma(u2, V, u2));
+                            p = sub(mul(p, t), lam);  // p_{kk-1}
+                        }
+                    }
+                }
+            }
+        });
+        if (need) {
+            gr = add(add(s, p), lam);
+            negc += is_neg(gr) ? 1 : 0;
+            nz2 = 1.0 + W + V;
+            rows += n;
+        }
+        return negc;
+    };
+
 #pragma unroll 1
     for (iters = 1; iters <= A.maxit; iters++) {
         const bool need = !done;
         if (!__syncthreads_or(need)) break;
-        int c = twisted(need);
+        int c = twisted_fixed(need);
         if (need) {
             if (c >= k) {
                 if (lt(lam, b)) b = lam;
@@ -522,6 +604,111 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
     if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
 }
 
+// ---------------------------------------------------------------------------
+// K5a: twist index of each singleton ("determine
+// r = argmin_k |gamma_k|"), located once in binary_x on the narrowed copy M_x
+// (L1071): a full twisted factorization at lam_loc = lam_start + 1e-4 gap --
+// close to lambda on the scale of the gap, far from it on the scale of the
+// binary_x rounding -- so |gamma_k| ~ |lambda - lam_loc| / z_k^2 and the argmin
+// picks a row where the eigenvector is large.  The binary_y iterations (k_rqi)
+// then keep r fixed and need only n rows per factorization: the RQ correction
+// gamma_r / ||z||^2 is exact to first order for any r with z_r != 0, and the
+// stopping test (Eq. (3.6)) is evaluated on the actual binary_y gamma_r.
+//   F: s_0 = -lam ; d+_i = d_i + s_i ; s_{i+1} = lld_i s_i / d+_i - lam
+//   B: p_{n-1} = d_{n-1} - lam ; D-_{i+1} = lld_i + p_{i+1} ; p_i = d_i p_{i+1} / D-_{i+1} - lam
+//   gamma_k = s_k + p_k + lam ;  r = argmin |gamma_k| (ties: smallest k)
+// s is checkpointed every RQ_C rows (binary64, in ck_W) and recomputed per block
+// during B; rows of M_x are staged through shared memory like k_rqi's.
+// ---------------------------------------------------------------------------
+template <class R>
+__global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
+    __shared__ __align__(16) double sx[2 * StageG<2>::TILE];
+    const int tid = threadIdx.x;
+    const RqiTask task = A.tasks[blockIdx.x];
+    const NodeInfo nd = A.nodes[task.node];
+    const int64_t n = nd.n;
+    const int64_t slot = (int64_t)blockIdx.x * RQ_TPB + tid;
+    const bool active = tid < task.cnt && n > 1;
+    int id = -1;
+    double lam = 0.0, pivmin = A.pivmin;
+    if (tid < task.cnt) {
+        id = A.list[task.first + tid];
+        const double a = hi(reinterpret_cast<const R *>(A.it.lo)[id]);
+        const double b = hi(reinterpret_cast<const R *>(A.it.hi)[id]);
+        double gap = fmin(A.it.lgap[id], A.it.rgap[id]);
+        if (!(gap > 0.0) || !(gap < INFINITY)) gap = fmax(b - a, 1e-300);
+        const double x0 = A.it.x0[id];
+        lam = (!isnan(x0) && x0 > a && x0 < b) ? x0 : 0.5 * (a + b);
+        lam += 1e-4 * gap;
+        if (n <= 1) A.it.twist[id] = 0;
+    }
+    auto xr = [&](const double *buf, int64_t t0, int64_t k) -> double2 {
+        return *reinterpret_cast<const double2 *>(buf + (k - t0 + RQ_HALO) * 2);
+    };
+    double s = -lam;
+    staged_pass_g<2>(sx, nd.repx, n, false, [&](const double *buf, int64_t t0) {
+        if (!active) return;
+#pragma unroll 1
+        for (int q = 0; q < RQ_TR / RQ_C; q++) {
+            const int64_t b0 = t0 + q * RQ_C;
+            if (b0 >= n) break;
+            A.ck_W[(b0 / RQ_C) * A.S + slot] = s;
+#pragma unroll
+            for (int j = 0; j < RQ_C; j++) {
+                const int64_t kk = b0 + j;
+                if (kk < n - 1) {
+                    const double2 rw = xr(buf, t0, kk);
+                    double dp = rw.x + s;
+                    dp = fabs(dp) < pivmin ? -pivmin : dp;
+                    s = fma_rn(mul_rn(rw.y, s), rcp(dp), -lam);
+                }
+            }
+        }
+    });
+    double p = 0.0, best = INFINITY;
+    int64_t rr = n - 1;
+    if (active) p = __ldg(nd.repx + 2 * (n - 1)) - lam;
+    staged_pass_g<2>(sx, nd.repx, n, true, [&](const double *buf, int64_t t0) {
+        if (!active) return;
+#pragma unroll 1
+        for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
+            const int64_t b0 = t0 + q * RQ_C;
+            if (b0 >= n) continue;
+            double sb[RQ_C];
+            double s2 = A.ck_W[(b0 / RQ_C) * A.S + slot];
+#pragma unroll
+            for (int j = 0; j < RQ_C; j++) {
+                const int64_t kk = b0 + j;
+                sb[j] = s2;
+                if (kk < n - 1) {
+                    const double2 rw = xr(buf, t0, kk);
+                    double dp = rw.x + s2;
+                    dp = fabs(dp) < pivmin ? -pivmin : dp;
+                    s2 = fma_rn(mul_rn(rw.y, s2), rcp(dp), -lam);
+                }
+            }
+#pragma unroll
+            for (int j = RQ_C - 1; j >= 0; j--) {
+                const int64_t kk = b0 + j;
+                if (kk < n) {
+                    const double g = fabs(sb[j] + p + lam);
+                    if (g <= best) {
+                        best = g;
+                        rr = kk;
+                    }
+                    if (kk > 0) {
+                        const double2 rw = xr(buf, t0, kk - 1);
+                        double Dm = rw.y + p;
+                        Dm = fabs(Dm) < pivmin ? -pivmin : Dm;
+                        p = fma_rn(mul_rn(rw.x, p), rcp(Dm), -lam);
+                    }
+                }
+            }
+        }
+    });
+    if (active) A.it.twist[id] = (int32_t)rr;
+}
+
 // rescale the columns whose binary64 norm estimate missed by more than 2^-54
 // (one CTA per column; columns with fac == 0 are already unit vectors)
 template <class OutT>
@@ -532,6 +719,18 @@ __global__ void k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols, const double *fac
     if (f == 0.0) return;
     OutT *colp = Z + c * ldz;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) colp[i] = (OutT)((double)colp[i] * f);
+}
+
+// sort keys (node, twist index) of the singletons for k_rqi's CTA grouping
+__global__ void k_twist_keys(const int32_t *__restrict__ list, int cnt,
+                             const int32_t *__restrict__ item_node,
+                             const int32_t *__restrict__ twist, unsigned long long *keys,
+                             int32_t *vals) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const int id = list[t];
+    keys[t] = ((unsigned long long)(unsigned)item_node[id] << 32) | (unsigned)twist[id];
+    vals[t] = id;
 }
 
 // CTA tasks for k_rqi: runs of <= RQ_TPB consecutive singletons of the same node

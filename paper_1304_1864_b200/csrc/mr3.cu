@@ -438,6 +438,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
         it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
+        it.twist = (int32_t *)getbuf(ctx, "it_twist", cnt * 4, &rc);
         if (rc) return rc;
         k_init_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, (int)k_lo, (int)ilw, (int)iuw, 0,
                                                           dbrk0);
@@ -462,6 +463,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
         it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
+        it.twist = (int32_t *)getbuf(ctx, "it_twist", cnt * 4, &rc);
         if (rc) return rc;
         CK(cudaMemcpyAsync(ditem0, item0.data(), item0.size() * 8, cudaMemcpyHostToDevice, s));
         k_init_items_blocks<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, dblocks, ctx->nblocks,
@@ -488,6 +490,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
     W.it.x0 = (double *)ctx->bufs["it_x0"].p;
+    W.it.twist = (int32_t *)ctx->bufs["it_twist"].p;
     W.nodes = dnodes;
     W.st = dst;
     double rtol = P[MR3_RTOL] > 0 ? P[MR3_RTOL] : 1e-2 * P[MR3_GAPTOL];
@@ -544,6 +547,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
     W.it.x0 = (double *)ctx->bufs["it_x0"].p;
+    W.it.twist = (int32_t *)ctx->bufs["it_twist"].p;
     W.nodes = (NodeInfo *)ctx->bufs["nodes"].p;
     W.st = (DevStats *)ctx->bufs["devstats"].p;
     double *dbrk = (double *)ctx->bufs["brk"].p;
@@ -751,64 +755,97 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                                             &rc2);
         int32_t *dseg = (int32_t *)getbuf(ctx, "rqi_seg", (size_t)(ncount + 1) * 4, &rc2);
         int *dnt = (int *)getbuf(ctx, "rqi_ntasks", 16, &rc2);
+        unsigned long long *tkeys =
+            (unsigned long long *)getbuf(ctx, "rqi_keys", (size_t)ncount * 8 * 2, &rc2);
+        int32_t *tvals = (int32_t *)getbuf(ctx, "rqi_vals", (size_t)ncount * 4, &rc2);
+        int32_t *slist = (int32_t *)getbuf(ctx, "rqi_sorted", (size_t)ncount * 4, &rc2);
         if (rc2) return rc2;
-        k_rqi_tasks<<<1, 1024, 0, s>>>(list, ncount, W.it.node, dseg, dtasks, dnt);
-        {
+        auto make_tasks = [&](const int32_t *lst, int *nt) -> int {
+            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
                 ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
                 return MR3_ERR_CUDA;
             }
             ctx->launches++;
-        }
-        int ntasks = 0;
-        if (cudaMemcpyAsync(&ntasks, dnt, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess) {
-            ctx->err = "k_rqi_tasks: copy";
-            return MR3_ERR_CUDA;
-        }
-        const int64_t tmax = std::max<int64_t>(1, Smax / RQ_TPB);
-        for (int off = 0; off < ntasks;) {
-            const int nb = (int)std::min<int64_t>(tmax, ntasks - off);
-            const int64_t S = (int64_t)nb * RQ_TPB;
-            char *ck = (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc2);
-            if (rc2) return rc2;
-            RqiArgs<R> A;
-            A.nodes = W.nodes;
-            A.it = W.it;
-            A.list = list;
-            A.tasks = dtasks + off;
-            A.ck_s = (R *)ck;
-            A.ck_p = (R *)(ck + nblk * S * sizeof(R));
-            A.ck_W = (double *)(ck + 2 * nblk * S * sizeof(R));
-            A.fac = dfac;
-            A.S = S;
-            A.pivmin = ctx->pivmin;
-            A.krs = P[MR3_KRS];
-            A.eps_x = eps_x;
-            A.gaptol = gaptol;
-            A.maxit = (int)P[MR3_MAX_RQI];
-            A.jobz_v = jobz == 'V';
-            A.w = w;
-            A.Z = Z;
-            A.ldz = ldz;
-            A.zcol0 = c0;
-            A.unscale = 1.0 / ctx->scale;
-            A.st = W.st;
-            A.dbg_iters = nullptr;
-            if (ctx->debug) A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc2);
-            KTime *t = kt_begin(ctx, "k_rqi");
-            k_rqi<R, OutT><<<nb, RQ_TPB, 0, s>>>(A);
-            kt_end(ctx, t);
-            cudaError_t e2 = cudaGetLastError();
-            if (e2 != cudaSuccess) {
-                ctx->err = std::string("k_rqi: ") + cudaGetErrorString(e2);
+            if (cudaMemcpyAsync(nt, dnt, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess) {
+                ctx->err = "k_rqi_tasks: copy";
                 return MR3_ERR_CUDA;
             }
-            ctx->launches++;
-            off += nb;
+            return 0;
+        };
+        const int64_t tmax = std::max<int64_t>(1, Smax / RQ_TPB);
+        auto launch_chunks = [&](bool locate, const int32_t *lst, int ntasks) -> int {
+            for (int off = 0; off < ntasks;) {
+                const int nb = (int)std::min<int64_t>(tmax, ntasks - off);
+                const int64_t S = (int64_t)nb * RQ_TPB;
+                int rc3 = 0;
+                char *ck =
+                    (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc3);
+                if (rc3) return rc3;
+                RqiArgs<R> A;
+                A.nodes = W.nodes;
+                A.it = W.it;
+                A.list = lst;
+                A.tasks = dtasks + off;
+                A.ck_s = (R *)ck;
+                A.ck_p = (R *)(ck + nblk * S * sizeof(R));
+                A.ck_W = (double *)(ck + 2 * nblk * S * sizeof(R));
+                A.fac = dfac;
+                A.S = S;
+                A.pivmin = ctx->pivmin;
+                A.krs = P[MR3_KRS];
+                A.eps_x = eps_x;
+                A.gaptol = gaptol;
+                A.maxit = (int)P[MR3_MAX_RQI];
+                A.jobz_v = jobz == 'V';
+                A.w = w;
+                A.Z = Z;
+                A.ldz = ldz;
+                A.zcol0 = c0;
+                A.unscale = 1.0 / ctx->scale;
+                A.st = W.st;
+                A.dbg_iters = nullptr;
+                if (ctx->debug)
+                    A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
+                KTime *t = kt_begin(ctx, locate ? "k_rqi_locate" : "k_rqi");
+                if (locate)
+                    k_rqi_locate<R><<<nb, RQ_TPB, 0, s>>>(A);
+                else
+                    k_rqi<R, OutT><<<nb, RQ_TPB, 0, s>>>(A);
+                kt_end(ctx, t);
+                cudaError_t e2 = cudaGetLastError();
+                if (e2 != cudaSuccess) {
+                    ctx->err = std::string(locate ? "k_rqi_locate: " : "k_rqi: ") +
+                               cudaGetErrorString(e2);
+                    return MR3_ERR_CUDA;
+                }
+                ctx->launches++;
+                off += nb;
+            }
+            return 0;
+        };
+        // K5a: twist indices in binary_x, then group the singletons by (node, r) so
+        // that the CTAs of the fixed-twist iterations sweep nearly equal row ranges
+        int ntasks = 0;
+        if ((rc2 = make_tasks(list, &ntasks))) return rc2;
+        if ((rc2 = launch_chunks(true, list, ntasks))) return rc2;
+        k_twist_keys<<<(ncount + 255) / 256, 256, 0, s>>>(list, ncount, W.it.node, W.it.twist,
+                                                          tkeys, tvals);
+        CKL("k_twist_keys");
+        {
+            size_t tmpb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmpb, tkeys, tkeys + ncount, tvals, slist,
+                                            ncount, 0, 64, s);
+            void *tmp = getbuf(ctx, "cubtmp_rqi", tmpb, &rc2);
+            if (rc2) return rc2;
+            cub::DeviceRadixSort::SortPairs(tmp, tmpb, tkeys, tkeys + ncount, tvals, slist,
+                                            ncount, 0, 64, s);
+            CKL("radix sort (twist)");
         }
-        return 0;
+        if ((rc2 = make_tasks(slist, &ntasks))) return rc2;
+        return launch_chunks(false, slist, ntasks);
     };
 
     auto dump = [&](const char *tag, const int32_t *list, int cntl, int lvl) {
