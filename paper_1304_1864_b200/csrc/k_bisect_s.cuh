@@ -1,0 +1,322 @@
+// k_bisect_s.cuh -- K2: batched bisection / multisection with CTA-synchronous Sturm
+// counts over shared-memory-staged representation rows.
+//
+// Same computation as the per-thread form described in k_bisect.cuh (PAPER.md
+// Alg. 1 l.3 and l.16, L302-L304, L326-L328; Eq. (2.2); rtol =
+// 1e-2 gaptol, L1294-L1295; binary_x phase L1064-L1111): a group of G lanes
+// owns one eigenvalue index k and cuts its bracket [a, b] (count(a) < k <=
+// count(b)) into G+1 parts per round.  What differs is only where the rows come
+// from: every CTA holds items of ONE representation (host-built tasks), and all
+// its threads evaluate their Sturm counts together, tile by tile, from rows
+// staged through shared memory with cp.async (double-buffered).  A count is n
+// rows for every item, so the threads of a CTA stay in step naturally; a thread
+// whose item has converged idles through the remaining rounds of its CTA.  The
+// rows come from smem at broadcast (every lane reads the same row), so the
+// dependent recurrence is never exposed to L2 latency.
+// The path of every index depends only on (representation, k, bracket, G): the
+// CTA composition changes when a thread idles, never what it computes.
+#pragma once
+#include "k_bisect.cuh"
+
+namespace mr3 {
+
+constexpr int BS_TPB = 128;  // threads per CTA
+constexpr int BS_TR = 256;   // rows per staged tile
+constexpr int BS_TILE = BS_TR * 4;  // doubles per tile buffer (rows of up to 32 B)
+
+__device__ __forceinline__ void bs_cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void bs_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void bs_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// rows [t0, t0 + BS_TR) of M_x ({d, lld} binary64, 16 B per row)
+__device__ __forceinline__ void stage_x_tile(double *buf, const double *repx, int64_t n, int64_t t0) {
+    const int rows = (int)min((int64_t)BS_TR, n - t0);
+    for (int c = threadIdx.x; c < rows; c += BS_TPB) bs_cp_async16(buf + 2 * c, repx + 2 * (t0 + c));
+    bs_commit();
+}
+// {d, lld} of rows [t0, t0 + BS_TR) of M_y (first 2 R of each 4-R row)
+template <class R>
+__device__ __forceinline__ void stage_y_tile(double *buf, const double *rep, int64_t n, int64_t t0) {
+    constexpr int W = Prec<R>::words;
+    const int rows = (int)min((int64_t)BS_TR, n - t0);
+    for (int c = threadIdx.x; c < rows * W; c += BS_TPB) {
+        const int r = c / W, off = (c % W) * 2;
+        bs_cp_async16(buf + r * 2 * W + off, rep + (t0 + r) * 4 * W + off);
+    }
+    bs_commit();
+}
+
+// body(buf, t0, rows) over all tiles; collective (every thread of the CTA calls it)
+template <class Stage, class Body>
+__device__ __forceinline__ void tile_pass(double *smem, int64_t n, Stage stage, Body body) {
+    const int ntile = (int)((n + BS_TR - 1) / BS_TR);
+    stage(smem, (int64_t)0);
+    for (int i = 0; i < ntile; i++) {
+        if (i + 1 < ntile) {
+            stage(smem + ((i + 1) & 1) * BS_TILE, (int64_t)(i + 1) * BS_TR);
+            bs_wait<1>();
+        } else {
+            bs_wait<0>();
+        }
+        __syncthreads();
+        const int64_t t0 = (int64_t)i * BS_TR;
+        body(smem + (i & 1) * BS_TILE, t0, (int)min((int64_t)BS_TR, n - t0));
+        __syncthreads();
+    }
+}
+
+template <class R>
+__device__ __forceinline__ Row2<R> yrow(const double *buf, int j);
+template <>
+__device__ __forceinline__ Row2<dd> yrow<dd>(const double *buf, int j) {
+    const double2 *p = reinterpret_cast<const double2 *>(buf + 4 * j);
+    const double2 u = p[0], v = p[1];
+    Row2<dd> r;
+    r.d = mkdd(u.x, u.y);
+    r.lld = mkdd(v.x, v.y);
+    return r;
+}
+template <>
+__device__ __forceinline__ Row2<double> yrow<double>(const double *buf, int j) {
+    const double2 u = *reinterpret_cast<const double2 *>(buf + 2 * j);
+    Row2<double> r;
+    r.d = u.x;
+    r.lld = u.y;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// CTA-collective Sturm counts (every thread calls; `need` selects who counts).
+// binary_x: projective dstqds of negcount_x (kernels.cuh), rescaled every XB rows.
+// binary_y: the guarded dstqds negcount of kernels.cuh.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, bool need, double x,
+                                           double pivmin) {
+    const int64_t n = nd.n;
+    double p = -x, q = 1.0;
+    unsigned c = 0;
+    tile_pass(
+        smem, n, [&](double *buf, int64_t t0) { stage_x_tile(buf, nd.repx, n, t0); },
+        [&](const double *buf, int64_t t0, int rows) {
+            if (!need) return;
+            const double2 *t = reinterpret_cast<const double2 *>(buf);
+            const bool last = t0 + rows == n;
+            const int full = last ? rows - 1 : rows;
+            int j = 0;
+#pragma unroll 1
+            for (; j + XB <= full; j += XB) {
+                const double p0 = p, q0 = q;
+                const unsigned c0 = c;
+#pragma unroll
+                for (int u = 0; u < XB; u++) xrow(t[j + u], x, p, q, c);
+                const unsigned ep = (unsigned)__double2hiint(p) & 0x7ff00000u;
+                const unsigned eq = (unsigned)__double2hiint(q) & 0x7ff00000u;
+                const unsigned em = ep > eq ? ep : eq;
+                if (em == 0x7ff00000u) {  // overflow: redo the block in the guarded ratio form
+                    double s = p0 / q0;
+                    if (!(fabs(s) <= 1e300)) s = copysign(1e300, s);
+                    int cc = 0;
+                    for (int u = 0; u < XB; u++) nc_row_guarded(t[j + u].x, t[j + u].y, x, pivmin, s, cc);
+                    c = c0 + (unsigned)cc;
+                    p = s;
+                    q = 1.0;
+                } else {
+                    const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+                    p = mul_rn(p, sc);
+                    q = mul_rn(q, sc);
+                }
+            }
+#pragma unroll 1
+            for (; j < full; j++) xrow(t[j], x, p, q, c);
+            if (last) {
+                const double D = fma_rn(t[rows - 1].x, q, p);
+                c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+            } else {
+                const unsigned ep = (unsigned)__double2hiint(p) & 0x7ff00000u;
+                const unsigned eq = (unsigned)__double2hiint(q) & 0x7ff00000u;
+                const unsigned em = ep > eq ? ep : eq;
+                if (em != 0x7ff00000u) {
+                    const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+                    p = mul_rn(p, sc);
+                    q = mul_rn(q, sc);
+                }
+            }
+        });
+    return (int)c;
+}
+
+template <class R>
+__device__ __forceinline__ void ystep(const Row2<R> &rw, R x, double pivmin, R &s, int &c,
+                                      bool lastrow) {
+    R dp = guard(add(rw.d, s), pivmin);
+    c += is_neg(dp) ? 1 : 0;
+    if (!lastrow) s = sub(mul(rw.lld, div(s, dp)), x);
+}
+
+// one or two shifts per thread (two: xa and xb through the same rows, ILP 2)
+template <class R, bool TWO>
+__device__ __forceinline__ void count_y_cta(double *smem, const NodeInfo &nd, bool need, R xa,
+                                            R xb, double pivmin, int &ca, int &cb) {
+    const int64_t n = nd.n;
+    R sa = neg(xa), sb = neg(xb);
+    int c0 = 0, c1 = 0;
+    tile_pass(
+        smem, n, [&](double *buf, int64_t t0) { stage_y_tile<R>(buf, nd.rep, n, t0); },
+        [&](const double *buf, int64_t t0, int rows) {
+            if (!need) return;
+            const bool last = t0 + rows == n;
+            const int full = last ? rows - 1 : rows;
+#pragma unroll 2
+            for (int j = 0; j < full; j++) {
+                const Row2<R> rw = yrow<R>(buf, j);
+                ystep<R>(rw, xa, pivmin, sa, c0, false);
+                if (TWO) ystep<R>(rw, xb, pivmin, sb, c1, false);
+            }
+            if (last) {
+                const Row2<R> rw = yrow<R>(buf, rows - 1);
+                ystep<R>(rw, xa, pivmin, sa, c0, true);
+                if (TWO) ystep<R>(rw, xb, pivmin, sb, c1, true);
+            }
+        });
+    ca = c0;
+    cb = c1;
+}
+
+// CTA-synchronous multisection rounds of the groups (see multisect in k_bisect.cuh)
+template <class T, int G, class Count>
+__device__ __forceinline__ void msect_cta(T &a, T &b, bool active, int k, int lig, int lane,
+                                          unsigned gmask, double rtol, double absfloor,
+                                          double tolmul, unsigned long long &rows, int64_t n,
+                                          Count count) {
+    bool mdone = !active;
+#pragma unroll 1
+    for (int round = 0; round < 4000; round++) {
+        T x = a;
+        bool need = false, above = false;
+        if (!mdone) {
+            T w = sub(b, a);
+            double tol = tolmul * fmax(2.0 * rtol * fmax(fabs(hi(a)), fabs(hi(b))), absfloor);
+            if (hi(w) <= tol) {
+                mdone = true;
+            } else {
+                x = add(a, mul(w, (double)(lig + 1) / (double)(G + 1)));
+                above = lt(a, x);
+                need = above && lt(x, b);
+            }
+        }
+        if (!__syncthreads_or(!mdone)) break;
+        int c = count(need, x);
+        if (!mdone) {
+            if (need)
+                rows += n;
+            else
+                c = above ? k : k - 1;  // x == b counts as right of lambda_k, x == a as left
+            bool P = c >= k;
+            unsigned bal = __ballot_sync(gmask, P);
+            bal = (bal >> (lane & ~(G - 1) & 31)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
+            int first = bal ? __ffs(bal) : G + 1;
+            T xb = shfl_R<T>(gmask, x, first <= G ? first - 1 : 0, G);
+            T xa = shfl_R<T>(gmask, x, first >= 2 ? first - 2 : 0, G);
+            T nb = first <= G ? xb : b;
+            T na = first >= 2 ? xa : a;
+            if (same(na, a) && same(nb, b)) {
+                mdone = true;  // no representable progress
+            } else {
+                a = na;
+                b = nb;
+            }
+        }
+    }
+}
+
+template <class R, int G, bool XPHASE>
+__global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict__ nodes, Items it,
+                                                  const int32_t *__restrict__ list,
+                                                  const RqiTask *__restrict__ tasks,
+                                                  const int *__restrict__ ntasks, double rtol,
+                                                  double absfloor, double pivmin, double pivmin_x,
+                                                  double eps_x, int certify, DevStats *st) {
+    __shared__ __align__(16) double sbuf[2 * BS_TILE];
+    if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
+    const RqiTask task = tasks[blockIdx.x];
+    const NodeInfo nd = nodes[task.node];
+    const int64_t n = nd.n;
+    const int local = threadIdx.x / G, lig = threadIdx.x % G;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const bool active = local < task.cnt;
+    int id = -1, k = 0;
+    R a = mk<R>(0.0), b = a;
+    if (active) {
+        id = list[task.first + local];
+        k = it.k[id];
+        a = reinterpret_cast<R *>(it.lo)[id];
+        b = reinterpret_cast<R *>(it.hi)[id];
+    }
+    unsigned long long rows = 0, rows_x = 0;
+
+    // binary_y certification: count_y(a) < k <= count_y(b); failing ends are widened
+    // (by delta, then 8x per try) until certified (k_bisect.cuh certify_bracket)
+    auto certify_y = [&](double delta) {
+        bool cdone = !active;
+#pragma unroll 1
+        for (int tries = 0; tries < 200; tries++) {
+            if (!__syncthreads_or(!cdone)) break;
+            int ca = 0, cb = 0;
+            count_y_cta<R, true>(sbuf, nd, !cdone && lig == 0, a, b, pivmin, ca, cb);
+            if (!cdone) {
+                ca = __shfl_sync(gmask, ca, 0, G);
+                cb = __shfl_sync(gmask, cb, 0, G);
+                if (lig == 0) rows += 2 * n;
+                if (ca < k && cb >= k) {
+                    cdone = true;
+                } else {
+                    double w = fmax(delta, fmax(absfloor, 1e-3 * fabs(hi(b)) * (tries > 2 ? 1.0 : 0.0)));
+                    w = w * (double)(1ULL << (3 * (tries < 20 ? tries : 20)));
+                    if (ca >= k) a = sub(a, mk<R>(w));
+                    if (cb < k) b = add(b, mk<R>(w));
+                }
+            }
+        }
+    };
+
+    if (certify) certify_y(absfloor);
+    if (XPHASE) {
+        double ax = hi(a), bx = hi(b);
+        msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x, n,
+                             [&](bool need, double x) {
+                                 return count_x_cta(sbuf, nd, need, x, pivmin_x);
+                             });
+        double delta = absfloor;
+        if (active) {
+            double mag = fmax(fabs(ax), fabs(bx));
+            delta = 8.0 * eps_x * sqrt((double)n) * mag + absfloor;
+            R na = mk<R>(ax - delta), nb = mk<R>(bx + delta);
+            if (lt(na, a)) na = a;  // never leave the certified incoming bracket
+            if (lt(b, nb)) nb = b;
+            a = na;
+            b = nb;
+        }
+        certify_y(delta);
+    }
+    msect_cta<R, G>(a, b, active, k, lig, lane, gmask, rtol, absfloor, 1.0, rows, n,
+                    [&](bool need, R x) {
+                        int c, dummy;
+                        count_y_cta<R, false>(sbuf, nd, need, x, x, pivmin, c, dummy);
+                        return c;
+                    });
+    if (active && lig == 0) {
+        reinterpret_cast<R *>(it.lo)[id] = a;
+        reinterpret_cast<R *>(it.hi)[id] = b;
+    }
+    if (rows) atomicAdd(&st->bisect_rows, rows);
+    if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
+}
+
+}  // namespace mr3

@@ -44,12 +44,6 @@ constexpr int RQ_TR = 32;    // rows per staged tile = output tile rows (4 block
 constexpr int RQ_HALO = 8;   // rows staged below a tile (the sweeps need row t0 - 1)
 constexpr int RQ_TPB = 128;  // threads per CTA
 
-struct RqiTask {
-    int32_t first;  // offset into the singleton list
-    int32_t cnt;    // eigenpairs (<= RQ_TPB)
-    int32_t node;
-    int32_t pad;
-};
 
 template <class R>
 struct RqiArgs {
@@ -733,12 +727,12 @@ __global__ void k_twist_keys(const int32_t *__restrict__ list, int cnt,
     vals[t] = id;
 }
 
-// CTA tasks for k_rqi: runs of <= RQ_TPB consecutive singletons of the same node
+// CTA tasks for k_rqi / k_bisect_s: runs of <= per consecutive items of the same node
 // (one CTA of 1024 threads; two chunked scans).
 __global__ void __launch_bounds__(1024) k_rqi_tasks(const int32_t *__restrict__ singles, int cnt,
                                                     const int32_t *__restrict__ item_node,
                                                     int32_t *seg_begin /* cnt+1 */,
-                                                    RqiTask *tasks, int *ntasks) {
+                                                    RqiTask *tasks, int *ntasks, int per) {
     __shared__ int sh[33];
     __shared__ int carry[2];
     if (threadIdx.x < 2) carry[threadIdx.x] = 0;
@@ -765,14 +759,14 @@ __global__ void __launch_bounds__(1024) k_rqi_tasks(const int32_t *__restrict__ 
         if (sgi < nseg) {
             b0 = seg_begin[sgi];
             len = seg_begin[sgi + 1] - b0;
-            nt = (len + RQ_TPB - 1) / RQ_TPB;
+            nt = (len + per - 1) / per;
         }
         int tot;
         int ex = block_excl_scan(nt, &tot, sh);
         for (int q = 0; q < nt; q++) {
             RqiTask t;
-            t.first = b0 + q * RQ_TPB;
-            t.cnt = min(RQ_TPB, len - q * RQ_TPB);
+            t.first = b0 + q * per;
+            t.cnt = min(per, len - q * per);
             t.node = item_node[singles[b0]];
             t.pad = 0;
             tasks[carry[1] + ex + q] = t;

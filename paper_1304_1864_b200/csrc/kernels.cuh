@@ -34,6 +34,15 @@ struct Items {  // eigenvalue slots, SoA over the requested index set (+ guards)
     int32_t *twist;       // RQI twist index r (0-based row of the node), from k_rqi_locate
 };
 
+// CTA task: a run of consecutive list entries (items of ONE node) for the kernels
+// that stage that node's rows through shared memory (k_bisect_s, k_rqi*)
+struct RqiTask {
+    int32_t first;  // offset into the item list
+    int32_t cnt;    // items in this CTA
+    int32_t node;
+    int32_t pad;
+};
+
 struct DevStats {
     unsigned long long bisect_rows;    // binary_y Sturm rows
     unsigned long long bisect_rows_x;  // binary_x Sturm rows (fp64 phase)

@@ -19,6 +19,7 @@
 
 #include "../../include/mr3.h"
 #include "k_bisect.cuh"
+#include "k_bisect_s.cuh"
 #include "k_child.cuh"
 #include "k_misc.cuh"
 #include "k_rqi.cuh"
@@ -198,20 +199,29 @@ template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x) {
     if (cnt <= 0) return 0;
-    const int tpb = 128;
-    long long threads = (long long)cnt * G;
-    int grid = (int)((threads + tpb - 1) / tpb);
+    int rc = 0;
+    const int per = BS_TPB / G;
+    // CTA tasks: runs of <= per items of one node; the grid is an upper bound on
+    // their number (the kernel reads the exact count), so no host round trip
+    const int64_t bound = (cnt + per - 1) / per + std::max(1, ctx->nodes_used);
+    RqiTask *dtasks = (RqiTask *)getbuf(ctx, "bis_tasks", (size_t)bound * sizeof(RqiTask), &rc);
+    int32_t *dseg = (int32_t *)getbuf(ctx, "bis_seg", (size_t)(cnt + 1) * 4, &rc);
+    int *dnt = (int *)getbuf(ctx, "bis_ntasks", 16, &rc);
+    if (rc) return rc;
+    k_rqi_tasks<<<1, 1024, 0, ctx->stream>>>(list, cnt, W.it.node, dseg, dtasks, dnt, per);
+    CKL("k_rqi_tasks");
+    const int grid = (int)bound;
     const double pivmin_x = 0x1p-900;
     KTime *t = kt_begin(ctx, "k_bisect");
 #define BIS(GG)                                                                               \
     case GG:                                                                                  \
         if (xphase)                                                                           \
-            k_bisect<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                             \
-                W.nodes, W.it, list, cnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x,       \
+            k_bisect_s<R, GG, true><<<grid, BS_TPB, 0, ctx->stream>>>(                        \
+                W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
                 certify, W.st);                                                               \
         else                                                                                  \
-            k_bisect<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                            \
-                W.nodes, W.it, list, cnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x,       \
+            k_bisect_s<R, GG, false><<<grid, BS_TPB, 0, ctx->stream>>>(                       \
+                W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
                 certify, W.st);                                                               \
         break;
     switch (G) {
@@ -761,7 +771,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         int32_t *slist = (int32_t *)getbuf(ctx, "rqi_sorted", (size_t)ncount * 4, &rc2);
         if (rc2) return rc2;
         auto make_tasks = [&](const int32_t *lst, int *nt) -> int {
-            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt);
+            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, RQ_TPB);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
                 ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
