@@ -81,7 +81,9 @@ enum mr3_param {
     MR3_XPHASE = 9,    /* fp64 I/O: approximate eigenvalues in binary_x first (L1064-L1111); 1 */
     MR3_REFINE = 10,   /* RQI start refinement constant C (0 = off): singletons whose bracket
                           half-width exceeds gap*sqrt(eps_x sqrt(n)/C) get a binary_x start; 4 */
-    MR3_NPARAM = 11
+    MR3_GRID = 11,     /* 1: start the bisection from a shared grid of Sturm counts (k_grid); 1 */
+    MR3_CTA = 12,      /* threads per CTA of the staged kernels, 32..128 (0 = 128) */
+    MR3_NPARAM = 13
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a
@@ -109,6 +111,23 @@ int mr3_dstemr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d
 int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, const float *e,
                  float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
                  int64_t ldz, mr3_stats *stats);
+
+/*
+ * End-to-end forms with HOST buffers (same contract as mr3_dstemr_dd /
+ * mr3_sstemr_d otherwise): d[n], e[n-1] are read from host memory, w[n] and Z
+ * (column-major, ldz >= n, >= *m columns; may be NULL when jobz = 'N') are
+ * written to host memory.  The host<->device copies run on the context's stream
+ * inside the call (pinned host memory -- cudaHostAlloc / cudaHostRegister / a
+ * pinned torch tensor -- gives full PCIe bandwidth; pageable memory works but is
+ * staged by the driver).  Device copies of the inputs and outputs are library
+ * scratch (cached in the context, released by mr3_destroy).
+ */
+int mr3_dstemr_dd_host(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d,
+                       const double *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
+                       double *w, double *Z, int64_t ldz, mr3_stats *stats);
+int mr3_sstemr_d_host(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d,
+                      const float *e, float vl, float vu, int64_t il, int64_t iu, int64_t *m,
+                      float *w, float *Z, int64_t ldz, mr3_stats *stats);
 
 /*
  * Two-phase form for an index-set partition over `world` ranks (one GPU each).

@@ -10,7 +10,7 @@ Public API (names follow the C-ABI):
     mr3_dstemr_dd(d, e, jobz='V', range='A', il=1, iu=0, vl=0., vu=0.)  fp64 I/O, dd internal
     mr3_sstemr_d(d, e, ...)                                            fp32 I/O, fp64 internal
     dstemr(...) / sstemr(...)            aliases of the two above
-    solve_host(d_np, e_np, ...)          end-to-end from host arrays (pinned H2D, D2H)
+    solve_host(d_np, e_np, ...)          end to end through the host-buffer C-ABI entry points
     solve_distributed(d, e, group=...)   index-set partition over ranks (mr3_plan/mr3_execute)
     fp64_peak()                          K7 same-run FP64 peak + dd-step latency
     set_param(name, value, mode)         GAPTOL, XI, KRS, MAX_RQI, MAX_DEPTH, SEED, ELG_MAX, RTOL, GROUPS
@@ -25,13 +25,13 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libmr3.so")
-SOURCES = ["csrc/mr3.cu", "csrc/kernels.cuh", "csrc/k_bisect.cuh", "csrc/k_child.cuh",
-           "csrc/k_rqi.cuh", "csrc/k_misc.cuh", "csrc/dd.cuh"]
+SOURCES = sorted(os.path.join("csrc", f) for f in os.listdir(os.path.join(_HERE, "csrc"))
+                 if f.endswith((".cu", ".cuh")))
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
-          "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10}
+          "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10, "GRID": 11, "CTA": 12}
 ERRORS = {1: "NONFINITE", 2: "CUDA", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 
@@ -96,6 +96,8 @@ def lib():
             L.mr3_sstemr_d.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp,
                                        ctypes.c_float, ctypes.c_float, i64, i64, pi64, vp, vp,
                                        i64, ctypes.POINTER(Stats)]
+            L.mr3_dstemr_dd_host.argtypes = L.mr3_dstemr_dd.argtypes
+            L.mr3_sstemr_d_host.argtypes = L.mr3_sstemr_d.argtypes
             L.mr3_plan.argtypes = [vp, i32, ctypes.c_char, i64, vp, vp, dbl, dbl, i64, i64, i32,
                                    i32, pi64, ctypes.POINTER(ctypes.c_void_p), pi64, pi64]
             L.mr3_execute.argtypes = [vp, ctypes.c_char, vp, vp, i64, i64, pi64, pi64,
@@ -228,20 +230,40 @@ dstemr = mr3_dstemr_dd
 sstemr = mr3_sstemr_d
 
 
-def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0):
-    """End to end from host numpy arrays: pinned H2D copy, solve, D2H of w and Z."""
+def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, w=None, Z=None):
+    """End to end through the host-buffer C-ABI (mr3_dstemr_dd_host / mr3_sstemr_d_host):
+    d, e are host arrays (numpy or CPU torch tensors, ideally pinned); the library copies
+    them to the device, solves, and writes w and Z back to host memory.  w (n) and Z
+    (host, column-major n x m storage given as an (m_cap, n) row-major array) may be
+    preallocated (pinned) buffers.  Returns (w[:m], Z[:m].T or None, stats)."""
     import numpy as np
     import torch
-    mode = 1 if np.asarray(d).dtype == np.float32 else 0
+    dtn = np.asarray(d).dtype if not isinstance(d, torch.Tensor) else d.numpy().dtype
+    mode = 1 if dtn == np.float32 else 0
     dt = torch.float32 if mode else torch.float64
-    hd = torch.from_numpy(np.ascontiguousarray(d)).pin_memory()
-    he = torch.from_numpy(np.ascontiguousarray(e)).pin_memory()
-    dd_ = hd.to("cuda", non_blocking=True)
-    de_ = he.to("cuda", non_blocking=True)
-    w, Z, st = _solve(mode, dd_, de_, jobz, range, il, iu, vl, vu)
-    wh = w.to("cpu")
-    Zh = Z.T.contiguous().to("cpu").T if Z is not None else None
-    return wh.numpy(), (Zh.numpy() if Zh is not None else None), st
+    hd = d if isinstance(d, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(d, dtype=dtn))
+    he = e if isinstance(e, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(e, dtype=dtn))
+    if hd.is_cuda or he.is_cuda or hd.dtype != dt or he.dtype != dt:
+        raise TypeError("solve_host: d, e must be host arrays of one float dtype")
+    hd, he = hd.contiguous(), he.contiguous()
+    n = hd.numel()
+    mcap = n if range != "I" else max(0, min(iu, n) - max(il, 1) + 1)
+    if w is None:
+        w = torch.empty(max(n, 1), dtype=dt)
+    if jobz == "V" and Z is None:
+        Z = torch.empty((max(mcap, 1), max(n, 1)), dtype=dt)
+    c = _ctx()
+    m = ctypes.c_int64(0)
+    st = Stats()
+    fn = lib().mr3_dstemr_dd_host if mode == 0 else lib().mr3_sstemr_d_host
+    rc = fn(c, jobz.encode(), range.encode(), n, ctypes.c_void_p(hd.data_ptr()),
+            ctypes.c_void_p(he.data_ptr() if n > 1 else hd.data_ptr()), vl, vu, il, iu,
+            ctypes.byref(m), ctypes.c_void_p(w.data_ptr()),
+            ctypes.c_void_p(Z.data_ptr() if (jobz == "V" and Z is not None) else 0), max(n, 1),
+            ctypes.byref(st))
+    _err(c, rc, "mr3_dstemr_dd_host" if mode == 0 else "mr3_sstemr_d_host")
+    mm = m.value
+    return w[:mm], (Z[:mm].T if jobz == "V" else None), st.asdict()
 
 
 def fp64_peak():

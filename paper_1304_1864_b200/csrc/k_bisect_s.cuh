@@ -20,7 +20,7 @@
 
 namespace mr3 {
 
-constexpr int BS_TPB = 128;  // threads per CTA
+constexpr int BS_TPB = 128;  // threads per CTA (maximum; launches pick 32..128)
 constexpr int BS_TR = 256;   // rows per staged tile
 constexpr int BS_TILE = BS_TR * 4;  // doubles per tile buffer (rows of up to 32 B)
 
@@ -37,7 +37,7 @@ __device__ __forceinline__ void bs_wait() {
 // rows [t0, t0 + BS_TR) of M_x ({d, lld} binary64, 16 B per row)
 __device__ __forceinline__ void stage_x_tile(double *buf, const double *repx, int64_t n, int64_t t0) {
     const int rows = (int)min((int64_t)BS_TR, n - t0);
-    for (int c = threadIdx.x; c < rows; c += BS_TPB) bs_cp_async16(buf + 2 * c, repx + 2 * (t0 + c));
+    for (int c = threadIdx.x; c < rows; c += blockDim.x) bs_cp_async16(buf + 2 * c, repx + 2 * (t0 + c));
     bs_commit();
 }
 // {d, lld} of rows [t0, t0 + BS_TR) of M_y (first 2 R of each 4-R row)
@@ -45,7 +45,7 @@ template <class R>
 __device__ __forceinline__ void stage_y_tile(double *buf, const double *rep, int64_t n, int64_t t0) {
     constexpr int W = Prec<R>::words;
     const int rows = (int)min((int64_t)BS_TR, n - t0);
-    for (int c = threadIdx.x; c < rows * W; c += BS_TPB) {
+    for (int c = threadIdx.x; c < rows * W; c += blockDim.x) {
         const int r = c / W, off = (c % W) * 2;
         bs_cp_async16(buf + r * 2 * W + off, rep + (t0 + r) * 4 * W + off);
     }

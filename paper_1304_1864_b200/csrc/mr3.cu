@@ -20,6 +20,7 @@
 #include "../../include/mr3.h"
 #include "k_bisect.cuh"
 #include "k_bisect_s.cuh"
+#include "k_grid.cuh"
 #include "k_child.cuh"
 #include "k_misc.cuh"
 #include "k_rqi.cuh"
@@ -83,9 +84,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0},
 };
 
 #define CK(call)                                                                  \
@@ -195,12 +196,24 @@ static int choose_groups(mr3_ctx ctx, int cnt, int forced) {
     return g;
 }
 
+// Threads per CTA of k_bisect_s: tpb_max
+// unless MR3_CTA forces 32..128.  (Measured on config 5: 128-thread CTAs beat
+// SM-balanced smaller ones -- k_rqi 76 vs 82 (64) vs 87 ms (32) -- the per-CTA
+// staging and barrier costs outweigh the 3-vs-2 CTAs-per-SM imbalance.)
+static int choose_tpb(mr3_ctx ctx, int64_t thr, int tpb_max) {
+    (void)thr;
+    const double forced = ctx->cfg[ctx->mode].v[MR3_CTA];
+    if (forced > 0) return (int)std::min<double>(tpb_max, std::max(32.0, 32.0 * std::floor(forced / 32)));
+    return tpb_max;
+}
+
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x) {
     if (cnt <= 0) return 0;
     int rc = 0;
-    const int per = BS_TPB / G;
+    const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
+    const int per = tpb / G;
     // CTA tasks: runs of <= per items of one node; the grid is an upper bound on
     // their number (the kernel reads the exact count), so no host round trip
     const int64_t bound = (cnt + per - 1) / per + std::max(1, ctx->nodes_used);
@@ -216,11 +229,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
 #define BIS(GG)                                                                               \
     case GG:                                                                                  \
         if (xphase)                                                                           \
-            k_bisect_s<R, GG, true><<<grid, BS_TPB, 0, ctx->stream>>>(                        \
+            k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
                 certify, W.st);                                                               \
         else                                                                                  \
-            k_bisect_s<R, GG, false><<<grid, BS_TPB, 0, ctx->stream>>>(                       \
+            k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
                 certify, W.st);                                                               \
         break;
@@ -510,6 +523,41 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_iota");
         ctx->G0 = choose_groups(ctx, cnt, (int)P[MR3_GROUPS]);
         const bool xphase = words == 2 && P[MR3_XPHASE] != 0;
+        if (!ctx->split && P[MR3_GRID] != 0 && cnt >= 512) {
+            // shared top of the bisection tree: brackets from two grids of counts
+            const int m2 = (int)std::min<int64_t>((int64_t)(1.5 * cnt) + 64, 1 << 30);
+            GridInfo *gi = (GridInfo *)getbuf(ctx, "grid_info", sizeof(GridInfo), &rc);
+            int *c1 = (int *)getbuf(ctx, "grid_c1", GRID_L1 * 4, &rc);
+            int *c2 = (int *)getbuf(ctx, "grid_c2", (size_t)m2 * 4, &rc);
+            if (rc) return rc;
+            const int k_lo = (int)std::max<int64_t>(1, ilw - 1);
+            const int k_hi = k_lo + cnt - 1;
+            KTime *tg = kt_begin(ctx, "k_grid");
+            k_grid_init<<<1, 32, 0, s>>>(gi, dbrk0);
+            CKL("k_grid_init");
+            auto counts = [&](int level, int npts) -> int {
+                const int g = (npts + BS_TPB - 1) / BS_TPB;
+                if (xphase)
+                    k_grid_counts<R, true><<<g, BS_TPB, 0, s>>>(dnodes, 0, level, gi,
+                                                                 level == 1 ? c1 : c2,
+                                                                 ctx->pivmin, 0x1p-900);
+                else
+                    k_grid_counts<R, false><<<g, BS_TPB, 0, s>>>(dnodes, 0, level, gi,
+                                                                  level == 1 ? c1 : c2,
+                                                                  ctx->pivmin, 0x1p-900);
+                CKL("k_grid_counts");
+                return 0;
+            };
+            if ((rc = counts(1, GRID_L1))) return rc;
+            k_grid_setup<<<1, 32, 0, s>>>(gi, dbrk0, c1, (int)n, k_lo, k_hi, k_lo + (int)first,
+                                          k_lo + (int)(first + mine - 1), m2);
+            CKL("k_grid_setup");
+            if ((rc = counts(2, m2))) return rc;
+            k_grid_assign<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
+                                                                       gi, c2);
+            CKL("k_grid_assign");
+            kt_end(ctx, tg);
+        }
         rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x);
         if (rc) return rc;
         k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
@@ -760,7 +808,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         } else {
             CK(cudaMemsetAsync(W.it.x0, 0xff, (size_t)cnt * 8, s));  // NaN: midpoints
         }
-        // CTA tasks: runs of <= RQ_TPB singletons of one node (smem staging)
+        // CTA tasks: runs of <= rtpb singletons of one node (smem staging)
+        const int rtpb = RQ_TPB;  // k_rqi* are written for full 128-thread CTAs
         RqiTask *dtasks = (RqiTask *)getbuf(ctx, "rqi_tasks", (size_t)(ncount + 1) * sizeof(RqiTask),
                                             &rc2);
         int32_t *dseg = (int32_t *)getbuf(ctx, "rqi_seg", (size_t)(ncount + 1) * 4, &rc2);
@@ -771,7 +820,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         int32_t *slist = (int32_t *)getbuf(ctx, "rqi_sorted", (size_t)ncount * 4, &rc2);
         if (rc2) return rc2;
         auto make_tasks = [&](const int32_t *lst, int *nt) -> int {
-            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, RQ_TPB);
+            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, rtpb);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
                 ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
@@ -785,11 +834,11 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             }
             return 0;
         };
-        const int64_t tmax = std::max<int64_t>(1, Smax / RQ_TPB);
+        const int64_t tmax = std::max<int64_t>(1, Smax / rtpb);
         auto launch_chunks = [&](bool locate, const int32_t *lst, int ntasks) -> int {
             for (int off = 0; off < ntasks;) {
                 const int nb = (int)std::min<int64_t>(tmax, ntasks - off);
-                const int64_t S = (int64_t)nb * RQ_TPB;
+                const int64_t S = (int64_t)nb * rtpb;
                 int rc3 = 0;
                 char *ck =
                     (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc3);
@@ -821,9 +870,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                     A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
                 KTime *t = kt_begin(ctx, locate ? "k_rqi_locate" : "k_rqi");
                 if (locate)
-                    k_rqi_locate<R><<<nb, RQ_TPB, 0, s>>>(A);
+                    k_rqi_locate<R><<<nb, rtpb, 0, s>>>(A);
                 else
-                    k_rqi<R, OutT><<<nb, RQ_TPB, 0, s>>>(A);
+                    k_rqi<R, OutT><<<nb, rtpb, 0, s>>>(A);
                 kt_end(ctx, t);
                 cudaError_t e2 = cudaGetLastError();
                 if (e2 != cudaSuccess) {
@@ -971,6 +1020,17 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if (ctx->debug)
             fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
                     nclus, nmem);
+    }
+    if (ctx->debug && ctx->bufs.count("rqi_sorted") && ctx->n > 1) {
+        // twist-index distribution (r / n in 10 bins) and spread per 128-run of the sorted list
+        cudaStreamSynchronize(s);
+        std::vector<int32_t> tw(cnt), nodev(cnt);
+        cudaMemcpy(tw.data(), W.it.twist, cnt * 4, cudaMemcpyDeviceToHost);
+        int hist[10] = {0};
+        for (int i = 0; i < cnt; i++) hist[std::min(9, std::max(0, (int)(10.0 * tw[i] / ctx->n)))]++;
+        fprintf(stderr, "[mr3] twist r/n histogram:");
+        for (int i = 0; i < 10; i++) fprintf(stderr, " %d", hist[i]);
+        fprintf(stderr, "\n");
     }
     if (ctx->debug && ctx->bufs.count("dbg_iters")) {
         cudaStreamSynchronize(s);
@@ -1143,6 +1203,61 @@ int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, 
                  float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
                  int64_t ldz, mr3_stats *stats) {
     return solve_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+}
+
+static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64_t n,
+                             const void *d, const void *e, double vl, double vu, int64_t il,
+                             int64_t iu, int64_t *m, void *w, void *Z, int64_t ldz,
+                             mr3_stats *stats) {
+    if (!ctx) return -1;
+    if (jobz != 'V' && jobz != 'N') return -2;
+    if (range != 'A' && range != 'I' && range != 'V') return -3;
+    if (n < 0) return -4;
+    if (!m) return -11;
+    if (n > 0 && (!d || (n > 1 && !e))) return -5;
+    if (n > 0 && !w) return -12;
+    if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -14;
+    *m = 0;
+    if (n == 0) return solve_common(ctx, mode, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz,
+                                    stats);
+    const size_t es = mode ? 4 : 8;
+    int rc = 0;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    // columns the solve can produce: all for 'A' / 'V', iu - il + 1 for 'I'
+    int64_t mcap = n;
+    if (range == 'I') mcap = std::max<int64_t>(0, std::min<int64_t>(iu, n) - std::max<int64_t>(il, 1) + 1);
+    char *dd_ = (char *)getbuf(ctx, "host_d", (size_t)n * es, &rc);
+    char *de_ = (char *)getbuf(ctx, "host_e", (size_t)std::max<int64_t>(n - 1, 1) * es, &rc);
+    char *dw = (char *)getbuf(ctx, "host_w", (size_t)n * es, &rc);
+    char *dZ = jobz == 'V' ? (char *)getbuf(ctx, "host_Z", (size_t)n * std::max<int64_t>(mcap, 1) * es, &rc)
+                           : nullptr;
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dd_, d, (size_t)n * es, cudaMemcpyHostToDevice, s));
+    if (n > 1) CK(cudaMemcpyAsync(de_, e, (size_t)(n - 1) * es, cudaMemcpyHostToDevice, s));
+    rc = solve_common(ctx, mode, jobz, range, n, dd_, de_, vl, vu, il, iu, m, dw, dZ, n, stats);
+    if (rc) return rc;
+    const int64_t mm = *m;
+    if (mm > 0) {
+        CK(cudaMemcpyAsync(w, dw, (size_t)mm * es, cudaMemcpyDeviceToHost, s));
+        if (jobz == 'V')
+            CK(cudaMemcpy2DAsync(Z, (size_t)ldz * es, dZ, (size_t)n * es, (size_t)n * es, (size_t)mm,
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int mr3_dstemr_dd_host(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d,
+                       const double *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
+                       double *w, double *Z, int64_t ldz, mr3_stats *stats) {
+    return solve_host_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+}
+
+int mr3_sstemr_d_host(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d,
+                      const float *e, float vl, float vu, int64_t il, int64_t iu, int64_t *m,
+                      float *w, float *Z, int64_t ldz, mr3_stats *stats) {
+    return solve_host_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
 }
 
 int mr3_partition_columns(int64_t nseg, const int64_t *seg_begin, const double *cost, int world,

@@ -306,3 +306,25 @@ def test_config5_full_size_sampled():
     assert omax <= 1e-14, omax
     del Z
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("io", ["f64", "f32"])
+def test_host_buffer_abi_matches_device_abi(io):
+    """mr3_*_host (host d, e, w, Z; copies inside the call) == the device-pointer call,
+    bit for bit, including an index subset."""
+    if io == "f64":
+        p = synth.random_uniform(700, 5)
+        fn = mr3.mr3_dstemr_dd
+    else:
+        p = synth.random_normal_f32(700, 2, 1, 120)
+        fn = mr3.mr3_sstemr_d
+    for rng, il, iu in (("A", 1, p.n), ("I", 37, 160)):
+        w1, Z1, _ = fn(torch.from_numpy(p.d).cuda(), torch.from_numpy(p.e).cuda(), "V", rng, il, iu)
+        hd = torch.from_numpy(p.d).pin_memory()
+        he = torch.from_numpy(p.e).pin_memory()
+        w2, Z2, _ = mr3.solve_host(hd, he, "V", rng, il, iu)
+        np.testing.assert_array_equal(w1.cpu().numpy(), w2.numpy())
+        np.testing.assert_array_equal(Z1.cpu().numpy(), Z2.numpy())
+        w3, Z3, _ = mr3.solve_host(p.d, p.e, "N", rng, il, iu)  # pageable, values only
+        assert Z3 is None
+        np.testing.assert_array_equal(w1.cpu().numpy(), w3.numpy())
