@@ -286,6 +286,7 @@ def main():
                          "launches_per_step": kb_n / args.steps},
             "kernels": kt,
             "dd_step_latency_ns": dd_step_ns,
+            "step_ms": [round(t, 3) for t in times],
             "gpu_launches": launches,
             "stats": {k: v for k, v in (stats or {}).items()},
             "clocks": clk.summary(),

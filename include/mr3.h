@@ -83,7 +83,8 @@ enum mr3_param {
                           half-width exceeds gap*sqrt(eps_x sqrt(n)/C) get a binary_x start; 4 */
     MR3_GRID = 11,     /* 1: start the bisection from a shared grid of Sturm counts (k_grid); 1 */
     MR3_CTA = 12,      /* threads per CTA of the staged kernels, 32..128 (0 = 128) */
-    MR3_NPARAM = 13
+    MR3_XPTS = 13,     /* binary_x multisection points per lane and round, 1 or 2; 1 */
+    MR3_NPARAM = 14
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

@@ -154,6 +154,23 @@ MR3_HD dd div(dd a, dd b) {
     double h = quick_two_sum(q1, q2, l);
     return mkdd(h, l);
 }
+// a * b + c in pair arithmetic (one two-prod, one two-sum; error ~ eps_y (|a b| + |c|))
+MR3_HD dd fma_dd(dd a, dd b, dd c) {
+    double p = mul_rn(a.hi, b.hi);
+    double e = fma_rn(a.hi, b.hi, -p);
+    e = fma_rn(a.hi, b.lo, e);
+    e = fma_rn(a.lo, b.hi, e);
+    double s2;
+    double s = two_sum(p, c.hi, s2);
+    s2 = add_rn(s2, add_rn(e, c.lo));
+    double l;
+    s = quick_two_sum(s, s2, l);
+    return mkdd(s, l);
+}
+MR3_HD double fma_dd(double a, double b, double c) { return fma_rn(a, b, c); }
+// exact scaling by a power of two
+MR3_HD dd scale_pow2(dd a, double sc) { return mkdd(mul_rn(a.hi, sc), mul_rn(a.lo, sc)); }
+MR3_HD double scale_pow2(double a, double sc) { return mul_rn(a, sc); }
 MR3_HD dd half(dd a) { return mkdd(0.5 * a.hi, 0.5 * a.lo); }
 MR3_HD double hi(dd a) { return a.hi; }
 MR3_HD double lo_part(dd a) { return a.lo; }

@@ -94,7 +94,8 @@ __device__ __forceinline__ Row2<double> yrow<double>(const double *buf, int j) {
 // ---------------------------------------------------------------------------
 // CTA-collective Sturm counts (every thread calls; `need` selects who counts).
 // binary_x: projective dstqds of negcount_x (kernels.cuh), rescaled every XB rows.
-// binary_y: the guarded dstqds negcount of kernels.cuh.
+// binary_y: projective dstqds in R (below); the guarded ratio form of kernels.cuh
+// only as the overflow fallback.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, bool need, double x,
                                            double pivmin) {
@@ -151,12 +152,135 @@ __device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, boo
     return (int)c;
 }
 
+// binary_y Sturm count in the projective (division-free) form of negcount_x,
+// carried out in R (pair arithmetic for fp64 I/O): with s_j = p_j / q_j,
+//   D_j = d_j q_j + p_j,  q_{j+1} = D_j,  p_{j+1} = lld_j p_j - x D_j,
+//   d+_j < 0  <=>  sign(D_j) != sign(q_j).
+// Each step is a relative perturbation of O(eps_y) of d_j, lld_j, x and the
+// state, like the dstqds it rewrites (no division, so no pivot guard is needed:
+// D_j = 0 gives q_{j+1} = 0, i.e. s_{j+1} = inf, which the next row absorbs);
+// per row two pair FMAs and one pair product, a dependent chain of two FMAs.
+// (p, q) is rescaled by an exact power of two every XB rows; an overflow (only
+// possible for |lld| > 1e38) redoes the block in the guarded ratio form.
+// two shifts per thread through the same rows (two independent FMA chains: the
+// binary_x row chain is two dependent DFMAs, so one chain per thread leaves the
+// FP64 pipe waiting on latency at the 2-3 warps per scheduler a 50000-item
+// launch provides)
+__device__ __forceinline__ bool xrescale(double &p, double &q) {
+    const unsigned ep = (unsigned)__double2hiint(p) & 0x7ff00000u;
+    const unsigned eq = (unsigned)__double2hiint(q) & 0x7ff00000u;
+    const unsigned em = ep > eq ? ep : eq;
+    if (em == 0x7ff00000u) return false;
+    const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+    p = mul_rn(p, sc);
+    q = mul_rn(q, sc);
+    return true;
+}
+// (overflow path, inlined: a non-inline callee taking references would force the
+// hot recurrence state into local memory)
+__device__ __forceinline__ void xblock_ratio(const double2 *t, int j0, int j1, double x,
+                                             double pivmin, double &p, double &q, unsigned &c) {
+    double s = p / q;
+    if (!(fabs(s) <= 1e300)) s = copysign(1e300, s);
+    int cc = 0;
+    for (int u = j0; u < j1; u++) nc_row_guarded(t[u].x, t[u].y, x, pivmin, s, cc);
+    c += (unsigned)cc;
+    p = s;
+    q = 1.0;
+}
+__device__ __forceinline__ void count_x2_cta(double *smem, const NodeInfo &nd, bool need, double xa,
+                                             double xb, double pivmin, int &ca, int &cb) {
+    const int64_t n = nd.n;
+    double pa = -xa, qa = 1.0, pb = -xb, qb = 1.0;
+    unsigned c0 = 0, c1 = 0;
+    tile_pass(
+        smem, n, [&](double *buf, int64_t t0) { stage_x_tile(buf, nd.repx, n, t0); },
+        [&](const double *buf, int64_t t0, int rows) {
+            if (!need) return;
+            const double2 *t = reinterpret_cast<const double2 *>(buf);
+            const bool last = t0 + rows == n;
+            const int full = last ? rows - 1 : rows;
+            int j = 0;
+#pragma unroll 1
+            for (; j < full; j += XB) {
+                const int je = min(j + XB, full);
+                const double pa0 = pa, qa0 = qa, pb0 = pb, qb0 = qb;
+                const unsigned ca0 = c0, cb0 = c1;
+                if (je - j == XB) {
+#pragma unroll
+                    for (int u = 0; u < XB; u++) {
+                        const double2 r = t[j + u];
+                        xrow(r, xa, pa, qa, c0);
+                        xrow(r, xb, pb, qb, c1);
+                    }
+                } else {
+                    for (int u = j; u < je; u++) {
+                        xrow(t[u], xa, pa, qa, c0);
+                        xrow(t[u], xb, pb, qb, c1);
+                    }
+                }
+                if (!xrescale(pa, qa)) {
+                    pa = pa0;
+                    qa = qa0;
+                    c0 = ca0;
+                    xblock_ratio(t, j, je, xa, pivmin, pa, qa, c0);
+                }
+                if (!xrescale(pb, qb)) {
+                    pb = pb0;
+                    qb = qb0;
+                    c1 = cb0;
+                    xblock_ratio(t, j, je, xb, pivmin, pb, qb, c1);
+                }
+            }
+            if (last) {
+                const double Da = fma_rn(t[rows - 1].x, qa, pa);
+                c0 += (unsigned)(__double2hiint(Da) ^ __double2hiint(qa)) >> 31;
+                const double Db = fma_rn(t[rows - 1].x, qb, pb);
+                c1 += (unsigned)(__double2hiint(Db) ^ __double2hiint(qb)) >> 31;
+            }
+        });
+    ca = (int)c0;
+    cb = (int)c1;
+}
+
 template <class R>
-__device__ __forceinline__ void ystep(const Row2<R> &rw, R x, double pivmin, R &s, int &c,
-                                      bool lastrow) {
-    R dp = guard(add(rw.d, s), pivmin);
-    c += is_neg(dp) ? 1 : 0;
-    if (!lastrow) s = sub(mul(rw.lld, div(s, dp)), x);
+struct YState {
+    R p, q;
+    int c;
+};
+template <class R>
+__device__ __forceinline__ void yrow_proj(const Row2<R> &rw, R mx, YState<R> &st) {
+    const R D = fma_dd(rw.d, st.q, st.p);
+    st.c += (int)((unsigned)(__double2hiint(hi(D)) ^ __double2hiint(hi(st.q))) >> 31);
+    st.p = fma_dd(mx, D, mul(rw.lld, st.p));
+    st.q = D;
+}
+template <class R>
+__device__ __forceinline__ bool yrescale(YState<R> &st) {
+    const unsigned ep = (unsigned)__double2hiint(hi(st.p)) & 0x7ff00000u;
+    const unsigned eq = (unsigned)__double2hiint(hi(st.q)) & 0x7ff00000u;
+    const unsigned em = ep > eq ? ep : eq;
+    if (em == 0x7ff00000u || !(fabs(lo_part(st.p)) < INFINITY) || !(fabs(lo_part(st.q)) < INFINITY))
+        return false;
+    const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+    st.p = scale_pow2(st.p, sc);
+    st.q = scale_pow2(st.q, sc);
+    return true;
+}
+// rows [j0, j1) of a tile in the guarded ratio form from a saved state (overflow path)
+template <class R>
+__device__ __forceinline__ void yblock_ratio(const double *buf, int j0, int j1, R x, double pivmin,
+                                          YState<R> &st) {
+    R s = div(st.p, st.q);
+    if (!(fabs(hi(s)) <= 1e300)) s = mk<R>(copysign(1e300, hi(s)));
+    for (int j = j0; j < j1; j++) {
+        const Row2<R> rw = yrow<R>(buf, j);
+        R dp = guard(add(rw.d, s), pivmin);
+        st.c += is_neg(dp) ? 1 : 0;
+        s = sub(mul(rw.lld, div(s, dp)), x);
+    }
+    st.p = s;
+    st.q = mk<R>(1.0);
 }
 
 // one or two shifts per thread (two: xa and xb through the same rows, ILP 2)
@@ -164,28 +288,54 @@ template <class R, bool TWO>
 __device__ __forceinline__ void count_y_cta(double *smem, const NodeInfo &nd, bool need, R xa,
                                             R xb, double pivmin, int &ca, int &cb) {
     const int64_t n = nd.n;
-    R sa = neg(xa), sb = neg(xb);
-    int c0 = 0, c1 = 0;
+    const R ma = neg(xa), mb = neg(xb);
+    YState<R> A{ma, mk<R>(1.0), 0}, B{mb, mk<R>(1.0), 0};
     tile_pass(
         smem, n, [&](double *buf, int64_t t0) { stage_y_tile<R>(buf, nd.rep, n, t0); },
         [&](const double *buf, int64_t t0, int rows) {
             if (!need) return;
             const bool last = t0 + rows == n;
             const int full = last ? rows - 1 : rows;
-#pragma unroll 2
-            for (int j = 0; j < full; j++) {
-                const Row2<R> rw = yrow<R>(buf, j);
-                ystep<R>(rw, xa, pivmin, sa, c0, false);
-                if (TWO) ystep<R>(rw, xb, pivmin, sb, c1, false);
+            int j = 0;
+#pragma unroll 1
+            for (; j < full; j += XB) {
+                const int je = min(j + XB, full);
+                const YState<R> A0 = A, B0 = B;
+                if (je - j == XB) {
+#pragma unroll
+                    for (int u = 0; u < XB; u++) {
+                        const Row2<R> rw = yrow<R>(buf, j + u);
+                        yrow_proj<R>(rw, ma, A);
+                        if (TWO) yrow_proj<R>(rw, mb, B);
+                    }
+                } else {
+                    for (int u = j; u < je; u++) {
+                        const Row2<R> rw = yrow<R>(buf, u);
+                        yrow_proj<R>(rw, ma, A);
+                        if (TWO) yrow_proj<R>(rw, mb, B);
+                    }
+                }
+                if (!yrescale(A)) {
+                    A = A0;
+                    yblock_ratio<R>(buf, j, je, xa, pivmin, A);
+                }
+                if (TWO && !yrescale(B)) {
+                    B = B0;
+                    yblock_ratio<R>(buf, j, je, xb, pivmin, B);
+                }
             }
             if (last) {
                 const Row2<R> rw = yrow<R>(buf, rows - 1);
-                ystep<R>(rw, xa, pivmin, sa, c0, true);
-                if (TWO) ystep<R>(rw, xb, pivmin, sb, c1, true);
+                const R D = fma_dd(rw.d, A.q, A.p);
+                A.c += (int)((unsigned)(__double2hiint(hi(D)) ^ __double2hiint(hi(A.q))) >> 31);
+                if (TWO) {
+                    const R E = fma_dd(rw.d, B.q, B.p);
+                    B.c += (int)((unsigned)(__double2hiint(hi(E)) ^ __double2hiint(hi(B.q))) >> 31);
+                }
             }
         });
-    ca = c0;
-    cb = c1;
+    ca = A.c;
+    cb = B.c;
 }
 
 // CTA-synchronous multisection rounds of the groups (see multisect in k_bisect.cuh)
@@ -235,13 +385,78 @@ __device__ __forceinline__ void msect_cta(T &a, T &b, bool active, int k, int li
     }
 }
 
+// Same, with two points per lane: a group of G lanes cuts [a, b] into 2G + 1
+// parts per round (lane l evaluates points 2l+1 and 2l+2).  The new bracket is
+// [x_{f-1}, x_f] for the first point f whose count is >= k, so count(x_{f-1}) < k
+// <= count(x_f) holds whatever the monotonicity of the rounded counts.
+template <int G, class Count2>
+__device__ __forceinline__ void msect2_cta(double &a, double &b, bool active, int k, int lig,
+                                           int lane, unsigned gmask, double rtol, double absfloor,
+                                           double tolmul, unsigned long long &rows, int64_t n,
+                                           Count2 count2) {
+    bool mdone = !active;
+    constexpr int NPT = 2 * G;
+#pragma unroll 1
+    for (int round = 0; round < 4000; round++) {
+        double x0 = a, x1 = a;
+        bool n0 = false, n1 = false, ab0 = false, ab1 = false;
+        if (!mdone) {
+            const double w = b - a;
+            const double tol = tolmul * fmax(2.0 * rtol * fmax(fabs(a), fabs(b)), absfloor);
+            if (w <= tol) {
+                mdone = true;
+            } else {
+                x0 = a + w * ((double)(2 * lig + 1) / (double)(NPT + 1));
+                x1 = a + w * ((double)(2 * lig + 2) / (double)(NPT + 1));
+                ab0 = a < x0;
+                n0 = ab0 && x0 < b;
+                ab1 = a < x1;
+                n1 = ab1 && x1 < b;
+            }
+        }
+        if (!__syncthreads_or(!mdone)) break;
+        int c0 = 0, c1 = 0;
+        count2(n0 || n1, x0, x1, c0, c1);
+        if (!mdone) {
+            rows += (unsigned long long)((n0 ? 1 : 0) + (n1 ? 1 : 0)) * n;
+            if (!n0) c0 = ab0 ? k : k - 1;
+            if (!n1) c1 = ab1 ? k : k - 1;
+            const unsigned sh = lane & ~(G - 1) & 31;
+            const unsigned msk = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
+            const unsigned b0 = (__ballot_sync(gmask, c0 >= k) >> sh) & msk;
+            const unsigned b1 = (__ballot_sync(gmask, c1 >= k) >> sh) & msk;
+            const unsigned any = b0 | b1;
+            int first = NPT + 1;  // 1-based index of the first point with count >= k
+            if (any) {
+                const int l = __ffs(any) - 1;
+                first = 2 * l + (((b0 >> l) & 1u) ? 0 : 1) + 1;
+            }
+            const int fb = first <= NPT ? first - 1 : 0;  // 0-based point index of x_f
+            const int fa = first >= 2 ? first - 2 : 0;    // of x_{f-1}
+            const double vb0 = __shfl_sync(gmask, x0, fb >> 1, G);
+            const double vb1 = __shfl_sync(gmask, x1, fb >> 1, G);
+            const double va0 = __shfl_sync(gmask, x0, fa >> 1, G);
+            const double va1 = __shfl_sync(gmask, x1, fa >> 1, G);
+            const double nb = first <= NPT ? ((fb & 1) ? vb1 : vb0) : b;
+            const double na = first >= 2 ? ((fa & 1) ? va1 : va0) : a;
+            if (na == a && nb == b) {
+                mdone = true;  // no representable progress
+            } else {
+                a = na;
+                b = nb;
+            }
+        }
+    }
+}
+
 template <class R, int G, bool XPHASE>
 __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict__ nodes, Items it,
                                                   const int32_t *__restrict__ list,
                                                   const RqiTask *__restrict__ tasks,
                                                   const int *__restrict__ ntasks, double rtol,
                                                   double absfloor, double pivmin, double pivmin_x,
-                                                  double eps_x, int certify, DevStats *st) {
+                                                  double eps_x, int certify, int xpts,
+                                                  DevStats *st) {
     __shared__ __align__(16) double sbuf[2 * BS_TILE];
     if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
     const RqiTask task = tasks[blockIdx.x];
@@ -289,10 +504,16 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
     if (certify) certify_y(absfloor);
     if (XPHASE) {
         double ax = hi(a), bx = hi(b);
-        msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x, n,
-                             [&](bool need, double x) {
-                                 return count_x_cta(sbuf, nd, need, x, pivmin_x);
-                             });
+        if (xpts == 2)
+            msect2_cta<G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x, n,
+                          [&](bool need, double x0, double x1, int &c0, int &c1) {
+                              count_x2_cta(sbuf, nd, need, x0, x1, pivmin_x, c0, c1);
+                          });
+        else
+            msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x,
+                                 n, [&](bool need, double x) {
+                                     return count_x_cta(sbuf, nd, need, x, pivmin_x);
+                                 });
         double delta = absfloor;
         if (active) {
             double mag = fmax(fabs(ax), fabs(bx));

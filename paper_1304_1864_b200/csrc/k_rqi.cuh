@@ -64,6 +64,7 @@ struct RqiArgs {
     double unscale;   // multiply eigenvalues by this (exact power of 2)
     DevStats *st;
     int32_t *dbg_iters;  // optional (MR3_DEBUG): iterations per item
+    double *dbg_trace;   // optional (MR3_DEBUG): 8 per item: x0 used, gap, r, res/tol per iteration
 };
 
 __device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
@@ -390,6 +391,16 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
             double g = hi(gr);
             double corr = g / nz2;
             R lam_new = add(lam, mk<R>(corr));
+            if (A.dbg_trace) {
+                double *tr = A.dbg_trace + 8 * (int64_t)id;
+                if (iters == 1) {
+                    const double x0 = A.it.x0[id];
+                    tr[0] = isnan(x0) ? 0.0 : 1.0;
+                    tr[1] = gap;
+                    tr[2] = (double)r;
+                }
+                if (iters <= 5) tr[2 + iters] = fabs(g) / sqrt(nz2) / tol;
+            }
             if (fabs(g) / sqrt(nz2) <= tol || fabs(corr) <= 8.0 * Prec<R>::eps * fabs(hi(lam)) ||
                 g == 0.0) {
                 lam_out = lam_new;

@@ -84,9 +84,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 1.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 1.0},
 };
 
 #define CK(call)                                                                  \
@@ -213,6 +213,7 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
     if (cnt <= 0) return 0;
     int rc = 0;
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
+    const int xpts = ctx->cfg[ctx->mode].v[MR3_XPTS] == 1 ? 1 : 2;
     const int per = tpb / G;
     // CTA tasks: runs of <= per items of one node; the grid is an upper bound on
     // their number (the kernel reads the exact count), so no host round trip
@@ -231,11 +232,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
         if (xphase)                                                                           \
             k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, W.st);                                                               \
+                certify, xpts, W.st);                                                         \
         else                                                                                  \
             k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, W.st);                                                               \
+                certify, xpts, W.st);                                                         \
         break;
     switch (G) {
         BIS(1)
@@ -866,8 +867,11 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.unscale = 1.0 / ctx->scale;
                 A.st = W.st;
                 A.dbg_iters = nullptr;
-                if (ctx->debug)
+                A.dbg_trace = nullptr;
+                if (ctx->debug) {
                     A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
+                    A.dbg_trace = (double *)getbuf(ctx, "dbg_trace", (size_t)cnt * 64, &rc3);
+                }
                 KTime *t = kt_begin(ctx, locate ? "k_rqi_locate" : "k_rqi");
                 if (locate)
                     k_rqi_locate<R><<<nb, rtpb, 0, s>>>(A);
@@ -1048,13 +1052,22 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
         fprintf(stderr, "\n");
         int shown = 0;
-        for (int i = 0; i < cnt && shown < 40; i++)
-            if (itv[i] >= 4) {
-                fprintf(stderr, "  item %d iters %d lam %.17g lgap %.3g rgap %.3g\n", i, itv[i],
-                        hi_of(lam[i]), lg[i], rg[i]);
+        for (int i = 0; i < cnt && shown < 40; i++) {
+            double tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (itv[i] >= 4)
+                cudaMemcpy(tr, (double *)ctx->bufs["dbg_trace"].p + 8 * (size_t)i, 64,
+                           cudaMemcpyDeviceToHost);
+            if (itv[i] >= 4 && tr[5] != 0.0) {
+                fprintf(stderr,
+                        "  item %d iters %d lam %.17g lgap %.3g rgap %.3g | x0 %g gap %.3g r %g "
+                        "res/tol %.3g %.3g %.3g %.3g\n",
+                        i, itv[i], hi_of(lam[i]), lg[i], rg[i], tr[0], tr[1], tr[2], tr[3], tr[4],
+                        tr[5], tr[6]);
                 shown++;
             }
+        }
         cudaMemset(ctx->bufs["dbg_iters"].p, 0, cnt * 4);
+        cudaMemset(ctx->bufs["dbg_trace"].p, 0, (size_t)cnt * 64);
     }
     if (dfac) {
         KTime *tf = kt_begin(ctx, "k_fixnorm");
