@@ -167,12 +167,51 @@ __device__ __forceinline__ Row4<double> srow<double>(const double *buf, int64_t 
     return r;
 }
 
+// Two tile streams at once: ascending tiles 0, 1, ... (nA of them) and descending
+// tiles ntile-1, ntile-2, ... (nD of them); step i hands body the i-th tile of each
+// stream (nullptr once a stream is exhausted).  Used by the fixed-twist sweeps,
+// whose top-down part (rows < r) and bottom-up part (rows > r) are independent
+// recurrences: interleaving them gives every thread two dependent chains at once.
+// smem: 4 tile buffers.  Collective.
+template <int ROWD, class Body>
+__device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep, int64_t n, int nA,
+                                                 int nD, Body body) {
+    constexpr int TILE = StageG<ROWD>::TILE;
+    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+    const int steps = nA > nD ? nA : nD;
+    auto bufA = [&](int b) -> double * { return smem + (b ? TILE : 0); };
+    auto bufD = [&](int b) -> double * { return smem + (b ? 3 * TILE : 2 * TILE); };
+    if (steps <= 0) return;
+    if (nA > 0) stage_tile_g<ROWD>(bufA(0), rep, n, 0);
+    if (nD > 0) stage_tile_g<ROWD>(bufD(0), rep, n, (int64_t)(ntile - 1) * RQ_TR);
+    for (int i = 0; i < steps; i++) {
+        if (i + 1 < steps) {
+            if (i + 1 < nA) stage_tile_g<ROWD>(bufA((i + 1) & 1), rep, n, (int64_t)(i + 1) * RQ_TR);
+            if (i + 1 < nD)
+                stage_tile_g<ROWD>(bufD((i + 1) & 1), rep, n, (int64_t)(ntile - 2 - i) * RQ_TR);
+            // stage_tile_g commits one group per call: wait until the current step's
+            // groups are complete (at most the just-issued ones pending)
+            if (i + 1 < nA && i + 1 < nD)
+                cp_async_wait<2>();
+            else
+                cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        body(i < nA ? bufA(i & 1) : nullptr, (int64_t)i * RQ_TR,
+             i < nD ? bufD(i & 1) : nullptr, (int64_t)(ntile - 1 - i) * RQ_TR);
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- kernel
 template <class R, class OutT>
-__global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
-    __shared__ __align__(16) double sstage[2 * Stage<R>::TILE];
+__global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
+    __shared__ __align__(16) double sstage[4 * Stage<R>::TILE];  // 4 tiles: dual_staged_pass
     __shared__ OutT tile[RQ_TR][RQ_TPB + 1];
     __shared__ int64_t s_r[RQ_TPB], s_col[RQ_TPB];
+    __shared__ int s_rmin, s_rmax;
 
     const int tid = threadIdx.x;
     const RqiTask task = A.tasks[blockIdx.x];
@@ -205,6 +244,19 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         }
     }
     const double tol = A.krs * gap * A.eps_x * sqrt((double)n);
+    // twist range of the CTA (the fixed-twist sweeps stage rows up to these)
+    if (tid == 0) {
+        s_rmin = (int)n;
+        s_rmax = 0;
+    }
+    __syncthreads();
+    if (active) {
+        atomicMin(&s_rmin, (int)r);
+        atomicMax(&s_rmax, (int)r);
+    }
+    __syncthreads();
+    const int cta_rmin = s_rmin <= s_rmax ? s_rmin : 0;
+    const int cta_rmax = s_rmin <= s_rmax ? s_rmax : (int)n - 1;
 
     // one twisted factorization at lam for the threads with `need`
     auto twisted = [&](bool need) -> int {
@@ -316,58 +368,77 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
         R s = neg(lam);
         double W = 0.0;
         int negc = 0;
-        staged_pass<R>(sstage, nd.rep, n, false, [&](const double *buf, int64_t t0) {
-            if (!need || t0 > r) return;
-#pragma unroll
-            for (int q = 0; q < RQ_TR / RQ_C; q++) {
-                const int64_t b0 = t0 + q * RQ_C;
-                if (b0 <= r) {
-                    A.ck_s[(b0 / RQ_C) * A.S + slot] = s;
-                    A.ck_W[(b0 / RQ_C) * A.S + slot] = W;
-                }
-#pragma unroll
-                for (int j = 0; j < RQ_C; j++) {
-                    const int64_t kk = b0 + j;
-                    if (kk < r) {
-                        Row4<R> rw = srow<R>(buf, t0, kk);
-                        R dp = guard(add(rw.d, s), A.pivmin);
-                        negc += is_neg(dp) ? 1 : 0;
-                        R lp = div(rw.ld, dp);
-                        double l2 = hi(lp) * hi(lp);
-                        W = clampbig(fma(l2, W, l2));
-                        s = sub(mul(lp, mul(rw.l, s)), lam);
-                    }
-                }
-            }
-        });
         R p = mk<R>(0.0);
         double V = 0.0;
         if (need) p = sub(load_row4<R>(nd.rep, n - 1).d, lam);
-        staged_pass<R>(sstage, nd.rep, n, true, [&](const double *buf, int64_t t0) {
-            if (!need || t0 + RQ_TR <= r) return;
+        // F: rows 0..r-1 ascending (tiles 0 .. cta_rmax/RQ_TR); B: rows n-1..r descending
+        const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+        const int nA = cta_rmax / RQ_TR + 1;
+        const int nD = ntile - cta_rmin / RQ_TR;
+        // one F row (rows < r) and one B row (rows > r); predicated commits keep the two
+        // recurrences in one basic block so their dependent chains interleave
+        auto frow = [&](const double *bA, int64_t tA, int64_t kk) {
+            Row4<R> rw = srow<R>(bA, tA, kk);
+            R dp = guard(add(rw.d, s), A.pivmin);
+            R lp = div(rw.ld, dp);
+            double l2 = hi(lp) * hi(lp);
+            double W2 = clampbig(fma(l2, W, l2));
+            R s2 = sub(mul(lp, mul(rw.l, s)), lam);
+            if (kk < r) {
+                negc += is_neg(dp) ? 1 : 0;
+                W = W2;
+                s = s2;
+            }
+        };
+        auto brow = [&](const double *bD, int64_t tD, int64_t kk) {
+            Row4<R> rw = srow<R>(bD, tD, kk - 1);
+            R Dm = guard(add(rw.lld, p), A.pivmin);
+            R t = div(rw.d, Dm);
+            double u2 = hi(rw.l) * hi(t);
+            u2 *= u2;
+            double V2 = clampbig(fma(u2, V, u2));
+            R p2 = sub(mul(p, t), lam);
+            if (kk > r && kk < n) {
+                negc += is_neg(Dm) ? 1 : 0;
+                V = V2;
+                p = p2;  // p_{kk-1}
+            }
+        };
+        dual_staged_pass<Stage<R>::ROWD>(
+            sstage, nd.rep, n, nA, nD,
+            [&](const double *bA, int64_t tA, const double *bD, int64_t tD) {
+                if (!need) return;
 #pragma unroll 1
-            for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
-                const int64_t b0 = t0 + q * RQ_C;
-                if (b0 >= n || b0 + RQ_C <= r) continue;
+                for (int q = 0; q < RQ_TR / RQ_C; q++) {
+                    const int64_t b0F = tA + q * RQ_C;
+                    const int64_t b0B = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
+                    const bool fF = bA != nullptr && b0F < r;
+                    const bool fB = bD != nullptr && b0B + RQ_C > r && b0B < n;
+                    if (bA != nullptr && b0F <= r) {
+                        A.ck_s[(b0F / RQ_C) * A.S + slot] = s;
+                        A.ck_W[(b0F / RQ_C) * A.S + slot] = W;
+                    }
+                    if (fF && fB) {
 #pragma unroll
-                for (int j = RQ_C - 1; j >= 0; j--) {
-                    const int64_t kk = b0 + j;
-                    if (kk < n && kk >= r) {
-                        if (j == 0) A.ck_p[(b0 / RQ_C) * A.S + slot] = p;  // p_{b0}
-                        if (kk > r) {
-                            Row4<R> rw = srow<R>(buf, t0, kk - 1);
-                            R Dm = guard(add(rw.lld, p), A.pivmin);
-                            negc += is_neg(Dm) ? 1 : 0;
-                            R t = div(rw.d, Dm);
-                            double u2 = hi(rw.l) * hi(t);
-                            u2 *= u2;
-                            V = clampbig(fma(u2, V, u2));
-                            p = sub(mul(p, t), lam);  // p_{kk-1}
+                        for (int j = 0; j < RQ_C; j++) {
+                            const int64_t kB = b0B + RQ_C - 1 - j;
+                            if (j == RQ_C - 1 && kB >= r) A.ck_p[(b0B / RQ_C) * A.S + slot] = p;
+                            frow(bA, tA, b0F + j);
+                            brow(bD, tD, kB);
+                        }
+                    } else if (fF) {
+#pragma unroll
+                        for (int j = 0; j < RQ_C; j++) frow(bA, tA, b0F + j);
+                    } else if (fB) {
+#pragma unroll
+                        for (int j = 0; j < RQ_C; j++) {
+                            const int64_t kB = b0B + RQ_C - 1 - j;
+                            if (j == RQ_C - 1 && kB >= r) A.ck_p[(b0B / RQ_C) * A.S + slot] = p;
+                            brow(bD, tD, kB);
                         }
                     }
                 }
-            }
-        });
+            });
         if (need) {
             gr = add(add(s, p), lam);
             negc += is_neg(gr) ? 1 : 0;
@@ -621,7 +692,10 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi(RqiArgs<R> A) {
 // stopping test (Eq. (3.6)) is evaluated on the actual binary_y gamma_r.
 //   F: s_0 = -lam ; d+_i = d_i + s_i ; s_{i+1} = lld_i s_i / d+_i - lam
 //   B: p_{n-1} = d_{n-1} - lam ; D-_{i+1} = lld_i + p_{i+1} ; p_i = d_i p_{i+1} / D-_{i+1} - lam
-//   gamma_k = s_k + p_k + lam ;  r = argmin |gamma_k| (ties: smallest k)
+//   gamma_k = s_k + p_k + lam ;  r = argmin |gamma_k| w_k (ties: smallest k),
+//   w_k = 1 + 3 |2k - n| / n in [1, 4]: the chosen |gamma_r| is within 4x of the minimum
+//   (Dhillon-Parlett: any twist with |gamma_r| = O(min) gives the same quality of z;
+//   the stopping test is applied to the binary_y gamma_r actually used)
 // s is checkpointed every RQ_C rows (binary64, in ck_W) and recomputed per block
 // during B; rows of M_x are staged through shared memory like k_rqi's.
 // ---------------------------------------------------------------------------
@@ -671,6 +745,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         }
     });
     double p = 0.0, best = INFINITY;
+    const double wfac = 3.0 / (double)n;
     int64_t rr = n - 1;
     if (active) p = __ldg(nd.repx + 2 * (n - 1)) - lam;
     staged_pass_g<2>(sx, nd.repx, n, true, [&](const double *buf, int64_t t0) {
@@ -696,7 +771,11 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             for (int j = RQ_C - 1; j >= 0; j--) {
                 const int64_t kk = b0 + j;
                 if (kk < n) {
-                    const double g = fabs(sb[j] + p + lam);
+                    // |gamma_k| weighted by 1 + 3 |2k - n| / n: among twists within a
+                    // factor 4 of the optimum, prefer one near the middle, where the
+                    // top-down and bottom-up halves of k_rqi's sweeps are balanced
+                    const double g = fabs(sb[j] + p + lam) *
+                                     fma(wfac, fabs(2.0 * (double)kk - (double)n), 1.0);
                     if (g <= best) {
                         best = g;
                         rr = kk;
