@@ -27,10 +27,15 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
-# SASS-counted FP64-pipe instructions (DADD/DMUL/DFMA/DSETP; MUFU.RCP64H is on the XU) per row of
-# the dd negcount loop of k_bisect<dd,1> (recount
-# with tools/count_sass.py after every change of the loop body).
-FP64_INST_PER_BISECT_ROW = {"dd": 45.25, "f64": 12, "x": 3.25}  # "x": binary_x phase rows (projective)
+# Algorithmic FP64 instructions (DADD/DMUL/DFMA) per unit of work, from the operation
+# counts of the recurrences in the arithmetic of dd.cuh (pair add 11,
+# pair mul 7, pair fma 15, pair div 14 + one MUFU.RCP64H):
+#   Sturm row, binary_y projective (2 pair fma + 1 pair mul)          37
+#   Sturm row, binary_x projective (2 DFMA + 1 DMUL + rescale/8)      3.25
+#   Sturm row, fp64-internal mode (projective, binary64)              3.25
+#   RQI row (rqi_rows: 2 fixed-twist passes of n rows at 49 + the z sweeps' n rows at 69) 56
+FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25}
+FP64_INST_PER_RQI_ROW = {"dd": 56.0, "f64": 12.0}
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 
 
@@ -245,21 +250,47 @@ def main():
         t_max = float(tt.item())
     value = m_req / (t_max * 1e-3)  # all ranks together produce the m eigenpairs of one solve
 
-    # roofline of the dominant kernel (K2 bisection): FP64-pipe instructions per row
-    kb_ms, kb_n = ktot.get("k_bisect", (0.0, 0))
+    # roofline of the dominant kernel (the larger of k_bisect and k_rqi): algorithmic FP64
+    # instructions per launch / its CUDA-event time inside the timed region
     mode = "f64" if p.io == "f32" else "dd"
-    rows = stats["bisect_rows"] if stats else 0.0
-    rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
-    # bisect_rows(_x) count plan + cluster refinement of the last step:
-    inst = rows * FP64_INST_PER_BISECT_ROW[mode] + rows_x * FP64_INST_PER_BISECT_ROW["x"]
-    achieved = inst / (kb_ms / args.steps * 1e-3) if kb_ms else 0
-    traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic_tab = {}
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"config{args.config}", {}).get("k_bisect")
+            traffic_tab = json.load(open(tp)).get(f"config{args.config}", {})
         except Exception:
-            traffic = None
+            traffic_tab = {}
+
+    def roof(kname):
+        ms, nl = ktot.get(kname, (0.0, 0))
+        if kname == "k_bisect":
+            rows = stats["bisect_rows"] if stats else 0.0
+            rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
+            inst = rows * FP64_INST_PER_BISECT_ROW[mode] + rows_x * FP64_INST_PER_BISECT_ROW["x"]
+            per = {"binary_y_row": FP64_INST_PER_BISECT_ROW[mode],
+                   "binary_x_row": FP64_INST_PER_BISECT_ROW["x"]}
+            units = {"binary_y_rows": rows, "binary_x_rows": rows_x}
+        else:
+            rows = stats["rqi_rows"] if stats else 0.0
+            inst = rows * FP64_INST_PER_RQI_ROW[mode]
+            per = {"rqi_row": FP64_INST_PER_RQI_ROW[mode]}
+            units = {"rqi_rows": rows}
+        t_launch = ms / max(nl, 1) * 1e-3  # average launch duration
+        inst_launch = inst / max(nl / args.steps, 1)
+        ach = inst_launch / t_launch if t_launch else 0.0
+        return {"bound": "alu", "kernel": kname, "achieved": ach / 1e12,
+                "peak": DERIVED_FP64_PEAK / 1e12, "unit": "T FP64-inst/s",
+                "frac": ach / DERIVED_FP64_PEAK, "traffic": traffic_tab.get(kname),
+                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz (MEASURED_PEAKS.json "
+                               "has no FP64 entry); measured_peak_same_run = K7 DFMA microbenchmark",
+                "measured_peak_same_run": peak_ips / 1e12,
+                "frac_of_measured": ach / peak_ips if peak_ips else None,
+                "inst_per_unit": per, "units_per_step": units,
+                "launches_per_step": nl / args.steps, "ms_per_launch": t_launch * 1e3}
+
+    cand = [k for k in ("k_bisect", "k_rqi") if k in ktot]
+    dom = max(cand, key=lambda k: ktot[k][0]) if cand else "k_bisect"
+    roofs = {k: roof(k) for k in cand}
 
     result = None
     if rank == 0:
@@ -273,17 +304,8 @@ def main():
             "config": {"workload": p.name, "n": n, "m": m_req, "range": p.range,
                        "io": p.io, "parallelism": f"index-set partition x{world}",
                        "l2": "512 MB buffer written between timed steps; Z output > L2"},
-            "roofline": {"bound": "alu", "kernel": "k_bisect",
-                         "achieved": achieved / 1e12, "peak": DERIVED_FP64_PEAK / 1e12,
-                         "unit": "T FP64-inst/s", "frac": achieved / DERIVED_FP64_PEAK,
-                         "traffic": traffic,
-                         "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz",
-                         "measured_peak_same_run": peak_ips / 1e12,
-                         "frac_of_measured": achieved / peak_ips if peak_ips else None,
-                         "inst_per_row": {"binary_y": FP64_INST_PER_BISECT_ROW[mode],
-                                          "binary_x": FP64_INST_PER_BISECT_ROW["x"]},
-                         "rows_per_step": {"binary_y": rows, "binary_x": rows_x},
-                         "launches_per_step": kb_n / args.steps},
+            "roofline": roofs.get(dom, {}),
+            "roofline_other": {k: v for k, v in roofs.items() if k != dom},
             "kernels": kt,
             "dd_step_latency_ns": dd_step_ns,
             "step_ms": [round(t, 3) for t in times],

@@ -501,6 +501,21 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
         }
     };
 
+    if (XPHASE && certify == 2) {
+        // K2' (RQI starting points): binary_x multisection on M_x to relative rtol
+        // (a few ulps) from the certified bracket; x0 = midpoint if strictly inside it
+        double ax = hi(a), bx = hi(b);
+        msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 1.0, rows_x, n,
+                             [&](bool need, double x) {
+                                 return count_x_cta(sbuf, nd, need, x, pivmin_x);
+                             });
+        if (active && lig == 0) {
+            const double x = 0.5 * (ax + bx);
+            it.x0[id] = (x > hi(a) && x < hi(b)) ? x : NAN;
+        }
+        if (rows_x) atomicAdd(&st->refine_rows_x, rows_x);
+        return;
+    }
     if (certify) certify_y(absfloor);
     if (XPHASE) {
         double ax = hi(a), bx = hi(b);
@@ -538,6 +553,25 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
     }
     if (rows) atomicAdd(&st->bisect_rows, rows);
     if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
+}
+
+// K2' selection: singletons whose certified bracket half-width exceeds
+// gap sqrt(eps_x sqrt(n) / C) need a refined RQI start (see k_refine_x0 in
+// k_bisect.cuh for the argument); all others start at the bracket midpoint (x0 = NaN)
+template <class R>
+__global__ void k_refine_flags(const NodeInfo *__restrict__ nodes, Items it,
+                               const int32_t *__restrict__ list, int cnt, double eps_x,
+                               double cconv, char *flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const int id = list[t];
+    const int64_t n = nodes[it.node[id]].n;
+    const R a = reinterpret_cast<R *>(it.lo)[id];
+    const R b = reinterpret_cast<R *>(it.hi)[id];
+    const double gap = fmin(it.lgap[id], it.rgap[id]);
+    const double need = gap * sqrt(eps_x * sqrt((double)n) / cconv);
+    it.x0[id] = NAN;
+    flags[t] = (0.5 * hi(sub(b, a)) > need && n >= 2) ? 1 : 0;
 }
 
 }  // namespace mr3

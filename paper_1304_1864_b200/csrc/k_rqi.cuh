@@ -35,6 +35,8 @@
 // block of RQ_C rows is recomputed into registers when a sweep needs it in the
 // other direction (SURVEY.md §7 hard part 2, option (c)).
 #pragma once
+#include <type_traits>
+
 #include "k_bisect.cuh"
 
 namespace mr3 {
@@ -794,15 +796,48 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
 }
 
 // rescale the columns whose binary64 norm estimate missed by more than 2^-54
-// (one CTA per column; columns with fac == 0 are already unit vectors)
+// (grid-stride over (column, chunk) pairs; a chunk is 256 threads x 4 16-byte
+// vectors, all loads issued before the stores; columns with fac == 0 are already
+// unit vectors and are skipped)
 template <class OutT>
-__global__ void k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols, const double *fac, int64_t n) {
-    const int64_t c = blockIdx.x;
-    if (c >= ncols) return;
-    const double f = fac[c];
-    if (f == 0.0) return;
-    OutT *colp = Z + c * ldz;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) colp[i] = (OutT)((double)colp[i] * f);
+__global__ void __launch_bounds__(256) k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols,
+                                                 const double *fac, int64_t n) {
+    constexpr int VEC = 16 / sizeof(OutT);  // elements per 16-byte access
+    constexpr int U = 4;
+    constexpr int CHUNK = 256 * U * VEC;
+    const int64_t per_col = (n + CHUNK - 1) / CHUNK;
+    const int64_t total = ncols * per_col;
+    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+        const int64_t c = w / per_col, ch = w - c * per_col;
+        const double f = fac[c];
+        if (f == 0.0) continue;
+        OutT *colp = Z + c * ldz;
+        const int64_t i0 = ch * CHUNK;
+        const bool vec = ((reinterpret_cast<uintptr_t>(colp) & 15) == 0) && i0 + CHUNK <= n;
+        if (vec) {
+            using V = typename std::conditional<sizeof(OutT) == 8, double2, float4>::type;
+            V *v = reinterpret_cast<V *>(colp + i0);
+            V x[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) x[u] = v[threadIdx.x + u * 256];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if constexpr (sizeof(OutT) == 8) {
+                    x[u].x *= f;
+                    x[u].y *= f;
+                } else {
+                    x[u].x = (float)((double)x[u].x * f);
+                    x[u].y = (float)((double)x[u].y * f);
+                    x[u].z = (float)((double)x[u].z * f);
+                    x[u].w = (float)((double)x[u].w * f);
+                }
+                v[threadIdx.x + u * 256] = x[u];
+            }
+        } else {
+            for (int64_t i = i0 + threadIdx.x; i < min(i0 + CHUNK, n); i += 256)
+                colp[i] = (OutT)((double)colp[i] * f);
+        }
+    }
 }
 
 // sort keys (node, twist index) of the singletons for k_rqi's CTA grouping

@@ -53,6 +53,7 @@ struct DevStats {
     int largest_cluster;
     int n_clusters;
     int pad;
+    unsigned long long refine_rows_x;  // binary_x rows of the RQI start refinement (K2')
 };
 
 template <class R>

@@ -209,7 +209,8 @@ static int choose_tpb(mr3_ctx ctx, int64_t thr, int tpb_max) {
 
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
-                         double absfloor, int certify, bool xphase, double eps_x) {
+                         double absfloor, int certify, bool xphase, double eps_x,
+                         const char *tname = "k_bisect") {
     if (cnt <= 0) return 0;
     int rc = 0;
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
@@ -226,7 +227,7 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
     CKL("k_rqi_tasks");
     const int grid = (int)bound;
     const double pivmin_x = 0x1p-900;
-    KTime *t = kt_begin(ctx, "k_bisect");
+    KTime *t = certify == 2 ? nullptr : kt_begin(ctx, tname);
 #define BIS(GG)                                                                               \
     case GG:                                                                                  \
         if (xphase)                                                                           \
@@ -249,7 +250,7 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
             return MR3_ERR_STATE;
     }
 #undef BIS
-    kt_end(ctx, t);
+    if (t) kt_end(ctx, t);
     CKL("k_bisect");
     return 0;
 }
@@ -795,17 +796,32 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if (ncount <= 0) return 0;
         int rc2 = 0;
         if (P[MR3_REFINE] > 0) {  // K2': binary_x starting points for small-gap singletons
-            const long long threads = (long long)ncount * 4;
+            char *flags = (char *)getbuf(ctx, "ref_flags", (size_t)ncount, &rc2);
+            int32_t *rlist = (int32_t *)getbuf(ctx, "ref_list", (size_t)ncount * 4, &rc2);
+            int *rcnt = (int *)getbuf(ctx, "ref_cnt", 16, &rc2);
+            if (rc2) return rc2;
             KTime *tr = kt_begin(ctx, "k_refine_x0");
-            k_refine_x0<R, 4><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
-                W.nodes, W.it, list, ncount, eps_x, 0x1p-900, P[MR3_REFINE], W.st);
-            kt_end(ctx, tr);
-            cudaError_t e2 = cudaGetLastError();
-            if (e2 != cudaSuccess) {
-                ctx->err = std::string("k_refine_x0: ") + cudaGetErrorString(e2);
-                return MR3_ERR_CUDA;
+            k_refine_flags<R><<<(ncount + 255) / 256, 256, 0, s>>>(W.nodes, W.it, list, ncount,
+                                                                  eps_x, P[MR3_REFINE], flags);
+            CKL("k_refine_flags");
+            size_t tmpb = 0;
+            cub::DeviceSelect::Flagged(nullptr, tmpb, list, flags, rlist, rcnt, ncount, s);
+            void *tmp = getbuf(ctx, "cubtmp_ref", tmpb, &rc2);
+            if (rc2) return rc2;
+            cub::DeviceSelect::Flagged(tmp, tmpb, list, flags, rlist, rcnt, ncount, s);
+            CKL("select (refine)");
+            int hr = 0;
+            CK(cudaMemcpyAsync(&hr, rcnt, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (hr > 0) {
+                // many lanes per item: few items, short dependent chains (log2(G+1) bits/round)
+                int G = choose_groups(ctx, hr, 0);
+                if (G < 16) G = 16;
+                rc2 = launch_bisect<R>(ctx, W, rlist, hr, G, 2.0 * eps_x, 1e-300, 2, true, eps_x,
+                                       "k_refine_x0");
+                if (rc2) return rc2;
             }
-            ctx->launches++;
+            kt_end(ctx, tr);
         } else {
             CK(cudaMemsetAsync(W.it.x0, 0xff, (size_t)cnt * 8, s));  // NaN: midpoints
         }
@@ -1071,7 +1087,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     }
     if (dfac) {
         KTime *tf = kt_begin(ctx, "k_fixnorm");
-        k_fixnorm<OutT><<<(unsigned)(c1 - c0), 256, 0, s>>>(Z, ldz, c1 - c0, dfac, ctx->n);
+        k_fixnorm<OutT><<<ctx->nsm * 16, 256, 0, s>>>(Z, ldz, c1 - c0, dfac, ctx->n);
         kt_end(ctx, tf);
         CKL("k_fixnorm");
     }
