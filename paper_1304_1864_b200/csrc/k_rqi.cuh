@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 // stopping test (Eq. (3.6)) is evaluated on the actual binary_y gamma_r.
 //   F: s_0 = -lam ; d+_i = d_i + s_i ; s_{i+1} = lld_i s_i / d+_i - lam
 //   B: p_{n-1} = d_{n-1} - lam ; D-_{i+1} = lld_i + p_{i+1} ; p_i = d_i p_{i+1} / D-_{i+1} - lam
+//   (both evaluated in projective form, see below)
 //   gamma_k = s_k + p_k + lam ;  r = argmin |gamma_k| w_k (ties: smallest k),
 //   w_k = 1 + 3 |2k - n| / n in [1, 4]: the chosen |gamma_r| is within 4x of the minimum
 //   (Dhillon-Parlett: any twist with |gamma_r| = O(min) gives the same quality of z;
@@ -726,30 +727,47 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     auto xr = [&](const double *buf, int64_t t0, int64_t k) -> double2 {
         return *reinterpret_cast<const double2 *>(buf + (k - t0 + RQ_HALO) * 2);
     };
-    double s = -lam;
+    // projective states (division-free recurrences, as negcount_x): F: s_k = pf/qf,
+    //   D = d qf + pf, pf <- lld pf - lam D, qf <- D;  B: p_k = pb/qb,
+    //   E = lld_{k-1} qb + pb, pb <- d_{k-1} pb - lam E, qb <- E.
+    // The chains are two DFMAs per row; the ratios gamma_k needs are formed off-chain.
+    // Checkpoints (pf, qf) every RQ_C rows in ck_W / ck_p (binary64).
+    double* ckq = reinterpret_cast<double *>(A.ck_p);
+    auto rescale2 = [](double &x, double &y) {
+        const unsigned ex = (unsigned)__double2hiint(x) & 0x7ff00000u;
+        const unsigned ey = (unsigned)__double2hiint(y) & 0x7ff00000u;
+        const unsigned em = ex > ey ? ex : ey;
+        if (em == 0x7ff00000u || em == 0u) return;
+        const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+        x *= sc;
+        y *= sc;
+    };
+    double pf = -lam, qf = 1.0;
     staged_pass_g<2>(sx, nd.repx, n, false, [&](const double *buf, int64_t t0) {
         if (!active) return;
 #pragma unroll 1
         for (int q = 0; q < RQ_TR / RQ_C; q++) {
             const int64_t b0 = t0 + q * RQ_C;
             if (b0 >= n) break;
-            A.ck_W[(b0 / RQ_C) * A.S + slot] = s;
+            A.ck_W[(b0 / RQ_C) * A.S + slot] = pf;
+            ckq[(b0 / RQ_C) * A.S + slot] = qf;
 #pragma unroll
             for (int j = 0; j < RQ_C; j++) {
                 const int64_t kk = b0 + j;
                 if (kk < n - 1) {
                     const double2 rw = xr(buf, t0, kk);
-                    double dp = rw.x + s;
-                    dp = fabs(dp) < pivmin ? -pivmin : dp;
-                    s = fma_rn(mul_rn(rw.y, s), rcp(dp), -lam);
+                    const double D = fma_rn(rw.x, qf, pf);
+                    pf = fma_rn(-lam, D, mul_rn(rw.y, pf));
+                    qf = D;
                 }
             }
+            rescale2(pf, qf);
         }
     });
-    double p = 0.0, best = INFINITY;
+    double pb = 0.0, qb = 1.0, best = INFINITY;
     const double wfac = 3.0 / (double)n;
     int64_t rr = n - 1;
-    if (active) p = __ldg(nd.repx + 2 * (n - 1)) - lam;
+    if (active) pb = __ldg(nd.repx + 2 * (n - 1)) - lam;
     staged_pass_g<2>(sx, nd.repx, n, true, [&](const double *buf, int64_t t0) {
         if (!active) return;
 #pragma unroll 1
@@ -757,16 +775,17 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             const int64_t b0 = t0 + q * RQ_C;
             if (b0 >= n) continue;
             double sb[RQ_C];
-            double s2 = A.ck_W[(b0 / RQ_C) * A.S + slot];
+            double p2 = A.ck_W[(b0 / RQ_C) * A.S + slot];
+            double q2 = ckq[(b0 / RQ_C) * A.S + slot];
 #pragma unroll
             for (int j = 0; j < RQ_C; j++) {
                 const int64_t kk = b0 + j;
-                sb[j] = s2;
+                sb[j] = div(p2, q2);  // s_kk (off the chain)
                 if (kk < n - 1) {
                     const double2 rw = xr(buf, t0, kk);
-                    double dp = rw.x + s2;
-                    dp = fabs(dp) < pivmin ? -pivmin : dp;
-                    s2 = fma_rn(mul_rn(rw.y, s2), rcp(dp), -lam);
+                    const double D = fma_rn(rw.x, q2, p2);
+                    p2 = fma_rn(-lam, D, mul_rn(rw.y, p2));
+                    q2 = D;
                 }
             }
 #pragma unroll
@@ -776,7 +795,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                     // |gamma_k| weighted by 1 + 3 |2k - n| / n: among twists within a
                     // factor 4 of the optimum, prefer one near the middle, where the
                     // top-down and bottom-up halves of k_rqi's sweeps are balanced
-                    const double g = fabs(sb[j] + p + lam) *
+                    const double g = fabs(sb[j] + div(pb, qb) + lam) *
                                      fma(wfac, fabs(2.0 * (double)kk - (double)n), 1.0);
                     if (g <= best) {
                         best = g;
@@ -784,12 +803,13 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                     }
                     if (kk > 0) {
                         const double2 rw = xr(buf, t0, kk - 1);
-                        double Dm = rw.y + p;
-                        Dm = fabs(Dm) < pivmin ? -pivmin : Dm;
-                        p = fma_rn(mul_rn(rw.x, p), rcp(Dm), -lam);
+                        const double E = fma_rn(rw.y, qb, pb);
+                        pb = fma_rn(-lam, E, mul_rn(rw.x, pb));
+                        qb = E;
                     }
                 }
             }
+            rescale2(pb, qb);
         }
     });
     if (active) A.it.twist[id] = (int32_t)rr;
