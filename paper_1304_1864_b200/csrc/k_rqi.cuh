@@ -169,28 +169,26 @@ __device__ __forceinline__ Row4<double> srow<double>(const double *buf, int64_t 
     return r;
 }
 
-// Two tile streams at once: ascending tiles 0, 1, ... (nA of them) and descending
-// tiles ntile-1, ntile-2, ... (nD of them); step i hands body the i-th tile of each
-// stream (nullptr once a stream is exhausted).  Used by the fixed-twist sweeps,
-// whose top-down part (rows < r) and bottom-up part (rows > r) are independent
-// recurrences: interleaving them gives every thread two dependent chains at once.
-// smem: 4 tile buffers.  Collective.
+// Two tile streams at once: ascending tiles a0, a0+1, ... (nA of them) and descending
+// tiles d0, d0-1, ... (nD of them); step i hands body the i-th tile of each stream
+// (nullptr once a stream is exhausted).  Used by the fixed-twist sweeps (top-down
+// rows < r and bottom-up rows > r) and by the z sweeps (rows <= r downward and rows
+// > r upward): the two halves are independent recurrences, and interleaving them
+// gives every thread two dependent chains at once.  smem: 4 tile buffers.  Collective.
 template <int ROWD, class Body>
-__device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep, int64_t n, int nA,
-                                                 int nD, Body body) {
+__device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep, int64_t n, int a0,
+                                                 int nA, int d0, int nD, Body body) {
     constexpr int TILE = StageG<ROWD>::TILE;
-    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
     const int steps = nA > nD ? nA : nD;
     auto bufA = [&](int b) -> double * { return smem + (b ? TILE : 0); };
     auto bufD = [&](int b) -> double * { return smem + (b ? 3 * TILE : 2 * TILE); };
     if (steps <= 0) return;
-    if (nA > 0) stage_tile_g<ROWD>(bufA(0), rep, n, 0);
-    if (nD > 0) stage_tile_g<ROWD>(bufD(0), rep, n, (int64_t)(ntile - 1) * RQ_TR);
+    if (nA > 0) stage_tile_g<ROWD>(bufA(0), rep, n, (int64_t)a0 * RQ_TR);
+    if (nD > 0) stage_tile_g<ROWD>(bufD(0), rep, n, (int64_t)d0 * RQ_TR);
     for (int i = 0; i < steps; i++) {
         if (i + 1 < steps) {
-            if (i + 1 < nA) stage_tile_g<ROWD>(bufA((i + 1) & 1), rep, n, (int64_t)(i + 1) * RQ_TR);
-            if (i + 1 < nD)
-                stage_tile_g<ROWD>(bufD((i + 1) & 1), rep, n, (int64_t)(ntile - 2 - i) * RQ_TR);
+            if (i + 1 < nA) stage_tile_g<ROWD>(bufA((i + 1) & 1), rep, n, (int64_t)(a0 + i + 1) * RQ_TR);
+            if (i + 1 < nD) stage_tile_g<ROWD>(bufD((i + 1) & 1), rep, n, (int64_t)(d0 - i - 1) * RQ_TR);
             // stage_tile_g commits one group per call: wait until the current step's
             // groups are complete (at most the just-issued ones pending)
             if (i + 1 < nA && i + 1 < nD)
@@ -201,8 +199,8 @@ __device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep
             cp_async_wait<0>();
         }
         __syncthreads();
-        body(i < nA ? bufA(i & 1) : nullptr, (int64_t)i * RQ_TR,
-             i < nD ? bufD(i & 1) : nullptr, (int64_t)(ntile - 1 - i) * RQ_TR);
+        body(i < nA ? bufA(i & 1) : nullptr, (int64_t)(a0 + i) * RQ_TR,
+             i < nD ? bufD(i & 1) : nullptr, (int64_t)(d0 - i) * RQ_TR);
         __syncthreads();
     }
 }
@@ -211,8 +209,6 @@ __device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep
 template <class R, class OutT>
 __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     __shared__ __align__(16) double sstage[4 * Stage<R>::TILE];  // 4 tiles: dual_staged_pass
-    __shared__ OutT tile[RQ_TR][RQ_TPB + 1];
-    __shared__ int64_t s_r[RQ_TPB], s_col[RQ_TPB];
     __shared__ int s_rmin, s_rmax;
 
     const int tid = threadIdx.x;
@@ -407,7 +403,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             }
         };
         dual_staged_pass<Stage<R>::ROWD>(
-            sstage, nd.rep, n, nA, nD,
+            sstage, nd.rep, n, 0, nA, ntile - 1, nD,
             [&](const double *bA, int64_t tA, const double *bD, int64_t tD) {
                 if (!need) return;
 #pragma unroll 1
@@ -533,146 +529,143 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 
     // ---------------- final stage: z from the twisted factorization at lam -----
     const bool mine = active && col >= 0;
-    s_r[tid] = mine ? r : -1;
-    s_col[tid] = mine ? col - A.zcol0 : -1;
     const double inv = 1.0 / sqrt(nz2);
     double ss_hi = 0.0, ss_lo = 0.0;
     const double tiny = 1e-250;
     OutT *Zo = reinterpret_cast<OutT *>(A.Z);
-    const int warp = tid >> 5, lane = tid & 31;
-    __syncthreads();
 
-    // D sweep: rows k <= r, top-down, z_r = 1, z_k = -l+_k z_{k+1}
-    // (z_k = -(ld_{k+1}/ld_k) z_{k+2} if z_{k+1} == 0)
-    {
-        R z1 = mk<R>(0.0), z2v = mk<R>(0.0);  // z_{k+1}, z_{k+2}
-        R ldn = mk<R>(0.0);                   // ld_{k+1}
-        staged_pass<R>(sstage, nd.rep, n, true, [&](const double *buf, int64_t t0) {
-            if (mine && t0 <= r) {
-#pragma unroll 1
-                for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
-                    const int64_t b0 = t0 + q * RQ_C;
-                    if (b0 > r || b0 >= n) continue;
-                    R lpb[RQ_C];
-                    R s = A.ck_s[(b0 / RQ_C) * A.S + slot];
+    // z from the twisted factorization at lam, two sweeps outward from the twist r,
+    // interleaved (two dependent chains per thread):
+    //   D: rows k <= r, downward, z_r = 1, z_k = -l+_k z_{k+1}
+    //      (z_k = -(ld_{k+1}/ld_k) z_{k+2} if z_{k+1} == 0)
+    //   U: rows k > r, upward, z_k = -u-_{k-1} z_{k-1}
+    //      (z_k = -(ld_{k-2}/ld_{k-1}) z_{k-2} if z_{k-1} == 0)
+    // l+ / u- of each 8-row block are recomputed from the checkpoints of the last
+    // factorization.  Each thread stores its own column directly: successive rows of
+    // a column are contiguous, and the partial sectors merge in L2 before write-back.
+    OutT *zcol = mine ? Zo + nd.row0 + (col - A.zcol0) * A.ldz : nullptr;
+    R z1D = mk<R>(0.0), z2D = mk<R>(0.0), ldn = mk<R>(0.0);        // z_{k+1}, z_{k+2}, ld_{k+1}
+    R z1U = mk<R>(0.0), z2U = mk<R>(0.0);                          // z_{k-1}, z_{k-2}
+    R ldm1 = mk<R>(0.0), ldm2 = mk<R>(0.0), ucarry = mk<R>(0.0);  // ld_{k-1}, ld_{k-2}, u-_{b0-1}
+    auto put = [&](int64_t kk, R z) {
+        if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
+        const OutT zo = (OutT)hi(mul(z, inv));
+        accum_sq((double)zo, ss_hi, ss_lo);
+        zcol[kk] = zo;
+        return z;
+    };
+    auto drecompute = [&](const double *buf, int64_t t0, int64_t b0, R *lpb) {
+        R s = A.ck_s[(b0 / RQ_C) * A.S + slot];
 #pragma unroll
-                    for (int j = 0; j < RQ_C; j++) {
-                        const int64_t kk = b0 + j;
-                        lpb[j] = mk<R>(0.0);
-                        if (kk < n - 1 && kk < r) {
-                            Row4<R> rw = srow<R>(buf, t0, kk);
-                            R dp = guard(add(rw.d, s), A.pivmin);
-                            R lp = div(rw.ld, dp);
-                            lpb[j] = lp;
-                            s = sub(mul(lp, mul(rw.l, s)), lam);
-                        }
-                    }
+        for (int j = 0; j < RQ_C; j++) {
+            const int64_t kk = b0 + j;
+            lpb[j] = mk<R>(0.0);
+            if (kk < n - 1 && kk < r) {
+                Row4<R> rw = srow<R>(buf, t0, kk);
+                R dp = guard(add(rw.d, s), A.pivmin);
+                R lp = div(rw.ld, dp);
+                lpb[j] = lp;
+                s = sub(mul(lp, mul(rw.l, s)), lam);
+            }
+        }
+    };
+    auto dz = [&](const double *buf, int64_t t0, int64_t b0, const R *lpb) {
 #pragma unroll
-                    for (int j = RQ_C - 1; j >= 0; j--) {
-                        const int64_t kk = b0 + j;
-                        if (kk > r || kk >= n) continue;
-                        Row4<R> rw = srow<R>(buf, t0, kk);
-                        R z;
-                        if (kk == r) {
-                            z = mk<R>(1.0);
-                        } else if (hi(z1) == 0.0 && fabs(hi(z2v)) > tiny) {
-                            z = neg(mul(div(ldn, rw.ld), z2v));
-                        } else {
-                            z = neg(mul(lpb[j], z1));
-                        }
-                        if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
-                        OutT zo = (OutT)hi(mul(z, inv));
-                        tile[kk - t0][tid] = zo;
-                        accum_sq((double)zo, ss_hi, ss_lo);
-                        z2v = z1;
-                        z1 = z;
-                        ldn = rw.ld;
-                    }
+        for (int j = RQ_C - 1; j >= 0; j--) {
+            const int64_t kk = b0 + j;
+            if (kk > r || kk >= n) continue;
+            Row4<R> rw = srow<R>(buf, t0, kk);
+            R z;
+            if (kk == r)
+                z = mk<R>(1.0);
+            else if (hi(z1D) == 0.0 && fabs(hi(z2D)) > tiny)
+                z = neg(mul(div(ldn, rw.ld), z2D));
+            else
+                z = neg(mul(lpb[j], z1D));
+            z = put(kk, z);
+            z2D = z1D;
+            z1D = z;
+            ldn = rw.ld;
+        }
+    };
+    // u-_k for k in [b0, e), e = min(b0 + C, n - 1), from the checkpoint p_{b0+C}
+    auto urecompute = [&](const double *buf, int64_t t0, int64_t b0, R *ub) {
+        const int64_t e = (b0 + RQ_C < n - 1) ? b0 + RQ_C : n - 1;
+        R p;
+        if (e == b0 + RQ_C)
+            p = A.ck_p[((b0 + RQ_C) / RQ_C) * A.S + slot];
+        else
+            p = sub(srow<R>(buf, t0, n - 1).d, lam);
+#pragma unroll
+        for (int j = RQ_C - 1; j >= 0; j--) {
+            const int64_t kk = b0 + j;
+            ub[j] = mk<R>(0.0);
+            if (kk < e) {
+                Row4<R> rw = srow<R>(buf, t0, kk);
+                R Dm = guard(add(rw.lld, p), A.pivmin);
+                R t = div(rw.d, Dm);
+                ub[j] = mul(rw.l, t);
+                p = sub(mul(p, t), lam);
+            }
+        }
+    };
+    auto uz = [&](const double *buf, int64_t t0, int64_t b0, const R *ub) {
+#pragma unroll
+        for (int j = 0; j < RQ_C; j++) {
+            const int64_t kk = b0 + j;
+            const R uprev = (j == 0) ? ucarry : ub[j == 0 ? 0 : j - 1];
+            if (kk < n) {
+                const R ldk = srow<R>(buf, t0, kk).ld;
+                if (kk == r) {
+                    z1U = mk<R>(1.0);
+                    z2U = mk<R>(0.0);
+                } else if (kk > r) {
+                    R z;
+                    if (hi(z1U) == 0.0 && fabs(hi(z2U)) > tiny)
+                        z = neg(mul(div(ldm2, ldm1), z2U));
+                    else
+                        z = neg(mul(uprev, z1U));
+                    z = put(kk, z);
+                    z2U = z1U;
+                    z1U = z;
                 }
+                ldm2 = ldm1;
+                ldm1 = ldk;
             }
-            __syncthreads();
-            for (int c = warp; c < RQ_TPB; c += RQ_TPB / 32) {
-                const int64_t row = t0 + lane;
-                if (s_col[c] >= 0 && row < n && row <= s_r[c])
-                    Zo[(nd.row0 + row) + s_col[c] * A.ldz] = tile[lane][c];
-            }
-        });
-        if (mine) rows += r + 1;
-    }
-    // U sweep: rows k > r, bottom-up, z_k = -u-_{k-1} z_{k-1}
-    // (z_k = -(ld_{k-2}/ld_{k-1}) z_{k-2} if z_{k-1} == 0)
+        }
+        ucarry = ub[RQ_C - 1];
+    };
     {
-        R z1 = mk<R>(0.0), z2v = mk<R>(0.0);     // z_{k-1}, z_{k-2}
-        R ldm1 = mk<R>(0.0), ldm2 = mk<R>(0.0);  // ld_{k-1}, ld_{k-2}
-        R ucarry = mk<R>(0.0);                   // u-_{b0-1}
-        staged_pass<R>(sstage, nd.rep, n, false, [&](const double *buf, int64_t t0) {
-            if (mine && t0 + RQ_TR - 1 >= r) {
+        const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+        const int tmin = cta_rmin / RQ_TR, tmax = cta_rmax / RQ_TR;
+        // U: ascending from the tile of the smallest twist; D: descending from the largest
+        dual_staged_pass<Stage<R>::ROWD>(
+            sstage, nd.rep, n, tmin, ntile - tmin, tmax, tmax + 1,
+            [&](const double *bU, int64_t tU, const double *bD, int64_t tD) {
+                if (!mine) return;
 #pragma unroll 1
                 for (int q = 0; q < RQ_TR / RQ_C; q++) {
-                    const int64_t b0 = t0 + q * RQ_C;
-                    if (b0 >= n) continue;
-                    if (b0 + RQ_C - 1 < r) {  // below the twist: only track ld
-                        ldm2 = srow<R>(buf, t0, b0 + RQ_C - 2).ld;
-                        ldm1 = srow<R>(buf, t0, b0 + RQ_C - 1).ld;
-                        continue;
+                    const int64_t b0D = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
+                    const int64_t b0U = tU + q * RQ_C;
+                    const bool dD = bD != nullptr && b0D <= r && b0D < n;
+                    const bool dU = bU != nullptr && b0U < n && b0U + RQ_C - 1 >= r;
+                    if (bU != nullptr && b0U < n && b0U + RQ_C - 1 < r) {  // below the twist
+                        ldm2 = srow<R>(bU, tU, b0U + RQ_C - 2).ld;
+                        ldm1 = srow<R>(bU, tU, b0U + RQ_C - 1).ld;
                     }
-                    // recompute u-_k for k in [b0, e), e = min(b0 + C, n - 1)
-                    R ub[RQ_C];
-                    const int64_t e = (b0 + RQ_C < n - 1) ? b0 + RQ_C : n - 1;
-                    R p;
-                    if (e == b0 + RQ_C)
-                        p = A.ck_p[((b0 + RQ_C) / RQ_C) * A.S + slot];
-                    else
-                        p = sub(srow<R>(buf, t0, n - 1).d, lam);
-#pragma unroll
-                    for (int j = RQ_C - 1; j >= 0; j--) {
-                        const int64_t kk = b0 + j;
-                        ub[j] = mk<R>(0.0);
-                        if (kk < e) {
-                            Row4<R> rw = srow<R>(buf, t0, kk);
-                            R Dm = guard(add(rw.lld, p), A.pivmin);
-                            R t = div(rw.d, Dm);
-                            ub[j] = mul(rw.l, t);
-                            p = sub(mul(p, t), lam);
-                        }
+                    if (dD) {
+                        R lpb[RQ_C];
+                        drecompute(bD, tD, b0D, lpb);
+                        dz(bD, tD, b0D, lpb);
                     }
-#pragma unroll
-                    for (int j = 0; j < RQ_C; j++) {
-                        const int64_t kk = b0 + j;
-                        R uprev = (j == 0) ? ucarry : ub[j == 0 ? 0 : j - 1];
-                        if (kk < n) {
-                            R ldk = srow<R>(buf, t0, kk).ld;
-                            if (kk == r) {
-                                z1 = mk<R>(1.0);
-                                z2v = mk<R>(0.0);
-                            } else if (kk > r) {
-                                R z;
-                                if (hi(z1) == 0.0 && fabs(hi(z2v)) > tiny)
-                                    z = neg(mul(div(ldm2, ldm1), z2v));
-                                else
-                                    z = neg(mul(uprev, z1));
-                                if (fabs(hi(z)) < tiny) z = mk<R>(0.0);
-                                OutT zo = (OutT)hi(mul(z, inv));
-                                tile[kk - t0][tid] = zo;
-                                accum_sq((double)zo, ss_hi, ss_lo);
-                                z2v = z1;
-                                z1 = z;
-                            }
-                            ldm2 = ldm1;
-                            ldm1 = ldk;
-                        }
+                    if (dU) {
+                        R ub[RQ_C];
+                        urecompute(bU, tU, b0U, ub);
+                        uz(bU, tU, b0U, ub);
                     }
-                    ucarry = ub[RQ_C - 1];
                 }
-            }
-            __syncthreads();
-            for (int c = warp; c < RQ_TPB; c += RQ_TPB / 32) {
-                const int64_t row = t0 + lane;
-                if (s_col[c] >= 0 && row < n && row > s_r[c])
-                    Zo[(nd.row0 + row) + s_col[c] * A.ldz] = tile[lane][c];
-            }
-        });
-        if (mine) rows += n - r;
+            });
+        if (mine) rows += n + 1;
     }
     if (mine && A.fac) {
         // exact sum of squares of the written column vs 1 (fp64 output only)
