@@ -84,7 +84,10 @@ enum mr3_param {
     MR3_GRID = 11,     /* 1: start the bisection from a shared grid of Sturm counts (k_grid); 1 */
     MR3_CTA = 12,      /* threads per CTA of the staged kernels, 32..128 (0 = 128) */
     MR3_XPTS = 13,     /* binary_x multisection points per lane and round, 1 or 2; 1 */
-    MR3_NPARAM = 14
+    MR3_YCERT = 14,    /* 1: certify the root brackets of the binary_x phase by binary_y Sturm
+                          counts; 0: rigorous widening by the definite root's relative
+                          robustness bound instead (R8d); 0 */
+    MR3_NPARAM = 15
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

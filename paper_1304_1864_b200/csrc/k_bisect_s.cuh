@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
                                                   const int *__restrict__ ntasks, double rtol,
                                                   double absfloor, double pivmin, double pivmin_x,
                                                   double eps_x, int certify, int xpts,
-                                                  DevStats *st) {
+                                                  int ycert, DevStats *st) {
     __shared__ __align__(16) double sbuf[2 * BS_TILE];
     if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
     const RqiTask task = tasks[blockIdx.x];
@@ -538,6 +538,19 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
             if (lt(b, nb)) nb = b;
             a = na;
             b = nb;
+        }
+        if (!ycert && !certify) {
+            // root level without binary_y certification (reading R8d): [a, b] is the
+            // binary_x bracket widened by the typical M_x -> M_y shift; consumers that
+            // need a rigorous enclosure widen it by the relative-robustness bound of the
+            // definite root (k_rqi: root_widen)
+            if (active && lig == 0) {
+                reinterpret_cast<R *>(it.lo)[id] = a;
+                reinterpret_cast<R *>(it.hi)[id] = b;
+            }
+            if (rows) atomicAdd(&st->bisect_rows, rows);
+            if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
+            return;
         }
         certify_y(delta);
     }

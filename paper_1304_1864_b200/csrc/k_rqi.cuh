@@ -58,6 +58,8 @@ struct RqiArgs {
     double *fac;           // per local column: 1/||written column|| (fp64 output), 0 = exact
     int64_t S;             // checkpoint stride (CTAs in this launch * RQ_TPB)
     double pivmin, krs, eps_x, gaptol;
+    double root_widen;  // > 0: root-node brackets are binary_x brackets; the guard is widened
+                        // by root_widen * n * |lambda| (relative robustness of the root, R8d)
     int maxit;
     int jobz_v;
     void *w;          // eigenvalue output (global positions)
@@ -232,6 +234,11 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         lam = half(add(a, b));
         const double x0 = A.it.x0[id];
         if (!isnan(x0) && lt(a, mk<R>(x0)) && lt(mk<R>(x0), b)) lam = mk<R>(x0);
+        if (A.root_widen > 0.0 && nd.depth == 0) {
+            const double wd = A.root_widen * (double)n * fmax(fabs(hi(a)), fabs(hi(b)));
+            a = sub(a, mk<R>(wd));
+            b = add(b, mk<R>(wd));
+        }
         gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
         r = A.it.twist[id];

@@ -78,15 +78,16 @@ struct mr3_ctx_s {
     int G0 = 1;
     int64_t launches = 0;
     int debug = 0;
+    double root_widen = 0.0;  // relative guard widening per row of a root node (R8d), 0 = certified
     mr3_stats stats;
 };
 
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 1.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 1.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 1.0, 0.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 1.0, 0.0},
 };
 
 #define CK(call)                                                                  \
@@ -210,7 +211,7 @@ static int choose_tpb(mr3_ctx ctx, int64_t thr, int tpb_max) {
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x,
-                         const char *tname = "k_bisect") {
+                         const char *tname = "k_bisect", int ycert = 1) {
     if (cnt <= 0) return 0;
     int rc = 0;
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
@@ -233,11 +234,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
         if (xphase)                                                                           \
             k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, W.st);                                                         \
+                certify, xpts, ycert, W.st);                                                  \
         else                                                                                  \
             k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, W.st);                                                         \
+                certify, xpts, ycert, W.st);                                                  \
         break;
     switch (G) {
         BIS(1)
@@ -560,7 +561,12 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             CKL("k_grid_assign");
             kt_end(ctx, tg);
         }
-        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x);
+        // definite roots: binary_x brackets are enclosed rigorously after widening by the
+        // relative-robustness bound (R8d); binary_y certification only if MR3_YCERT
+        const int ycert = P[MR3_YCERT] != 0 ? 1 : 0;
+        ctx->root_widen = (xphase && !ycert) ? 10.0 * eps_x : 0.0;
+        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x,
+                              "k_bisect", ycert);
         if (rc) return rc;
         k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
                                                                     dbrk + 4 * first);
@@ -874,6 +880,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.krs = P[MR3_KRS];
                 A.eps_x = eps_x;
                 A.gaptol = gaptol;
+                A.root_widen = ctx->root_widen;
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
                 A.w = w;

@@ -328,3 +328,25 @@ def test_host_buffer_abi_matches_device_abi(io):
         w3, Z3, _ = mr3.solve_host(p.d, p.e, "N", rng, il, iu)  # pageable, values only
         assert Z3 is None
         np.testing.assert_array_equal(w1.cpu().numpy(), w3.numpy())
+
+
+@pytest.mark.parametrize("make", [lambda: synth.random_uniform(900, 11), lambda: synth.one_two_one(700),
+                                  lambda: synth.glued_wilkinson(12, 21),
+                                  lambda: synth.legendre(3000)])
+def test_root_certification_modes_agree(make):
+    """Reading R8d: the binary_x root brackets widened by the definite root's relative
+    robustness bound (MR3_YCERT = 0, default) give the same eigenpairs, bit for bit, as
+    certifying every bracket with binary_y Sturm counts (MR3_YCERT = 1)."""
+    p = make()
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    try:
+        mr3.set_param("YCERT", 1)
+        w1, Z1, s1 = mr3.mr3_dstemr_dd(d, e)
+        mr3.set_param("YCERT", 0)
+        w0, Z0, s0 = mr3.mr3_dstemr_dd(d, e)
+    finally:
+        mr3.set_param("YCERT", -1)
+    assert s1["bisect_rows"] > s0["bisect_rows"]
+    np.testing.assert_array_equal(w1.cpu().numpy(), w0.cpu().numpy())
+    np.testing.assert_array_equal(Z1.cpu().numpy(), Z0.cpu().numpy())
