@@ -33,8 +33,9 @@ import synth  # noqa: E402
 #   Sturm row, binary_y projective (2 pair fma + 1 pair mul)          37
 #   Sturm row, binary_x projective (2 DFMA + 1 DMUL + rescale/8)      3.25
 #   Sturm row, fp64-internal mode (projective, binary64)              3.25
+#   Newton pass row, binary_x (value + x-derivative, projective)      6.5
 #   RQI row (rqi_rows: 2 fixed-twist passes of n rows at 49 + the z sweeps' n rows at 69) 56
-FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25}
+FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25, "newton": 6.5}
 FP64_INST_PER_RQI_ROW = {"dd": 56.0, "f64": 12.0}
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 
@@ -266,10 +267,15 @@ def main():
         if kname == "k_bisect":
             rows = stats["bisect_rows"] if stats else 0.0
             rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
-            inst = rows * FP64_INST_PER_BISECT_ROW[mode] + rows_x * FP64_INST_PER_BISECT_ROW["x"]
+            rows_n = stats.get("newton_rows_x", 0.0) if stats else 0.0
+            inst = (rows * FP64_INST_PER_BISECT_ROW[mode] +
+                    (rows_x - rows_n) * FP64_INST_PER_BISECT_ROW["x"] +
+                    rows_n * FP64_INST_PER_BISECT_ROW["newton"])
             per = {"binary_y_row": FP64_INST_PER_BISECT_ROW[mode],
-                   "binary_x_row": FP64_INST_PER_BISECT_ROW["x"]}
-            units = {"binary_y_rows": rows, "binary_x_rows": rows_x}
+                   "binary_x_row": FP64_INST_PER_BISECT_ROW["x"],
+                   "binary_x_newton_row": FP64_INST_PER_BISECT_ROW["newton"]}
+            units = {"binary_y_rows": rows, "binary_x_rows": rows_x - rows_n,
+                     "binary_x_newton_rows": rows_n}
         else:
             rows = stats["rqi_rows"] if stats else 0.0
             inst = rows * FP64_INST_PER_RQI_ROW[mode]

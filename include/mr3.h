@@ -64,6 +64,7 @@ typedef struct {
     double bisect_rows;          /* Sturm-count rows executed (dstqds steps) */
     double rqi_rows;             /* twisted-factorisation rows executed */
     double bisect_rows_x;        /* Sturm-count rows executed in binary_x (fp64 phase) */
+    double newton_rows_x;        /* of which Newton passes (count + derivative, R8e) */
     double t_ms[8];
 } mr3_stats;
 
@@ -83,11 +84,13 @@ enum mr3_param {
                           half-width exceeds gap*sqrt(eps_x sqrt(n)/C) get a binary_x start; 4 */
     MR3_GRID = 11,     /* 1: start the bisection from a shared grid of Sturm counts (k_grid); 1 */
     MR3_CTA = 12,      /* threads per CTA of the staged kernels, 32..128 (0 = 128) */
-    MR3_XPTS = 13,     /* binary_x multisection points per lane and round, 1 or 2; 1 */
+    MR3_XPTS = 13,     /* binary_x root phase: 1 bisection / multisection, 2 two points per lane,
+                          3 Newton-accelerated bisection (G = 1; R8e); 3 */
     MR3_YCERT = 14,    /* 1: certify the root brackets of the binary_x phase by binary_y Sturm
                           counts; 0: rigorous widening by the definite root's relative
                           robustness bound instead (R8d); 0 */
-    MR3_NPARAM = 15
+    MR3_NEWTON = 15,   /* Newton passes per item before the many-lane multisection tail; 6 */
+    MR3_NPARAM = 16
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

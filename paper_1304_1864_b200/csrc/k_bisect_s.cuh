@@ -23,6 +23,7 @@ namespace mr3 {
 constexpr int BS_TPB = 128;  // threads per CTA (maximum; launches pick 32..128)
 constexpr int BS_TR = 256;   // rows per staged tile
 constexpr int BS_TILE = BS_TR * 4;  // doubles per tile buffer (rows of up to 32 B)
+constexpr int NEWTON_MAXPASS_DEFAULT = 8;  // Newton x-phase passes before the tail launch
 
 __device__ __forceinline__ void bs_cp_async16(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -162,6 +163,153 @@ __device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, boo
 // per row two pair FMAs and one pair product, a dependent chain of two FMAs.
 // (p, q) is rescaled by an exact power of two every XB rows; an overflow (only
 // possible for |lld| > 1e38) redoes the block in the guarded ratio form.
+// One binary_x pass giving the Sturm count at x and the Newton ratio f/f' of
+// f(x) = det(M_x - x I) = D_{n-1} (x the projective scale factors): the x-derivative
+// of the projective recurrence is carried along,
+//   D'_j = d_j q'_j + p'_j,  q'_{j+1} = D'_j,  p'_{j+1} = lld_j p'_j - D_j - x D'_j,
+// (p'_0 = -1, q'_0 = 0), rescaled with (p, q) by the same power of two (the ratio is
+// scale-free).  Six FP64 instructions per row; the derivative chain runs beside the
+// value chain.
+__device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, bool need, double x,
+                                             double pivmin, int &cnt, double &ratio) {
+    const int64_t n = nd.n;
+    double p = -x, q = 1.0, pd = -1.0, qd = 0.0;
+    unsigned c = 0;
+    bool bad = false;
+    tile_pass(
+        smem, n, [&](double *buf, int64_t t0) { stage_x_tile(buf, nd.repx, n, t0); },
+        [&](const double *buf, int64_t t0, int rows) {
+            if (!need) return;
+            const double2 *t = reinterpret_cast<const double2 *>(buf);
+            const bool last = t0 + rows == n;
+            const int full = last ? rows - 1 : rows;
+            auto row = [&](const double2 r) {
+                const double D = fma_rn(r.x, q, p);
+                const double Dd = fma_rn(r.x, qd, pd);
+                c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+                const double pn = fma_rn(-x, D, mul_rn(r.y, p));
+                pd = fma_rn(-x, Dd, fma_rn(r.y, pd, -D));
+                p = pn;
+                q = D;
+                qd = Dd;
+            };
+            int j = 0;
+#pragma unroll 1
+            for (; j < full; j += XB) {
+                const int je = min(j + XB, full);
+                if (je - j == XB) {
+#pragma unroll
+                    for (int u = 0; u < XB; u++) row(t[j + u]);
+                } else {
+                    for (int u = j; u < je; u++) row(t[u]);
+                }
+                // one power of two for all four (the largest exponent -> 2^0)
+                unsigned em = (unsigned)__double2hiint(p) & 0x7ff00000u;
+                em = max(em, (unsigned)__double2hiint(q) & 0x7ff00000u);
+                em = max(em, (unsigned)__double2hiint(pd) & 0x7ff00000u);
+                em = max(em, (unsigned)__double2hiint(qd) & 0x7ff00000u);
+                if (em == 0x7ff00000u) {
+                    bad = true;  // overflow: count and ratio unreliable -> caller bisects
+                    p = -x;
+                    q = 1.0;
+                    pd = -1.0;
+                    qd = 0.0;
+                } else {
+                    const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+                    p *= sc;
+                    q *= sc;
+                    pd *= sc;
+                    qd *= sc;
+                }
+            }
+            if (last) {
+                const double D = fma_rn(t[rows - 1].x, q, p);
+                const double Dd = fma_rn(t[rows - 1].x, qd, pd);
+                c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+                ratio = D / Dd;
+            }
+        });
+    cnt = (int)c;
+    if (__syncthreads_or(bad)) {  // rare: recount the affected threads (collective call)
+        const int c2 = count_x_cta(smem, nd, need && bad, x, pivmin);
+        if (bad) {
+            ratio = NAN;
+            cnt = c2;
+        }
+    }
+}
+
+// Sturm-count bisection accelerated by Newton steps on f(x) = det(M_x - x I) (G = 1):
+// every pass returns count(x) (the bracket invariant count(a) < k <= count(b) is kept
+// exactly as in bisection) and f/f'; the next point is the Newton iterate when it lies
+// inside the bracket and the bracket has been shrinking, else the midpoint.  Once the
+// Newton step is below tol/4 the next point is placed tol/4 beyond the estimate on the
+// other side, so one more pass closes the bracket to width <= tol/2.  Convergence is
+// quadratic near a simple eigenvalue; a bracket holding several eigenvalues is reduced
+// by the counts (any Newton iterate outside the bracket falls back to bisection).
+__device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, double &a, double &b,
+                                           bool active, int k, double rtol, double absfloor,
+                                           double tolmul, double pivmin,
+                                           unsigned long long &rows, int64_t n, int &passes,
+                                           int maxpass, bool &converged) {
+    bool mdone = !active;
+    passes = 0;
+    converged = false;
+    double xn = NAN;
+    double r1 = INFINITY, r2 = INFINITY;  // |Newton step| of the last two Newton passes
+    int nnewton = 0;
+#pragma unroll 1
+    for (int round = 0; round < 4000; round++) {
+        double x = a;
+        bool need = false;
+        double tol = 0.0;
+        bool took_newton = false;
+        if (!mdone) {
+            const double w = b - a;
+            tol = tolmul * fmax(2.0 * rtol * fmax(fabs(a), fabs(b)), absfloor);
+            if (w <= tol) {
+                mdone = true;
+                converged = true;
+            } else if (passes >= maxpass) {
+                mdone = true;  // left to the many-lane multisection (tail launch)
+            } else {
+                // Newton while its steps contract (|step| at least halves every round)
+                // and stay inside the bracket; bisection otherwise
+                const bool contracting = nnewton < 2 || r1 <= 0.5 * r2;
+                took_newton = !isnan(xn) && xn > a && xn < b && contracting && nnewton < 12;
+                x = took_newton ? xn : 0.5 * (a + b);
+                need = a < x && x < b;
+                if (!need) mdone = true;  // no representable progress
+            }
+        }
+        if (!__syncthreads_or(!mdone)) break;
+        int c = 0;
+        double ratio = NAN;
+        count_xn_cta(smem, nd, need, x, pivmin, c, ratio);
+        if (need) {
+            rows += n;
+            passes++;
+            if (c >= k)
+                b = x;
+            else
+                a = x;
+            xn = NAN;
+            if (fabs(ratio) < INFINITY) {
+                const double est = x - ratio;
+                if (took_newton || nnewton == 0) {
+                    nnewton++;
+                    r2 = r1;
+                    r1 = fabs(ratio);
+                }
+                if (fabs(ratio) <= 0.25 * tol)
+                    xn = est + (c >= k ? -0.25 * tol : 0.25 * tol);
+                else
+                    xn = est;
+            }
+        }
+    }
+}
+
 // two shifts per thread through the same rows (two independent FMA chains: the
 // binary_x row chain is two dependent DFMAs, so one chain per thread leaves the
 // FP64 pipe waiting on latency at the 2-3 warps per scheduler a 50000-item
@@ -456,7 +604,8 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
                                                   const int *__restrict__ ntasks, double rtol,
                                                   double absfloor, double pivmin, double pivmin_x,
                                                   double eps_x, int certify, int xpts,
-                                                  int ycert, DevStats *st) {
+                                                  int ycert, char *tailflag, int xpts_maxpass,
+                                                  DevStats *st) {
     __shared__ __align__(16) double sbuf[2 * BS_TILE];
     if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
     const RqiTask task = tasks[blockIdx.x];
@@ -519,7 +668,23 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
     if (certify) certify_y(absfloor);
     if (XPHASE) {
         double ax = hi(a), bx = hi(b);
-        if (xpts == 2)
+        if (G == 1 && xpts == 3) {
+            int passes = 0;
+            bool conv = true;
+            newton_cta(sbuf, nd, ax, bx, active, k, rtol, absfloor, 0.5, pivmin_x, rows_x, n, passes,
+                       tailflag ? xpts_maxpass : 4000, conv);
+            if (passes) atomicAdd(&st->newton_rows_x, (unsigned long long)passes * n);
+            if (active) it.x0[id] = (double)passes;  // diagnostics (MR3_DEBUG); reset before RQI
+            if (tailflag && active) tailflag[local + task.first] = conv ? 0 : 1;
+            if (tailflag && active && !conv) {
+                // unfinished: hand the current (valid) bracket to the tail launch
+                reinterpret_cast<R *>(it.lo)[id] = mk<R>(ax);
+                reinterpret_cast<R *>(it.hi)[id] = mk<R>(bx);
+                if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
+                return;  // tail mode is only used with ycert == 0, certify == 0: no barrier follows
+            }
+        }
+        else if (xpts == 2)
             msect2_cta<G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x, n,
                           [&](bool need, double x0, double x1, int &c0, int &c1) {
                               count_x2_cta(sbuf, nd, need, x0, x1, pivmin_x, c0, c1);

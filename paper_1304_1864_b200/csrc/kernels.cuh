@@ -54,6 +54,7 @@ struct DevStats {
     int n_clusters;
     int pad;
     unsigned long long refine_rows_x;  // binary_x rows of the RQI start refinement (K2')
+    unsigned long long newton_rows_x;  // binary_x rows of Newton passes (subset of bisect_rows_x)
 };
 
 template <class R>

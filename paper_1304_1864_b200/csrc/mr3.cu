@@ -85,9 +85,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 1.0, 0.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 1.0, 0.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0},
 };
 
 #define CK(call)                                                                  \
@@ -211,11 +211,15 @@ static int choose_tpb(mr3_ctx ctx, int64_t thr, int tpb_max) {
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x,
-                         const char *tname = "k_bisect", int ycert = 1) {
+                         const char *tname = "k_bisect", int ycert = 1, char *tailflag = nullptr) {
     if (cnt <= 0) return 0;
     int rc = 0;
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
-    const int xpts = ctx->cfg[ctx->mode].v[MR3_XPTS] == 1 ? 1 : 2;
+    int xpts = (int)ctx->cfg[ctx->mode].v[MR3_XPTS];
+    if (xpts == 3 && (G != 1 || !xphase || certify || ycert)) xpts = 1;  // Newton: G = 1 root x-phase only
+    if (xpts != 3) tailflag = nullptr;
+    const int maxpass = ctx->cfg[ctx->mode].v[MR3_NEWTON] > 0 ? (int)ctx->cfg[ctx->mode].v[MR3_NEWTON]
+                                                               : NEWTON_MAXPASS_DEFAULT;
     const int per = tpb / G;
     // CTA tasks: runs of <= per items of one node; the grid is an upper bound on
     // their number (the kernel reads the exact count), so no host round trip
@@ -234,11 +238,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
         if (xphase)                                                                           \
             k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, W.st);                                                  \
+                certify, xpts, ycert, tailflag, maxpass, W.st);                               \
         else                                                                                  \
             k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, W.st);                                                  \
+                certify, xpts, ycert, tailflag, maxpass, W.st);                               \
         break;
     switch (G) {
         BIS(1)
@@ -528,7 +532,9 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         const bool xphase = words == 2 && P[MR3_XPHASE] != 0;
         if (!ctx->split && P[MR3_GRID] != 0 && cnt >= 512) {
             // shared top of the bisection tree: brackets from two grids of counts
-            const int m2 = (int)std::min<int64_t>((int64_t)(1.5 * cnt) + 64, 1 << 30);
+            // level-2 points per requested index: MR3_GRID (1 = default 1.5)
+            const double gfac = P[MR3_GRID] == 1.0 ? 1.5 : P[MR3_GRID];
+            const int m2 = (int)std::min<int64_t>((int64_t)(gfac * cnt) + 64, 1 << 30);
             GridInfo *gi = (GridInfo *)getbuf(ctx, "grid_info", sizeof(GridInfo), &rc);
             int *c1 = (int *)getbuf(ctx, "grid_c1", GRID_L1 * 4, &rc);
             int *c2 = (int *)getbuf(ctx, "grid_c2", (size_t)m2 * 4, &rc);
@@ -565,8 +571,37 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         // relative-robustness bound (R8d); binary_y certification only if MR3_YCERT
         const int ycert = P[MR3_YCERT] != 0 ? 1 : 0;
         ctx->root_widen = (xphase && !ycert) ? 10.0 * eps_x : 0.0;
+        char *tail = nullptr;
+        const bool newton = xphase && !ycert && ctx->G0 == 1 && P[MR3_XPTS] == 3;
+        if (newton) {
+            tail = (char *)getbuf(ctx, "bis_tailflag", (size_t)mine, &rc);
+            if (rc) return rc;
+        }
         rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x,
-                              "k_bisect", ycert);
+                              "k_bisect", ycert, tail);
+        if (rc) return rc;
+        if (newton) {
+            // items whose Newton phase did not finish in NEWTON_MAXPASS passes: multisection
+            // with many lanes per item from their current brackets
+            int32_t *tl = (int32_t *)getbuf(ctx, "bis_taillist", (size_t)mine * 4, &rc);
+            int *tc = (int *)getbuf(ctx, "bis_tailcnt", 16, &rc);
+            if (rc) return rc;
+            size_t tmpb = 0;
+            cub::DeviceSelect::Flagged(nullptr, tmpb, list, tail, tl, tc, (int)mine, s);
+            void *tmp = getbuf(ctx, "cubtmp_tail", tmpb, &rc);
+            if (rc) return rc;
+            cub::DeviceSelect::Flagged(tmp, tmpb, list, tail, tl, tc, (int)mine, s);
+            CKL("select (tail)");
+            int ht = 0;
+            CK(cudaMemcpyAsync(&ht, tc, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (ht > 0) {
+                int G = choose_groups(ctx, ht, 0);
+                if (G < 8) G = 8;
+                rc = launch_bisect<R>(ctx, W, tl, ht, G, rtol, absfloor, 0, true, eps_x, "k_bisect",
+                                      0, nullptr);
+            }
+        }
         if (rc) return rc;
         k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
                                                                     dbrk + 4 * first);
@@ -705,6 +740,27 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int nsing = hc[0], nclus = hc[1], nmem = hc[2];
+    if (ctx->debug && P[MR3_XPTS] == 3) {  // passes per item of the Newton x-phase
+        std::vector<double> ps(cnt);
+        cudaMemcpy(ps.data(), W.it.x0, cnt * 8, cudaMemcpyDeviceToHost);
+        int hist[41] = {0};
+        for (int i = 0; i < cnt; i++) hist[std::min(40, std::max(0, (int)ps[i]))]++;
+        fprintf(stderr, "[mr3] newton passes histogram:");
+        for (int i = 0; i <= 40; i++)
+            if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
+        fprintf(stderr, "\n");
+        // per 128-item CTA: max passes histogram
+        int chist[41] = {0};
+        for (int b0 = 0; b0 < cnt; b0 += 128) {
+            int mx = 0;
+            for (int i = b0; i < std::min(cnt, b0 + 128); i++) mx = std::max(mx, (int)ps[i]);
+            chist[std::min(40, mx)]++;
+        }
+        fprintf(stderr, "[mr3] newton CTA-max passes histogram:");
+        for (int i = 0; i <= 40; i++)
+            if (chist[i]) fprintf(stderr, " %d:%d", i, chist[i]);
+        fprintf(stderr, "\n");
+    }
     if (ctx->debug) fprintf(stderr, "[mr3] level 0: %d singles %d clusters %d members\n", nsing, nclus, nmem);
 
     // multi-rank: cluster-whole partition of the output columns
@@ -1111,6 +1167,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     ctx->stats.rqi_iters_max = hst.rqi_iters_max;
     ctx->stats.bisect_rows = (double)hst.bisect_rows;
     ctx->stats.bisect_rows_x = (double)hst.bisect_rows_x;
+    ctx->stats.newton_rows_x = (double)hst.newton_rows_x;
     ctx->stats.rqi_rows = (double)hst.rqi_rows;
     for (auto &p : ctx->ktimes) {
         const std::string &nm = p.first;
