@@ -369,44 +369,64 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     // sweeps below need).  Returns the inertia of the twisted factorization
     // N_r Delta_r N_r^T = M - lam I, Delta_r = diag(d+_0..d+_{r-1}, gamma_r,
     // D-_{r+1}..D-_{n-1}), i.e. negcount(lam) (Sylvester).
+    // Fixed-twist factorization in projective (division-free) form, as the Sturm counts
+    // (R8b): top-down s = pF/qF with D = d qF + pF (= d+ qF), pF <- lld pF - lam D,
+    // qF <- D; bottom-up p = pB/qB with E = lld_{k-1} qB + pB (= D-_k qB),
+    // pB <- d_{k-1} pB - lam E, qB <- E.  Every row is two pair FMAs and a pair product
+    // (no division on the dependent chain); l+ and u- enter only the binary64 norm
+    // identities, formed off-chain.  Ratios s_b0, p_b0 are formed once per checkpoint.
     auto twisted_fixed = [&](bool need) -> int {
-        R s = neg(lam);
+        const R mlam = neg(lam);
+        R pF = mlam, qF = mk<R>(1.0);
         double W = 0.0;
         int negc = 0;
-        R p = mk<R>(0.0);
+        R pB = mk<R>(0.0), qB = mk<R>(1.0);
         double V = 0.0;
-        if (need) p = sub(load_row4<R>(nd.rep, n - 1).d, lam);
+        if (need) pB = sub(load_row4<R>(nd.rep, n - 1).d, lam);
         // F: rows 0..r-1 ascending (tiles 0 .. cta_rmax/RQ_TR); B: rows n-1..r descending
         const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
         const int nA = cta_rmax / RQ_TR + 1;
         const int nD = ntile - cta_rmin / RQ_TR;
+        auto sgn_ne = [](R x, R y) -> int {
+            return (int)((unsigned)(__double2hiint(hi(x)) ^ __double2hiint(hi(y))) >> 31);
+        };
+        auto rescale_pq = [](R &x, R &y) {
+            const unsigned ex = (unsigned)__double2hiint(hi(x)) & 0x7ff00000u;
+            const unsigned ey = (unsigned)__double2hiint(hi(y)) & 0x7ff00000u;
+            const unsigned em = ex > ey ? ex : ey;
+            if (em == 0x7ff00000u || em == 0u) return;
+            const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+            x = scale_pow2(x, sc);
+            y = scale_pow2(y, sc);
+        };
         // one F row (rows < r) and one B row (rows > r); predicated commits keep the two
         // recurrences in one basic block so their dependent chains interleave
         auto frow = [&](const double *bA, int64_t tA, int64_t kk) {
             Row4<R> rw = srow<R>(bA, tA, kk);
-            R dp = guard(add(rw.d, s), A.pivmin);
-            R lp = div(rw.ld, dp);
-            double l2 = hi(lp) * hi(lp);
-            double W2 = clampbig(fma(l2, W, l2));
-            R s2 = sub(mul(lp, mul(rw.l, s)), lam);
+            const R D = fma_dd(rw.d, qF, pF);
+            const double lpx = hi(rw.ld) * hi(qF) * rcp(hi(D));  // l+ = ld / d+
+            const double l2 = lpx * lpx;
+            const double W2 = clampbig(fma(l2, W, l2));
+            const R p2 = fma_dd(mlam, D, mul(rw.lld, pF));
             if (kk < r) {
-                negc += is_neg(dp) ? 1 : 0;
+                negc += sgn_ne(D, qF);
                 W = W2;
-                s = s2;
+                pF = p2;
+                qF = D;
             }
         };
         auto brow = [&](const double *bD, int64_t tD, int64_t kk) {
             Row4<R> rw = srow<R>(bD, tD, kk - 1);
-            R Dm = guard(add(rw.lld, p), A.pivmin);
-            R t = div(rw.d, Dm);
-            double u2 = hi(rw.l) * hi(t);
-            u2 *= u2;
-            double V2 = clampbig(fma(u2, V, u2));
-            R p2 = sub(mul(p, t), lam);
+            const R E = fma_dd(rw.lld, qB, pB);
+            const double ux = hi(rw.l) * hi(rw.d) * hi(qB) * rcp(hi(E));  // u- = l d / D-
+            const double u2 = ux * ux;
+            const double V2 = clampbig(fma(u2, V, u2));
+            const R P2 = fma_dd(mlam, E, mul(rw.d, pB));
             if (kk > r && kk < n) {
-                negc += is_neg(Dm) ? 1 : 0;
+                negc += sgn_ne(E, qB);
                 V = V2;
-                p = p2;  // p_{kk-1}
+                pB = P2;  // p_{kk-1} = pB / qB
+                qB = E;
             }
         };
         dual_staged_pass<Stage<R>::ROWD>(
@@ -420,14 +440,15 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                     const bool fF = bA != nullptr && b0F < r;
                     const bool fB = bD != nullptr && b0B + RQ_C > r && b0B < n;
                     if (bA != nullptr && b0F <= r) {
-                        A.ck_s[(b0F / RQ_C) * A.S + slot] = s;
+                        A.ck_s[(b0F / RQ_C) * A.S + slot] = div(pF, qF);
                         A.ck_W[(b0F / RQ_C) * A.S + slot] = W;
                     }
                     if (fF && fB) {
 #pragma unroll
                         for (int j = 0; j < RQ_C; j++) {
                             const int64_t kB = b0B + RQ_C - 1 - j;
-                            if (j == RQ_C - 1 && kB >= r) A.ck_p[(b0B / RQ_C) * A.S + slot] = p;
+                            if (j == RQ_C - 1 && kB >= r)
+                                A.ck_p[(b0B / RQ_C) * A.S + slot] = div(pB, qB);
                             frow(bA, tA, b0F + j);
                             brow(bD, tD, kB);
                         }
@@ -438,14 +459,17 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 #pragma unroll
                         for (int j = 0; j < RQ_C; j++) {
                             const int64_t kB = b0B + RQ_C - 1 - j;
-                            if (j == RQ_C - 1 && kB >= r) A.ck_p[(b0B / RQ_C) * A.S + slot] = p;
+                            if (j == RQ_C - 1 && kB >= r)
+                                A.ck_p[(b0B / RQ_C) * A.S + slot] = div(pB, qB);
                             brow(bD, tD, kB);
                         }
                     }
+                    if (fF) rescale_pq(pF, qF);
+                    if (fB) rescale_pq(pB, qB);
                 }
             });
         if (need) {
-            gr = add(add(s, p), lam);
+            gr = add(add(div(pF, qF), div(pB, qB)), lam);
             negc += is_neg(gr) ? 1 : 0;
             nz2 = 1.0 + W + V;
             rows += n;
