@@ -22,22 +22,25 @@
 //   lam <- lam + gamma_r / ||z||^2          (RQ correction, L714-L717)
 //   stop: |gamma_r|/||z|| <= k_rs gap eps_x sqrt(n)   (Eq. (3.6))
 //         or |gamma_r|/||z||^2 <= 8 eps_y |lam|        (stagnation, L720-L723)
-// The iterate is kept inside the certified bracket (F's count updates it); an
-// iterate leaving it is replaced by the bracket midpoint (RQI "guarded by
-// bisection", L315); after max_rqi iterations: bisection to relative
+// The iterate is kept inside the certified bracket (the inertia of each factorization
+// updates it); an iterate leaving it is replaced by the bracket midpoint (RQI "guarded
+// by bisection", L315); after max_rqi iterations: bisection to relative
 // eps_x sqrt(n) gaptol and one more twisted solve (L1154-L1163).
-// The output is normalised with the binary64 norm estimate and the exact norm
-// of what is written is summed in pair arithmetic; k_fixnorm rescales the few
-// columns whose estimate was off by more than 2^-54.
 //
-// Storage: the forward state (s, W) and backward state p are checkpointed every
-// RQ_C rows (5 B/row/eigenpair in dd) instead of storing whole sweeps; each
-// block of RQ_C rows is recomputed into registers when a sweep needs it in the
-// other direction (SURVEY.md §7 hard part 2, option (c)).
+// Fixed twist (R9b): the binary_y factorizations run with the twist r located by
+// k_rqi_locate, top-down to r and bottom-up to r interleaved (two chains per thread),
+// in projective form (R8b).  The eigenvector (K6) is written by the last
+// factorization itself in product form (k_zprod.cuh): z_i = y_i / y_r above the
+// twist and x_k / x_r below it, so no back-substitution sweep and no checkpoint
+// storage is needed on the regular path; k_zscale applies the per-column factors
+// and the exact 1/||z|| (squares accumulated with compensated sums while writing).
+// Only the rare fallback path keeps the sweep form (checkpoints of (s, W) and p every
+// RQ_C rows, blocks recomputed when the sweep needs them in the other direction).
 #pragma once
 #include <type_traits>
 
 #include "k_bisect.cuh"
+#include "k_zprod.cuh"
 
 namespace mr3 {
 
@@ -55,7 +58,7 @@ struct RqiArgs {
     const RqiTask *tasks;  // one per CTA
     R *ck_s, *ck_p;        // [nblk][S]
     double *ck_W;          // [nblk][S]
-    double *fac;           // per local column: 1/||written column|| (fp64 output), 0 = exact
+    ZCol *zc;              // per local column: rows, twist and factors for k_zscale
     int64_t S;             // checkpoint stride (CTAs in this launch * RQ_TPB)
     double pivmin, krs, eps_x, gaptol;
     double root_widen;  // > 0: root-node brackets are binary_x brackets; the guard is widened
@@ -212,6 +215,9 @@ template <class R, class OutT>
 __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     __shared__ __align__(16) double sstage[4 * Stage<R>::TILE];  // 4 tiles: dual_staged_pass
     __shared__ int s_rmin, s_rmax;
+    __shared__ OutT ztF[16][RQ_TPB + 1], ztB[16][RQ_TPB + 1];  // z tiles of a storing pass
+    __shared__ int64_t s_r[RQ_TPB], s_zoff[RQ_TPB];
+    __shared__ int s_wz[RQ_TPB];
 
     const int tid = threadIdx.x;
     const RqiTask task = A.tasks[blockIdx.x];
@@ -262,6 +268,25 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     __syncthreads();
     const int cta_rmin = s_rmin <= s_rmax ? s_rmin : 0;
     const int cta_rmax = s_rmin <= s_rmax ? s_rmax : (int)n - 1;
+
+    // output column of this eigenpair (rows of its block) and the factors for k_zscale
+    const int64_t col0 = active ? A.it.col[id] : -1;
+    OutT *zcol = (A.jobz_v && active && col0 >= 0)
+                     ? reinterpret_cast<OutT *>(A.Z) + nd.row0 + (col0 - A.zcol0) * A.ldz
+                     : nullptr;
+    ZCol zinfo;
+    zinfo.row0 = nd.row0;
+    zinfo.n = (int32_t)n;
+    zinfo.r = (int32_t)r;
+    zinfo.cF = 1.0;
+    zinfo.cB = 1.0;
+    zinfo.ss = 1.0;
+    bool zwritten = false, zfinal = false;
+    int erefF = 0, erefB = 0;
+    if (zcol != nullptr && n == 1) {  // 1x1 block: z = e_1
+        zcol[0] = (OutT)1.0;
+        zfinal = true;
+    }
 
     // one twisted factorization at lam for the threads with `need`
     auto twisted = [&](bool need) -> int {
@@ -375,9 +400,12 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     // pB <- d_{k-1} pB - lam E, qB <- E.  Every row is two pair FMAs and a pair product
     // (no division on the dependent chain); l+ and u- enter only the binary64 norm
     // identities, formed off-chain.  Ratios s_b0, p_b0 are formed once per checkpoint.
-    auto twisted_fixed = [&](bool need) -> int {
+    auto twisted_fixed = [&](bool need, bool store) -> int {
+        if (need) zwritten = false;
+        double sF = 0.0, cF_ = 0.0, sB = 0.0, cB_ = 0.0;  // Kahan sums of written squares
         const R mlam = neg(lam);
         R pF = mlam, qF = mk<R>(1.0);
+        int EqF = 0, EqB = 0;  // exponents taken out of (pF, qF) / (pB, qB) by the rescaling
         double W = 0.0;
         int negc = 0;
         R pB = mk<R>(0.0), qB = mk<R>(1.0);
@@ -390,7 +418,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         auto sgn_ne = [](R x, R y) -> int {
             return (int)((unsigned)(__double2hiint(hi(x)) ^ __double2hiint(hi(y))) >> 31);
         };
-        auto rescale_pq = [](R &x, R &y) {
+        auto rescale_pq = [](R &x, R &y, int &E) {
             const unsigned ex = (unsigned)__double2hiint(hi(x)) & 0x7ff00000u;
             const unsigned ey = (unsigned)__double2hiint(hi(y)) & 0x7ff00000u;
             const unsigned em = ex > ey ? ex : ey;
@@ -398,6 +426,28 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
             x = scale_pow2(x, sc);
             y = scale_pow2(y, sc);
+            E += (int)(em >> 20) - 1023;
+        };
+        // z components in product form (k_zprod.cuh): row kk <= r: y = qF / PP_kk,
+        // row kk >= r: x = QB PP_kk, written scaled by 2^-ref (ref from the previous pass)
+        const bool wz = store && need && zcol != nullptr;
+        auto ppr = [&](int64_t kk, double &pm, double &ipm, int &e) {
+            const double2 *q = reinterpret_cast<const double2 *>(nd.pp + kk * PP_STRIDE);
+            const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
+            pm = a0.x;
+            ipm = a0.y;
+            e = (int)a1.x;
+        };
+        // value * 2^k (k <= 1023; results below the normal range flush to zero)
+        auto pow2mul = [](double v, int k) -> double {
+            return k < -1022 ? 0.0 : v * __hiloint2double((k + 1023) << 20, 0);
+        };
+        // compensated (Kahan) sums of the squares of the written F and B parts
+        auto kahan = [](double x, double &sum, double &comp) {
+            const double y = fma(x, x, -comp);
+            const double t = sum + y;
+            comp = (t - sum) - y;
+            sum = t;
         };
         // one F row (rows < r) and one B row (rows > r); predicated commits keep the two
         // recurrences in one basic block so their dependent chains interleave
@@ -409,6 +459,14 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double W2 = clampbig(fma(l2, W, l2));
             const R p2 = fma_dd(mlam, D, mul(rw.lld, pF));
             if (kk < r) {
+                if (wz) {
+                    double pm, ipm;
+                    int e;
+                    ppr(kk, pm, ipm, e);
+                    const OutT zo = (OutT)pow2mul(hi(qF) * ipm, EqF - e - erefF);
+                    ztF[(kk - tA) & 15][tid] = zo;
+                    kahan((double)zo, sF, cF_);
+                }
                 negc += sgn_ne(D, qF);
                 W = W2;
                 pF = p2;
@@ -423,49 +481,77 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double V2 = clampbig(fma(u2, V, u2));
             const R P2 = fma_dd(mlam, E, mul(rw.d, pB));
             if (kk > r && kk < n) {
+                if (wz) {
+                    double pm, ipm;
+                    int e;
+                    ppr(kk, pm, ipm, e);
+                    const OutT zo = (OutT)pow2mul(hi(qB) * pm, EqB + e - erefB);
+                    ztB[(kk - tD) & 15][tid] = zo;
+                    kahan((double)zo, sB, cB_);
+                }
                 negc += sgn_ne(E, qB);
                 V = V2;
                 pB = P2;  // p_{kk-1} = pB / qB
                 qB = E;
             }
         };
+        // storing pass: the written components go through two 16-row smem tiles (one per
+        // stream) and leave as coalesced 128-byte column segments
+        const bool cta_store = store && A.jobz_v;  // uniform over the CTA
+        if (cta_store) {
+            s_wz[tid] = wz ? 1 : 0;
+            s_r[tid] = r;
+            s_zoff[tid] = wz ? (col0 - A.zcol0) * A.ldz + nd.row0 : 0;
+        }
+        auto flush = [&](const double *bA, int64_t tA, int hA, const double *bD, int64_t tD,
+                         int hD) {
+            __syncthreads();
+            OutT *Zo = reinterpret_cast<OutT *>(A.Z);
+            const int warp = tid >> 5, lane = tid & 31, row = lane & 15;
+            for (int c = 2 * warp + (lane >> 4); c < RQ_TPB; c += 2 * (RQ_TPB / 32)) {
+                if (!s_wz[c]) continue;
+                const int64_t rc = s_r[c];
+                if (bA != nullptr) {
+                    const int64_t g = tA + 16 * hA + row;
+                    if (g < rc) Zo[s_zoff[c] + g] = ztF[row][c];
+                }
+                if (bD != nullptr) {
+                    const int64_t g = tD + 16 * hD + row;
+                    if (g > rc && g < n) Zo[s_zoff[c] + g] = ztB[row][c];
+                }
+            }
+            __syncthreads();
+        };
         dual_staged_pass<Stage<R>::ROWD>(
             sstage, nd.rep, n, 0, nA, ntile - 1, nD,
             [&](const double *bA, int64_t tA, const double *bD, int64_t tD) {
-                if (!need) return;
 #pragma unroll 1
-                for (int q = 0; q < RQ_TR / RQ_C; q++) {
-                    const int64_t b0F = tA + q * RQ_C;
-                    const int64_t b0B = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
-                    const bool fF = bA != nullptr && b0F < r;
-                    const bool fB = bD != nullptr && b0B + RQ_C > r && b0B < n;
-                    if (bA != nullptr && b0F <= r) {
-                        A.ck_s[(b0F / RQ_C) * A.S + slot] = div(pF, qF);
-                        A.ck_W[(b0F / RQ_C) * A.S + slot] = W;
-                    }
-                    if (fF && fB) {
+                for (int h = 0; h < 2; h++) {
+                    if (need) {
+#pragma unroll 1
+                        for (int q = 2 * h; q < 2 * h + 2; q++) {
+                            const int64_t b0F = tA + q * RQ_C;
+                            const int64_t b0B = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
+                            const bool fF = bA != nullptr && b0F < r;
+                            const bool fB = bD != nullptr && b0B + RQ_C > r && b0B < n;
+                            if (fF && fB) {
 #pragma unroll
-                        for (int j = 0; j < RQ_C; j++) {
-                            const int64_t kB = b0B + RQ_C - 1 - j;
-                            if (j == RQ_C - 1 && kB >= r)
-                                A.ck_p[(b0B / RQ_C) * A.S + slot] = div(pB, qB);
-                            frow(bA, tA, b0F + j);
-                            brow(bD, tD, kB);
-                        }
-                    } else if (fF) {
+                                for (int j = 0; j < RQ_C; j++) {
+                                    frow(bA, tA, b0F + j);
+                                    brow(bD, tD, b0B + RQ_C - 1 - j);
+                                }
+                            } else if (fF) {
 #pragma unroll
-                        for (int j = 0; j < RQ_C; j++) frow(bA, tA, b0F + j);
-                    } else if (fB) {
+                                for (int j = 0; j < RQ_C; j++) frow(bA, tA, b0F + j);
+                            } else if (fB) {
 #pragma unroll
-                        for (int j = 0; j < RQ_C; j++) {
-                            const int64_t kB = b0B + RQ_C - 1 - j;
-                            if (j == RQ_C - 1 && kB >= r)
-                                A.ck_p[(b0B / RQ_C) * A.S + slot] = div(pB, qB);
-                            brow(bD, tD, kB);
+                                for (int j = 0; j < RQ_C; j++) brow(bD, tD, b0B + RQ_C - 1 - j);
+                            }
+                            if (fF) rescale_pq(pF, qF, EqF);
+                            if (fB) rescale_pq(pB, qB, EqB);
                         }
                     }
-                    if (fF) rescale_pq(pF, qF);
-                    if (fB) rescale_pq(pB, qB);
+                    if (cta_store) flush(bA, tA, h, bD, tD, 1 - h);
                 }
             });
         if (need) {
@@ -473,6 +559,24 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             negc += is_neg(gr) ? 1 : 0;
             nz2 = 1.0 + W + V;
             rows += n;
+            // y_r = qF / PP_r and x_r = QB PP_r: references for the next pass and the
+            // per-column factors (z_i = Z_i 2^refF / y_r, z_k = Z_k 2^refB / x_r)
+            double pm = 1.0, ipm = 1.0;
+            int e = 0;
+            if (nd.pp != nullptr) ppr(r, pm, ipm, e);
+            const double yr = hi(qF) * ipm, xr = hi(qB) * pm;
+            const int eyr = EqF - e, exr = EqB + e;
+            if (wz) {
+                const OutT zo = (OutT)pow2mul(yr, eyr - erefF);
+                zcol[r] = zo;
+                kahan((double)zo, sF, cF_);
+                zinfo.cF = ldexp(1.0, erefF - eyr) / yr;
+                zinfo.cB = ldexp(1.0, erefB - exr) / xr;
+                zinfo.ss = zinfo.cF * zinfo.cF * sF + zinfo.cB * zinfo.cB * sB;
+                zwritten = true;
+            }
+            erefF = eyr + expo_of(yr);
+            erefB = exr + expo_of(xr);
         }
         return negc;
     };
@@ -481,7 +585,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     for (iters = 1; iters <= A.maxit; iters++) {
         const bool need = !done;
         if (!__syncthreads_or(need)) break;
-        int c = twisted_fixed(need);
+        int c = twisted_fixed(need, A.jobz_v && iters >= 2);
         if (need) {
             if (c >= k) {
                 if (lt(lam, b)) b = lam;
@@ -505,10 +609,19 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                 g == 0.0) {
                 lam_out = lam_new;
                 done = true;
+                zfinal = zwritten;  // z of this (converged) factorization is in Z
             } else {
                 if (!(lt(a, lam_new) && lt(lam_new, b))) lam_new = half(add(a, b));
                 lam = lam_new;
             }
+        }
+    }
+    // converged in the first (non-storing) pass: one more pass at the same shift writes z
+    {
+        const bool extra = A.jobz_v && done && !zfinal && zcol != nullptr && n > 1;
+        if (__syncthreads_or(extra)) {
+            twisted_fixed(extra, true);
+            if (extra) zfinal = zwritten;
         }
     }
     // fallback: bisection to relative eps_x sqrt(n) gaptol, then one more solve
@@ -558,23 +671,23 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         return;
     }
 
-    // ---------------- final stage: z from the twisted factorization at lam -----
-    const bool mine = active && col >= 0;
+    // ---------------- fallback only: z by sweeps from the checkpoints of twisted() ------
+    // (the regular path wrote z in product form during its last fixed-twist pass)
+    const bool mine = zcol != nullptr && fb && !zfinal;
+    if (!__syncthreads_or(mine)) {
+        if (zcol != nullptr) A.zc[col0 - A.zcol0] = zinfo;
+        if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
+        return;
+    }
     const double inv = 1.0 / sqrt(nz2);
     double ss_hi = 0.0, ss_lo = 0.0;
     const double tiny = 1e-250;
-    OutT *Zo = reinterpret_cast<OutT *>(A.Z);
-
-    // z from the twisted factorization at lam, two sweeps outward from the twist r,
-    // interleaved (two dependent chains per thread):
+    // two sweeps outward from the twist r, interleaved:
     //   D: rows k <= r, downward, z_r = 1, z_k = -l+_k z_{k+1}
     //      (z_k = -(ld_{k+1}/ld_k) z_{k+2} if z_{k+1} == 0)
     //   U: rows k > r, upward, z_k = -u-_{k-1} z_{k-1}
     //      (z_k = -(ld_{k-2}/ld_{k-1}) z_{k-2} if z_{k-1} == 0)
-    // l+ / u- of each 8-row block are recomputed from the checkpoints of the last
-    // factorization.  Each thread stores its own column directly: successive rows of
-    // a column are contiguous, and the partial sectors merge in L2 before write-back.
-    OutT *zcol = mine ? Zo + nd.row0 + (col - A.zcol0) * A.ldz : nullptr;
+    // l+ / u- of each 8-row block are recomputed from the checkpoints of twisted().
     R z1D = mk<R>(0.0), z2D = mk<R>(0.0), ldn = mk<R>(0.0);        // z_{k+1}, z_{k+2}, ld_{k+1}
     R z1U = mk<R>(0.0), z2U = mk<R>(0.0);                          // z_{k-1}, z_{k-2}
     R ldm1 = mk<R>(0.0), ldm2 = mk<R>(0.0), ucarry = mk<R>(0.0);  // ld_{k-1}, ld_{k-2}, u-_{b0-1}
@@ -698,11 +811,16 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             });
         if (mine) rows += n + 1;
     }
-    if (mine && A.fac) {
-        // exact sum of squares of the written column vs 1 (fp64 output only)
-        double dev = (ss_hi - 1.0) + ss_lo;
-        A.fac[col - A.zcol0] = fabs(dev) > 0x1p-54 ? 1.0 / sqrt(ss_hi + ss_lo) : 0.0;
+    if (zcol != nullptr) {
+        if (mine) {  // written normalised by the estimate; k_zscale renormalises exactly
+            zinfo.cF = 1.0;
+            zinfo.cB = 1.0;
+            zinfo.ss = ss_hi + ss_lo;
+        }
+        A.zc[col0 - A.zcol0] = zinfo;
     }
+    (void)ss_hi;
+    (void)ss_lo;
     if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
 }
 
@@ -837,51 +955,6 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         }
     });
     if (active) A.it.twist[id] = (int32_t)rr;
-}
-
-// rescale the columns whose binary64 norm estimate missed by more than 2^-54
-// (grid-stride over (column, chunk) pairs; a chunk is 256 threads x 4 16-byte
-// vectors, all loads issued before the stores; columns with fac == 0 are already
-// unit vectors and are skipped)
-template <class OutT>
-__global__ void __launch_bounds__(256) k_fixnorm(OutT *Z, int64_t ldz, int64_t ncols,
-                                                 const double *fac, int64_t n) {
-    constexpr int VEC = 16 / sizeof(OutT);  // elements per 16-byte access
-    constexpr int U = 4;
-    constexpr int CHUNK = 256 * U * VEC;
-    const int64_t per_col = (n + CHUNK - 1) / CHUNK;
-    const int64_t total = ncols * per_col;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-        const int64_t c = w / per_col, ch = w - c * per_col;
-        const double f = fac[c];
-        if (f == 0.0) continue;
-        OutT *colp = Z + c * ldz;
-        const int64_t i0 = ch * CHUNK;
-        const bool vec = ((reinterpret_cast<uintptr_t>(colp) & 15) == 0) && i0 + CHUNK <= n;
-        if (vec) {
-            using V = typename std::conditional<sizeof(OutT) == 8, double2, float4>::type;
-            V *v = reinterpret_cast<V *>(colp + i0);
-            V x[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) x[u] = v[threadIdx.x + u * 256];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if constexpr (sizeof(OutT) == 8) {
-                    x[u].x *= f;
-                    x[u].y *= f;
-                } else {
-                    x[u].x = (float)((double)x[u].x * f);
-                    x[u].y = (float)((double)x[u].y * f);
-                    x[u].z = (float)((double)x[u].z * f);
-                    x[u].w = (float)((double)x[u].w * f);
-                }
-                v[threadIdx.x + u * 256] = x[u];
-            }
-        } else {
-            for (int64_t i = i0 + threadIdx.x; i < min(i0 + CHUNK, n); i += 256)
-                colp[i] = (OutT)((double)colp[i] * f);
-        }
-    }
 }
 
 // sort keys (node, twist index) of the singletons for k_rqi's CTA grouping

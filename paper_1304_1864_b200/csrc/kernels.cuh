@@ -22,6 +22,7 @@ struct NodeInfo {
     double sig_hi, sig_lo;  // accumulated shift sigma (scaled units), Alg.1 l.19/29
     int32_t depth;
     int32_t block;
+    const double *pp;   // per row {PP, 1/PP, exponent} of prod_{j<k} (-ld_j) (k_zprod.cuh)
 };
 
 struct Items {  // eigenvalue slots, SoA over the requested index set (+ guards)
@@ -604,6 +605,7 @@ __global__ void k_root_nodes(const BlockDesc *blocks, int nblocks, const double 
     ni.sig_lo = 0.0;
     ni.depth = 0;
     ni.block = b;
+    ni.pp = nullptr;
     nodes[b] = ni;
 }
 

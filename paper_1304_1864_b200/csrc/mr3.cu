@@ -421,6 +421,12 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     k_root_nodes<R><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(dblocks, ctx->nblocks, dmu, rep_pool,
                                                              repx_pool, dnodes);
     CKL("k_root_nodes");
+    {  // prod_{j<k} (-ld_j) per root (product-form eigenvectors, k_zprod.cuh)
+        double *pp = (double *)getbuf(ctx, "pp_root", (size_t)n * PP_STRIDE * 8, &rc);
+        if (rc) return rc;
+        k_node_pp<R><<<ctx->nblocks, 256, 0, s>>>(dnodes, 0, pp, 0, 1);
+        CKL("k_node_pp");
+    }
     ctx->nodes_used = ctx->nblocks;
 
     // index set
@@ -847,11 +853,11 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     int64_t per_thread = nblk * (2 * (int64_t)sizeof(R) + 8);
     int64_t Smax = std::max<int64_t>(RQ_TPB, (int64_t)(budget / std::max<int64_t>(per_thread, 1)));
     Smax = (Smax / RQ_TPB) * RQ_TPB;
-    double *dfac = nullptr;
-    if (jobz == 'V' && sizeof(OutT) == 8 && c1 > c0) {
-        dfac = (double *)getbuf(ctx, "fac", (size_t)(c1 - c0) * 8, &rc);
+    ZCol *dzc = nullptr;  // per local column: factors for k_zscale (written by k_rqi)
+    if (jobz == 'V' && c1 > c0) {
+        dzc = (ZCol *)getbuf(ctx, "zcol_info", (size_t)(c1 - c0) * sizeof(ZCol), &rc);
         if (rc) return rc;
-        CK(cudaMemsetAsync(dfac, 0, (size_t)(c1 - c0) * 8, s));
+        CK(cudaMemsetAsync(dzc, 0, (size_t)(c1 - c0) * sizeof(ZCol), s));
     }
 
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
@@ -930,7 +936,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.ck_s = (R *)ck;
                 A.ck_p = (R *)(ck + nblk * S * sizeof(R));
                 A.ck_W = (double *)(ck + 2 * nblk * S * sizeof(R));
-                A.fac = dfac;
+                A.zc = dzc;
                 A.S = S;
                 A.pivmin = ctx->pivmin;
                 A.krs = P[MR3_KRS];
@@ -1080,6 +1086,13 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 fprintf(stderr, "[mr3] child %d: lane %g growth %.3g delta %.3g tau %.17g\n", c,
                         hd[4 * c], hd[4 * c + 1], hd[4 * c + 2], hd[4 * c + 3]);
         }
+        {
+            double *ppc = (double *)getbuf(ctx, pname + "pp", (size_t)nclus * ctx->n * PP_STRIDE * 8,
+                                           &rc);
+            if (rc) return rc;
+            k_node_pp<R><<<nclus, 256, 0, s>>>(W.nodes, ctx->nodes_used, ppc, ctx->n, 0);
+            CKL("k_node_pp");
+        }
         ctx->nodes_used += nclus;
         dump("after child", nxt, nmem, level + 1);
         // K2: refine in the child coordinates (certified)
@@ -1148,11 +1161,12 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         cudaMemset(ctx->bufs["dbg_iters"].p, 0, cnt * 4);
         cudaMemset(ctx->bufs["dbg_trace"].p, 0, (size_t)cnt * 64);
     }
-    if (dfac) {
-        KTime *tf = kt_begin(ctx, "k_fixnorm");
-        k_fixnorm<OutT><<<ctx->nsm * 16, 256, 0, s>>>(Z, ldz, c1 - c0, dfac, ctx->n);
+    if (dzc) {  // K6 epilogue: per-column factors and exact normalisation (k_zprod.cuh)
+        KTime *tf = kt_begin(ctx, "k_zscale");
+        const int64_t nc = c1 - c0;
+        k_zscale<OutT><<<ctx->nsm * 16, 256, 0, s>>>(Z, ldz, nc, dzc, ctx->n);
         kt_end(ctx, tf);
-        CKL("k_fixnorm");
+        CKL("k_zscale");
     }
     ctx->stats.d_max = level;
     DevStats hst;
