@@ -780,8 +780,22 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         ucarry = ub[RQ_C - 1];
     };
     {
+        // the fallback's full factorization chose its own twists: range of the sweeping threads
+        __syncthreads();
+        if (tid == 0) {
+            s_rmin = (int)n;
+            s_rmax = 0;
+        }
+        __syncthreads();
+        if (mine) {
+            atomicMin(&s_rmin, (int)r);
+            atomicMax(&s_rmax, (int)r);
+        }
+        __syncthreads();
+        const int fr_min = s_rmin <= s_rmax ? s_rmin : 0;
+        const int fr_max = s_rmin <= s_rmax ? s_rmax : (int)n - 1;
         const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
-        const int tmin = cta_rmin / RQ_TR, tmax = cta_rmax / RQ_TR;
+        const int tmin = fr_min / RQ_TR, tmax = fr_max / RQ_TR;
         // U: ascending from the tile of the smallest twist; D: descending from the largest
         dual_staged_pass<Stage<R>::ROWD>(
             sstage, nd.rep, n, tmin, ntile - tmin, tmax, tmax + 1,
@@ -813,6 +827,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     }
     if (zcol != nullptr) {
         if (mine) {  // written normalised by the estimate; k_zscale renormalises exactly
+            zinfo.r = (int32_t)r;
             zinfo.cF = 1.0;
             zinfo.cB = 1.0;
             zinfo.ss = ss_hi + ss_lo;

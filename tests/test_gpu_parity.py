@@ -350,3 +350,33 @@ def test_root_certification_modes_agree(make):
     assert s1["bisect_rows"] > s0["bisect_rows"]
     np.testing.assert_array_equal(w1.cpu().numpy(), w0.cpu().numpy())
     np.testing.assert_array_equal(Z1.cpu().numpy(), Z0.cpu().numpy())
+
+
+def _with_params(params, fn):
+    try:
+        for k, v in params.items():
+            mr3.set_param(k, v)
+        return fn()
+    finally:
+        for k in params:
+            mr3.set_param(k, -1)
+
+
+@pytest.mark.parametrize("params", [
+    {"MAX_RQI": 1},            # every singleton takes the bisection fallback + sweep-form z
+    {"REFINE": 1e12},          # all starts refined: many converge in the first (non-storing)
+                               # pass, whose z then comes from an extra storing pass
+    {"NEWTON": 1},             # almost every item through the many-lane multisection tail
+    {"XPTS": 1},               # plain bisection in the binary_x phase
+    {"XPTS": 2},               # two points per lane
+    {"GRID": 0},               # no shared grid start
+    {"REFINE": 0},             # midpoints as RQI starts
+])
+def test_rare_paths_parity(params):
+    """The paths the default workload rarely takes, forced by parameters, against the oracle."""
+    for p in (synth.random_uniform(700, 4), synth.glued_wilkinson(4, 21), synth.legendre(1500)):
+        w, Z, st = _with_params(params, lambda: run(p))
+        res = check_solution(p, w, Z, np.arange(1, p.n + 1))
+        assert_parity(res)
+        if params.get("MAX_RQI") == 1 and not p.name.startswith("glued"):
+            assert st["rqi_fallbacks"] > 0
