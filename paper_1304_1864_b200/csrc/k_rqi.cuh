@@ -108,15 +108,28 @@ struct StageG {
 template <class R>
 struct Stage : StageG<4 * Prec<R>::words> {};
 
-// rows [t0 - HALO, t0 + TR) of rep (clamped to [0, n)) -> buf, asynchronously
+// rows [t0 - HALO, t0 + TR) of rep (clamped to [0, n)) -> buf, asynchronously; with
+// pp != nullptr also the same rows of the node's PP array (4 doubles per row) -> buf + TILE
+constexpr int PP_TILE = (RQ_TR + RQ_HALO) * 4;  // doubles of a staged PP tile
 template <int ROWD>
-__device__ __forceinline__ void stage_tile_g(double *buf, const double *rep, int64_t n, int64_t t0) {
+__device__ __forceinline__ void stage_tile_g(double *buf, const double *rep, int64_t n, int64_t t0,
+                                             const double *pp = nullptr) {
     constexpr int CH = StageG<ROWD>::ROWS * ROWD / 2;  // 16-byte chunks
     for (int c = threadIdx.x; c < CH; c += RQ_TPB) {
         int r = c / (ROWD / 2), off = (c % (ROWD / 2)) * 2;
         int64_t g = t0 - RQ_HALO + r;
         g = g < 0 ? 0 : (g >= n ? n - 1 : g);
         cp_async16(buf + r * ROWD + off, rep + g * ROWD + off);
+    }
+    if (pp != nullptr) {
+        constexpr int CP = (RQ_TR + RQ_HALO) * 2;
+        double *pb = buf + StageG<ROWD>::TILE;
+        for (int c = threadIdx.x; c < CP; c += RQ_TPB) {
+            int r = c >> 1, off = (c & 1) * 2;
+            int64_t g = t0 - RQ_HALO + r;
+            g = g < 0 ? 0 : (g >= n ? n - 1 : g);
+            cp_async16(pb + r * 4 + off, pp + g * 4 + off);
+        }
     }
     cp_async_commit();
 }
@@ -182,18 +195,21 @@ __device__ __forceinline__ Row4<double> srow<double>(const double *buf, int64_t 
 // gives every thread two dependent chains at once.  smem: 4 tile buffers.  Collective.
 template <int ROWD, class Body>
 __device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep, int64_t n, int a0,
-                                                 int nA, int d0, int nD, Body body) {
-    constexpr int TILE = StageG<ROWD>::TILE;
+                                                 int nA, int d0, int nD, Body body,
+                                                 const double *pp = nullptr) {
+    constexpr int TILE = StageG<ROWD>::TILE + PP_TILE;  // buffer stride (PP rows after the rows)
     const int steps = nA > nD ? nA : nD;
     auto bufA = [&](int b) -> double * { return smem + (b ? TILE : 0); };
     auto bufD = [&](int b) -> double * { return smem + (b ? 3 * TILE : 2 * TILE); };
     if (steps <= 0) return;
-    if (nA > 0) stage_tile_g<ROWD>(bufA(0), rep, n, (int64_t)a0 * RQ_TR);
-    if (nD > 0) stage_tile_g<ROWD>(bufD(0), rep, n, (int64_t)d0 * RQ_TR);
+    if (nA > 0) stage_tile_g<ROWD>(bufA(0), rep, n, (int64_t)a0 * RQ_TR, pp);
+    if (nD > 0) stage_tile_g<ROWD>(bufD(0), rep, n, (int64_t)d0 * RQ_TR, pp);
     for (int i = 0; i < steps; i++) {
         if (i + 1 < steps) {
-            if (i + 1 < nA) stage_tile_g<ROWD>(bufA((i + 1) & 1), rep, n, (int64_t)(a0 + i + 1) * RQ_TR);
-            if (i + 1 < nD) stage_tile_g<ROWD>(bufD((i + 1) & 1), rep, n, (int64_t)(d0 - i - 1) * RQ_TR);
+            if (i + 1 < nA)
+                stage_tile_g<ROWD>(bufA((i + 1) & 1), rep, n, (int64_t)(a0 + i + 1) * RQ_TR, pp);
+            if (i + 1 < nD)
+                stage_tile_g<ROWD>(bufD((i + 1) & 1), rep, n, (int64_t)(d0 - i - 1) * RQ_TR, pp);
             // stage_tile_g commits one group per call: wait until the current step's
             // groups are complete (at most the just-issued ones pending)
             if (i + 1 < nA && i + 1 < nD)
@@ -210,14 +226,28 @@ __device__ __forceinline__ void dual_staged_pass(double *smem, const double *rep
     }
 }
 
+// dynamic shared memory of k_rqi: 4 staged tiles (rows + PP rows), the two z tiles of a
+// storing pass, per-thread column data
+template <class R, class OutT>
+constexpr size_t rqi_smem_bytes() {
+    return 4 * (size_t)(Stage<R>::TILE + PP_TILE) * sizeof(double) +
+           2 * 16 * (size_t)(RQ_TPB + 1) * sizeof(OutT) + 2 * RQ_TPB * sizeof(int64_t) +
+           RQ_TPB * sizeof(int) + 4 * sizeof(int);
+}
+
 // ---------------------------------------------------------------- kernel
 template <class R, class OutT>
 __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
-    __shared__ __align__(16) double sstage[4 * Stage<R>::TILE];  // 4 tiles: dual_staged_pass
-    __shared__ int s_rmin, s_rmax;
-    __shared__ OutT ztF[16][RQ_TPB + 1], ztB[16][RQ_TPB + 1];  // z tiles of a storing pass
-    __shared__ int64_t s_r[RQ_TPB], s_zoff[RQ_TPB];
-    __shared__ int s_wz[RQ_TPB];
+    extern __shared__ __align__(16) double rq_dyn[];  // rqi_smem_bytes<R, OutT>()
+    double *sstage = rq_dyn;                           // 4 tiles: dual_staged_pass
+    OutT(*ztF)[RQ_TPB + 1] = reinterpret_cast<OutT(*)[RQ_TPB + 1]>(
+        rq_dyn + 4 * (Stage<R>::TILE + PP_TILE));      // z tiles of a storing pass
+    OutT(*ztB)[RQ_TPB + 1] = ztF + 16;
+    int64_t *s_r = reinterpret_cast<int64_t *>(ztB + 16);
+    int64_t *s_zoff = s_r + RQ_TPB;
+    int *s_wz = reinterpret_cast<int *>(s_zoff + RQ_TPB);
+    int &s_rmin = s_wz[RQ_TPB];
+    int &s_rmax = s_wz[RQ_TPB + 1];
 
     const int tid = threadIdx.x;
     const RqiTask task = A.tasks[blockIdx.x];
@@ -438,6 +468,16 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             ipm = a0.y;
             e = (int)a1.x;
         };
+        // the PP row of kk from the staged tile (rows follow the representation rows)
+        auto sppr = [&](const double *buf, int64_t t0, int64_t kk, double &pm, double &ipm,
+                        int &e) {
+            const double2 *q = reinterpret_cast<const double2 *>(
+                buf + Stage<R>::TILE + (kk - t0 + RQ_HALO) * 4);
+            const double2 a0 = q[0], a1 = q[1];
+            pm = a0.x;
+            ipm = a0.y;
+            e = (int)a1.x;
+        };
         // value * 2^k (k <= 1023; results below the normal range flush to zero)
         auto pow2mul = [](double v, int k) -> double {
             return k < -1022 ? 0.0 : v * __hiloint2double((k + 1023) << 20, 0);
@@ -462,7 +502,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                 if (wz) {
                     double pm, ipm;
                     int e;
-                    ppr(kk, pm, ipm, e);
+                    sppr(bA, tA, kk, pm, ipm, e);
                     const OutT zo = (OutT)pow2mul(hi(qF) * ipm, EqF - e - erefF);
                     ztF[(kk - tA) & 15][tid] = zo;
                     kahan((double)zo, sF, cF_);
@@ -484,7 +524,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                 if (wz) {
                     double pm, ipm;
                     int e;
-                    ppr(kk, pm, ipm, e);
+                    sppr(bD, tD, kk, pm, ipm, e);
                     const OutT zo = (OutT)pow2mul(hi(qB) * pm, EqB + e - erefB);
                     ztB[(kk - tD) & 15][tid] = zo;
                     kahan((double)zo, sB, cB_);
@@ -553,7 +593,8 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                     }
                     if (cta_store) flush(bA, tA, h, bD, tD, 1 - h);
                 }
-            });
+            },
+            cta_store ? nd.pp : nullptr);
         if (need) {
             gr = add(add(div(pF, qF), div(pB, qB)), lam);
             negc += is_neg(gr) ? 1 : 0;

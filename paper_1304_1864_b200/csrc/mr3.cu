@@ -961,7 +961,12 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 if (locate)
                     k_rqi_locate<R><<<nb, rtpb, 0, s>>>(A);
                 else
-                    k_rqi<R, OutT><<<nb, rtpb, 0, s>>>(A);
+                {
+                    constexpr size_t smem = rqi_smem_bytes<R, OutT>();
+                    cudaFuncSetAttribute(k_rqi<R, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+                    k_rqi<R, OutT><<<nb, rtpb, smem, s>>>(A);
+                }
                 kt_end(ctx, t);
                 cudaError_t e2 = cudaGetLastError();
                 if (e2 != cudaSuccess) {
