@@ -61,6 +61,7 @@ struct RqiArgs {
     ZCol *zc;              // per local column: rows, twist and factors for k_zscale
     int64_t S;             // checkpoint stride (CTAs in this launch * RQ_TPB)
     double pivmin, krs, eps_x, gaptol;
+    double twist_w;     // twist weight slope: |gamma_k| (1 + twist_w |2k - n| / n) is minimised
     double root_widen;  // > 0: root-node brackets are binary_x brackets; the guard is widened
                         // by root_widen * n * |lambda| (relative robustness of the root, R8d)
     int maxit;
@@ -963,7 +964,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         }
     });
     double pb = 0.0, qb = 1.0, best = INFINITY;
-    const double wfac = 3.0 / (double)n;
+    const double wfac = A.twist_w / (double)n;
     int64_t rr = n - 1;
     if (active) pb = __ldg(nd.repx + 2 * (n - 1)) - lam;
     staged_pass_g<2>(sx, nd.repx, n, true, [&](const double *buf, int64_t t0) {

@@ -85,9 +85,9 @@ struct mr3_ctx_s {
 // ------------------------------------------------------------------ helpers
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 3.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 3.0},
 };
 
 #define CK(call)                                                                  \
@@ -943,6 +943,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.eps_x = eps_x;
                 A.gaptol = gaptol;
                 A.root_widen = ctx->root_widen;
+                A.twist_w = P[MR3_TWISTW];
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
                 A.w = w;
