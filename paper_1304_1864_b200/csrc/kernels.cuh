@@ -47,6 +47,8 @@ struct RqiTask {
 struct DevStats {
     unsigned long long bisect_rows;    // binary_y Sturm rows
     unsigned long long bisect_rows_x;  // binary_x Sturm rows (fp64 phase)
+    unsigned long long newton_rows_x;  // binary_x rows of Newton passes (subset of bisect_rows_x)
+    // ---- fields above are plan-phase counters; execute resets from rqi_rows on
     unsigned long long rqi_rows;
     int rqi_fallbacks;
     int rqi_iters_max;
@@ -55,7 +57,6 @@ struct DevStats {
     int n_clusters;
     int pad;
     unsigned long long refine_rows_x;  // binary_x rows of the RQI start refinement (K2')
-    unsigned long long newton_rows_x;  // binary_x rows of Newton passes (subset of bisect_rows_x)
 };
 
 template <class R>
@@ -529,14 +530,62 @@ __global__ void k_root_chunkmat(const T *__restrict__ d, const T *__restrict__ e
     mats[k] = M;
 }
 
-// one thread per block: incoming state of every chunk, (p, q) = (1, 0) at the top
+// incoming state of every chunk ((p, q) = (1, 0) at the top of the block): one CTA per
+// block; each thread composes the transfer matrices of a run of chunks, a Hillis-Steele
+// scan composes the runs (matrix products are associative; later chunks multiply from
+// the left), and each thread then walks its run from the composed incoming state.
+// Every product is rescaled by a power of two (the state is projective).
 template <class R>
-__global__ void k_root_scan(const int *blk_chunk0, int nblocks, const Mat2<R> *mats,
-                            R *states) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nblocks) return;
+__device__ __forceinline__ Mat2<R> mat_mul(const Mat2<R> &X, const Mat2<R> &Y) {  // X * Y
+    Mat2<R> Z;
+    Z.a = add(mul(X.a, Y.a), mul(X.b, Y.c));
+    Z.b = add(mul(X.a, Y.b), mul(X.b, Y.d));
+    Z.c = add(mul(X.c, Y.a), mul(X.d, Y.c));
+    Z.d = add(mul(X.c, Y.b), mul(X.d, Y.d));
+    double mx = fmax(fmax(fabs(hi(Z.a)), fabs(hi(Z.b))), fmax(fabs(hi(Z.c)), fabs(hi(Z.d))));
+    int ex = 0;
+    if (mx > 0) frexp(mx, &ex);
+    Z.a = scale2(Z.a, -ex);
+    Z.b = scale2(Z.b, -ex);
+    Z.c = scale2(Z.c, -ex);
+    Z.d = scale2(Z.d, -ex);
+    return Z;
+}
+constexpr int RS_TPB = 128;
+template <class R>
+__global__ void __launch_bounds__(RS_TPB) k_root_scan(const int *blk_chunk0, int nblocks,
+                                                      const Mat2<R> *mats, R *states) {
+    const int b = blockIdx.x;
+    const int c0 = blk_chunk0[b], c1 = blk_chunk0[b + 1];
+    const int nc = c1 - c0;
+    const int per = (nc + RS_TPB - 1) / RS_TPB;
+    const int r0 = c0 + threadIdx.x * per, r1 = min(r0 + per, c1);
+    Mat2<R> L;  // composed transfer matrix of this thread's run (identity if empty)
+    L.a = mk<R>(1.0);
+    L.b = mk<R>(0.0);
+    L.c = mk<R>(0.0);
+    L.d = mk<R>(1.0);
+    for (int k = r0; k < r1; k++) L = mat_mul<R>(mats[k], L);
+    __shared__ Mat2<R> sm[RS_TPB];
+    sm[threadIdx.x] = L;
+    __syncthreads();
+    for (int off = 1; off < RS_TPB; off <<= 1) {  // inclusive scan: S_t = L_t ... L_0
+        Mat2<R> v = sm[threadIdx.x];
+        const bool take = (int)threadIdx.x >= off;
+        Mat2<R> u;
+        if (take) u = sm[threadIdx.x - off];
+        __syncthreads();
+        if (take) sm[threadIdx.x] = mat_mul<R>(v, u);
+        __syncthreads();
+    }
+    // incoming state of the run: S_{t-1} (1, 0)
     R p = mk<R>(1.0), q = mk<R>(0.0);
-    for (int k = blk_chunk0[b]; k < blk_chunk0[b + 1]; k++) {
+    if (threadIdx.x > 0) {
+        const Mat2<R> E = sm[threadIdx.x - 1];
+        p = E.a;
+        q = E.c;
+    }
+    for (int k = r0; k < r1; k++) {
         states[2 * k] = p;
         states[2 * k + 1] = q;
         const Mat2<R> M = mats[k];
@@ -548,6 +597,7 @@ __global__ void k_root_scan(const int *blk_chunk0, int nblocks, const Mat2<R> *m
         p = scale2(np, -ex);
         q = scale2(nq, -ex);
     }
+    (void)nblocks;
 }
 
 template <class R, class T>

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -47,6 +48,8 @@ struct Cfg {  // per-mode parameters
 }  // namespace
 
 struct mr3_ctx_s {
+    double t_last = 0.0;  // host wall time of the last synchronisation point (MR3_DEBUG & 2)
+    int dump = 0;         // MR3_DEBUG & 1: items to dump
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -83,6 +86,14 @@ struct mr3_ctx_s {
 };
 
 // ------------------------------------------------------------------ helpers
+#include <chrono>
+static double host_now_ms();
+static void hsync_note(mr3_ctx ctx, const char *where) {
+    if (!(ctx->debug & 2)) return;
+    const double t = host_now_ms();
+    fprintf(stderr, "[mr3] %s: %.3f ms since last sync point\n", where, t - ctx->t_last);
+    ctx->t_last = t;
+}
 
 static const double kDefaults[2][MR3_NPARAM] = {
     // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW
@@ -109,6 +120,15 @@ static const double kDefaults[2][MR3_NPARAM] = {
         ctx->launches++;                                                                  \
     } while (0)
 
+// MR3_DEBUG & 2: wall time between host synchronisation points (finds device idle gaps)
+#include <chrono>
+static double host_now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+static void hsync_note(mr3_ctx ctx, const char *where);
+
 static void *getbuf(mr3_ctx ctx, const std::string &name, size_t bytes, int *rc) {
     Buf &b = ctx->bufs[name];
     if (bytes == 0) bytes = 16;
@@ -120,6 +140,7 @@ static void *getbuf(mr3_ctx ctx, const std::string &name, size_t bytes, int *rc)
             b.cap = 0;
         }
         size_t want = bytes + bytes / 8;
+        if (ctx->debug & 2) fprintf(stderr, "[mr3] cudaMalloc %s %zu\n", name.c_str(), want);
         cudaError_t e = cudaMalloc(&b.p, want);
         if (e != cudaSuccess) {
             e = cudaMalloc(&b.p, bytes);
@@ -155,6 +176,12 @@ static void kt_collect(mr3_ctx ctx) {
     for (size_t i = 0; i < ctx->kt_used; i++) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->kt[i].a, ctx->kt[i].b);
+        if (ctx->debug & 4) {  // device timeline of the timed regions (finds idle gaps)
+            float st = 0.f;
+            cudaEventElapsedTime(&st, ctx->kt[0].a, ctx->kt[i].a);
+            fprintf(stderr, "[mr3] timeline %-14s start %9.3f ms  dur %8.3f ms\n", ctx->kt[i].name,
+                    st, ms);
+        }
         std::string nm = ctx->kt[i].name;
         bool found = false;
         for (auto &p : ctx->ktimes)
@@ -311,7 +338,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     CKL("k_scan_input");
     ScanInfo info;
     CK(cudaMemcpyAsync(&info, dscan, sizeof(info), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#1");
     if (info.nonfinite) return MR3_ERR_NONFINITE;
     ctx->norm1 = info.norm1;
     int ex = 0;
@@ -331,7 +358,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     }
     unsigned long long nsplit = 0;
     CK(cudaMemcpyAsync(&nsplit, dcnt, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#2");
     if (nsplit == 0) {
         blocks.push_back({0, n});
     } else {
@@ -343,7 +370,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_split_list");
         std::vector<int64_t> pos(nsplit);
         CK(cudaMemcpyAsync(pos.data(), dpos, nsplit * 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#3");
         std::sort(pos.begin(), pos.end());
         int64_t r0 = 0;
         for (int64_t p : pos) {
@@ -403,7 +430,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         k_root_chunkmat<R, T><<<(nch + 127) / 128, 128, 0, s>>>(d, e, dchunks, nch, dblocks,
                                                                  ctx->scale, dmu, dmats);
         CKL("k_root_chunkmat");
-        k_root_scan<R><<<(ctx->nblocks + 63) / 64, 64, 0, s>>>(dbc0, ctx->nblocks, dmats, dstates);
+        k_root_scan<R><<<ctx->nblocks, RS_TPB, 0, s>>>(dbc0, ctx->nblocks, dmats, dstates);
         CKL("k_root_scan");
         k_root_factor<R, T><<<(nch + 127) / 128, 128, 0, s>>>(d, e, dchunks, nch, dblocks,
                                                                ctx->scale, dmu, dstates, right, xi,
@@ -411,7 +438,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_root_factor");
         int hfail = 0;
         CK(cudaMemcpyAsync(&hfail, dfail, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#4");
         if (!hfail) break;
         if (attempt == 11) {
             ctx->err = "root representation: no definite shift found";
@@ -443,7 +470,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_count_at");
         int hc[2];
         CK(cudaMemcpyAsync(hc, dc, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#5");
         ilw = hc[0] + 1;
         iuw = hc[1];
     }
@@ -600,7 +627,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             CKL("select (tail)");
             int ht = 0;
             CK(cudaMemcpyAsync(&ht, tc, 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#6");
             if (ht > 0) {
                 int G = choose_groups(ctx, ht, 0);
                 if (G < 8) G = 8;
@@ -613,7 +640,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                                                                     dbrk + 4 * first);
         CKL("k_items_to_brk");
     }
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#7");
     *m = ctx->m;
     *brk = dbrk;
     *slice_cap = cap;
@@ -659,7 +686,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.st = (DevStats *)ctx->bufs["devstats"].p;
     double *dbrk = (double *)ctx->bufs["brk"].p;
     // per-execute counters (bisect_rows of the plan is kept)
-    CK(cudaMemsetAsync((char *)W.st + 16, 0, sizeof(DevStats) - 16, s));
+    CK(cudaMemsetAsync((char *)W.st + offsetof(DevStats, rqi_rows), 0,
+                       sizeof(DevStats) - offsetof(DevStats, rqi_rows), s));
     if (ctx->world > 1) {
         k_brk_to_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(W.it, cnt, (int)ctx->slice_cap,
                                                             ctx->world, dbrk);
@@ -694,14 +722,14 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         CKL("k_assign_cols");
         int64_t hm = 0;
         CK(cudaMemcpyAsync(&hm, mc, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#8");
         ctx->m = hm;
         int64_t first_rank = md == 1 ? ctx->il : 1;
         if (md == 2) {
             // first wanted rank = 1 + #items at or below vl: ranks are contiguous
             std::vector<int64_t> cols(cnt);
             CK(cudaMemcpyAsync(cols.data(), W.it.col, cnt * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#9");
             int64_t mn = INT64_MAX;
             for (auto c : cols)
                 if (c >= 0) mn = std::min(mn, c);
@@ -744,9 +772,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     CKL("k_classify");
     int hc[4];
     CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#10");
     int nsing = hc[0], nclus = hc[1], nmem = hc[2];
-    if (ctx->debug && P[MR3_XPTS] == 3) {  // passes per item of the Newton x-phase
+    if (ctx->dump && P[MR3_XPTS] == 3) {  // passes per item of the Newton x-phase
         std::vector<double> ps(cnt);
         cudaMemcpy(ps.data(), W.it.x0, cnt * 8, cudaMemcpyDeviceToHost);
         int hist[41] = {0};
@@ -767,7 +795,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             if (chist[i]) fprintf(stderr, " %d:%d", i, chist[i]);
         fprintf(stderr, "\n");
     }
-    if (ctx->debug) fprintf(stderr, "[mr3] level 0: %d singles %d clusters %d members\n", nsing, nclus, nmem);
+    if (ctx->dump) fprintf(stderr, "[mr3] level 0: %d singles %d clusters %d members\n", nsing, nclus, nmem);
 
     // multi-rank: cluster-whole partition of the output columns
     int64_t c0 = 0, c1 = m;
@@ -781,7 +809,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             CK(cudaMemcpyAsync(hm.data(), listB, nmem * 4, cudaMemcpyDeviceToHost, s));
         }
         CK(cudaMemcpyAsync(cols.data(), W.it.col, cnt * 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#11");
         // segments: (first column, cost, kind, index)
         struct Seg {
             int64_t c0;
@@ -835,7 +863,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             CK(cudaMemcpyAsync(cend, ne.data(), nclus * 4, cudaMemcpyHostToDevice, s));
             CK(cudaMemcpyAsync(listB, nm.data(), nmem * 4, cudaMemcpyHostToDevice, s));
         }
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#12");
     }
     *zcol_begin = c0;
     *zcol_end = c1;
@@ -880,7 +908,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             CKL("select (refine)");
             int hr = 0;
             CK(cudaMemcpyAsync(&hr, rcnt, 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#13");
             if (hr > 0) {
                 // many lanes per item: few items, short dependent chains (log2(G+1) bits/round)
                 int G = choose_groups(ctx, hr, 0);
@@ -954,7 +982,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.st = W.st;
                 A.dbg_iters = nullptr;
                 A.dbg_trace = nullptr;
-                if (ctx->debug) {
+                if (ctx->dump) {
                     A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
                     A.dbg_trace = (double *)getbuf(ctx, "dbg_trace", (size_t)cnt * 64, &rc3);
                 }
@@ -1003,7 +1031,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     };
 
     auto dump = [&](const char *tag, const int32_t *list, int cntl, int lvl) {
-        if (!ctx->debug) return;
+        if (!ctx->dump) return;
         cudaStreamSynchronize(ctx->stream);
         std::vector<int32_t> ids(cntl);
         std::vector<R> lo(cnt), hi(cnt);
@@ -1019,7 +1047,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         std::vector<NodeInfo> nds(ctx->nodes_used);
         cudaMemcpy(nds.data(), W.nodes, ctx->nodes_used * sizeof(NodeInfo), cudaMemcpyDeviceToHost);
         fprintf(stderr, "[mr3] level %d %s: %d items\n", lvl, tag, cntl);
-        for (int i = 0; i < cntl && i < ctx->debug; i++) {
+        for (int i = 0; i < cntl && i < ctx->dump; i++) {
             int id = ids[i];
             const NodeInfo &nd = nds[nodev[id]];
             fprintf(stderr, "  id %d k %d node %d depth %d sig %.17g lo %.17g%+.3g hi %.17g%+.3g w %.3g lg %.3g rg %.3g\n",
@@ -1062,7 +1090,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             CK(cudaMalloc(&nn, newcap * sizeof(NodeInfo)));
             CK(cudaMemcpyAsync(nn, W.nodes, ctx->nodes_used * sizeof(NodeInfo),
                                cudaMemcpyDeviceToDevice, s));
-            CK(cudaStreamSynchronize(s));
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#14");
             cudaFree(ctx->bufs["nodes"].p);
             ctx->bufs["nodes"].p = nn;
             ctx->bufs["nodes"].cap = newcap * sizeof(NodeInfo);
@@ -1077,18 +1105,18 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if (rc) return rc;
         CK(cudaMemsetAsync(poolx + 2 * (size_t)nclus * ctx->n, 0, XPAD * 16, s));
         double *cdbg = nullptr;
-        if (ctx->debug) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
+        if (ctx->dump) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
         k_child<R><<<nclus, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, nxt, cbeg, cend, nclus,
                                         pool, poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin,
                                         W.st, cdbg);
         kt_end(ctx, tch);
         CKL("k_child");
-        if (ctx->debug) {
+        if (ctx->dump) {
             std::vector<double> hd(4 * nclus);
             cudaStreamSynchronize(s);
             cudaMemcpy(hd.data(), cdbg, nclus * 32, cudaMemcpyDeviceToHost);
-            for (int c = 0; c < nclus && c < ctx->debug; c++)
+            for (int c = 0; c < nclus && c < ctx->dump; c++)
                 fprintf(stderr, "[mr3] child %d: lane %g growth %.3g delta %.3g tau %.17g\n", c,
                         hd[4 * c], hd[4 * c + 1], hd[4 * c + 2], hd[4 * c + 3]);
         }
@@ -1114,16 +1142,16 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         kt_end(ctx, tc2);
         CKL("k_classify");
         CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#15");
         nsing = hc[0];
         nclus = hc[1];
         nmem = hc[2];
         level++;
-        if (ctx->debug)
+        if (ctx->dump)
             fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
                     nclus, nmem);
     }
-    if (ctx->debug && ctx->bufs.count("rqi_sorted") && ctx->n > 1) {
+    if (ctx->dump && ctx->bufs.count("rqi_sorted") && ctx->n > 1) {
         // twist-index distribution (r / n in 10 bins) and spread per 128-run of the sorted list
         cudaStreamSynchronize(s);
         std::vector<int32_t> tw(cnt), nodev(cnt);
@@ -1134,7 +1162,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         for (int i = 0; i < 10; i++) fprintf(stderr, " %d", hist[i]);
         fprintf(stderr, "\n");
     }
-    if (ctx->debug && ctx->bufs.count("dbg_iters")) {
+    if (ctx->dump && ctx->bufs.count("dbg_iters")) {
         cudaStreamSynchronize(s);
         std::vector<int32_t> itv(cnt);
         std::vector<double> lg(cnt), rg(cnt);
@@ -1177,7 +1205,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     ctx->stats.d_max = level;
     DevStats hst;
     CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#16");
     kt_collect(ctx);
     ctx->stats.n_clusters = hst.n_clusters;
     ctx->stats.largest_cluster = std::max(1, hst.largest_cluster);
@@ -1227,6 +1255,8 @@ int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     const char *dbg = getenv("MR3_DEBUG");
     ctx->debug = dbg ? atoi(dbg) : 0;
+    // MR3_DEBUG bits: 1 = dumps and histograms, 2 = host sync points, 4 = device timeline
+    ctx->dump = (ctx->debug & 1) ? (ctx->debug > 8 ? ctx->debug : 40) : 0;
     *out = ctx;
     return 0;
 }
@@ -1357,7 +1387,7 @@ static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64
             CK(cudaMemcpy2DAsync(Z, (size_t)ldz * es, dZ, (size_t)n * es, (size_t)n * es, (size_t)mm,
                                  cudaMemcpyDeviceToHost, s));
     }
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#17");
     return 0;
 }
 
