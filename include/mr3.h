@@ -47,6 +47,8 @@ typedef struct mr3_ctx_s *mr3_ctx;
 #define MR3_ERR_ZCAP 6      /* two-phase form: Z has fewer columns than needed */
 #define MR3_ERR_STATE 7     /* two-phase form: execute without a matching plan */
 
+#define MR3_BRK_REC 6 /* doubles per bracket record of the two-phase form (mr3_plan) */
+
 /*
  * Statistics of one solve (PAPER.md L425 d_max, L961 rho).
  * t_ms: device time per phase {root, bisect, classify, child, rqi, total, -, -}.
@@ -142,8 +144,9 @@ int mr3_sstemr_d_host(mr3_ctx ctx, char jobz, char range, int64_t n, const float
  *
  * mr3_plan: root representation (replicated), the requested index set, and
  * bisection of this rank's static slice of it.  Returns in *brk a DEVICE buffer
- * of world * slice_cap records of 4 doubles (bracket lo.hi, lo.lo, hi.hi, hi.lo
- * in root coordinates) of which this rank filled records
+ * of world * slice_cap records of MR3_BRK_REC doubles (bracket lo.hi, lo.lo, hi.hi,
+ * hi.lo in root coordinates, then the binary_x Newton estimate of the eigenvalue and
+ * the size of its last step, NaN / INF if none) of which this rank filled records
  * [rank*slice_cap, rank*slice_cap + slice_cnt); the caller must all-gather it in
  * place (equal-size slices, e.g. ncclAllGather / torch.distributed) before
  * mr3_execute.  The buffer stays owned by the context.

@@ -251,10 +251,13 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
                                            bool active, int k, double rtol, double absfloor,
                                            double tolmul, double pivmin,
                                            unsigned long long &rows, int64_t n, int &passes,
-                                           int maxpass, bool &converged) {
+                                           int maxpass, bool &converged, double &est_last,
+                                           double &step_last) {
     bool mdone = !active;
     passes = 0;
     converged = false;
+    est_last = NAN;        // Newton estimate x - f/f' of the last pass (the RQI start, R10)
+    step_last = INFINITY;  // |f/f'| of that pass
     double xn = NAN;
     double r1 = INFINITY, r2 = INFINITY;  // |Newton step| of the last two Newton passes
     int nnewton = 0;
@@ -294,8 +297,12 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
             else
                 a = x;
             xn = NAN;
+            est_last = NAN;
+            step_last = INFINITY;
             if (fabs(ratio) < INFINITY) {
                 const double est = x - ratio;
+                est_last = est;
+                step_last = fabs(ratio);
                 if (took_newton || nnewton == 0) {
                     nnewton++;
                     r2 = r1;
@@ -605,7 +612,7 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
                                                   double absfloor, double pivmin, double pivmin_x,
                                                   double eps_x, int certify, int xpts,
                                                   int ycert, char *tailflag, int xpts_maxpass,
-                                                  DevStats *st) {
+                                                  double widen, DevStats *st) {
     __shared__ __align__(16) double sbuf[2 * BS_TILE];
     if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
     const RqiTask task = tasks[blockIdx.x];
@@ -652,7 +659,15 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
 
     if (XPHASE && certify == 2) {
         // K2' (RQI starting points): binary_x multisection on M_x to relative rtol
-        // (a few ulps) from the certified bracket; x0 = midpoint if strictly inside it
+        // (a few ulps) from the certified bracket; x0 = midpoint if strictly inside it.
+        // Root brackets of the uncertified binary_x phase (R8d) are first widened as k_rqi
+        // widens its guard (widen = root_widen): the binary_x eigenvalue seen by count_x may
+        // lie just outside a bracket that count_xn (Newton) produced
+        if (widen > 0.0 && nd.depth == 0 && active) {
+            const double wd = widen * (double)n * fmax(fabs(hi(a)), fabs(hi(b)));
+            a = sub(a, mk<R>(wd));
+            b = add(b, mk<R>(wd));
+        }
         double ax = hi(a), bx = hi(b);
         msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 1.0, rows_x, n,
                              [&](bool need, double x) {
@@ -671,10 +686,14 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
         if (G == 1 && xpts == 3) {
             int passes = 0;
             bool conv = true;
+            double est = NAN, step = INFINITY;
             newton_cta(sbuf, nd, ax, bx, active, k, rtol, absfloor, 0.5, pivmin_x, rows_x, n, passes,
-                       tailflag ? xpts_maxpass : 4000, conv);
+                       tailflag ? xpts_maxpass : 4000, conv, est, step);
             if (passes) atomicAdd(&st->newton_rows_x, (unsigned long long)passes * n);
-            if (active) it.x0[id] = (double)passes;  // diagnostics (MR3_DEBUG); reset before RQI
+            if (active) {  // the last Newton estimate: RQI start unless k_refine_flags rejects it
+                it.x0[id] = conv ? est : NAN;
+                it.dx[id] = conv ? step : INFINITY;
+            }
             if (tailflag && active) tailflag[local + task.first] = conv ? 0 : 1;
             if (tailflag && active && !conv) {
                 // unfinished: hand the current (valid) bracket to the tail launch
@@ -694,6 +713,12 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
                                  n, [&](bool need, double x) {
                                      return count_x_cta(sbuf, nd, need, x, pivmin_x);
                                  });
+        if (!(G == 1 && xpts == 3) && !ycert && !certify && active && lig == 0) {
+            // multisection result: its midpoint is the RQI start, |error| <= half-width
+            // (dx < 0 marks a direct bound, dx >= 0 a Newton step; k_refine_flags)
+            it.x0[id] = 0.5 * (ax + bx);
+            it.dx[id] = -0.5 * (bx - ax);
+        }
         double delta = absfloor;
         if (active) {
             double mag = fmax(fabs(ax), fabs(bx));
@@ -735,7 +760,11 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
 
 // K2' selection: singletons whose certified bracket half-width exceeds
 // gap sqrt(eps_x sqrt(n) / C) need a refined RQI start (see k_refine_x0 in
-// k_bisect.cuh for the argument); all others start at the bracket midpoint (x0 = NaN)
+// k_bisect.cuh for the argument); all others start at the bracket midpoint (x0 = NaN).
+// A root item whose binary_x phase ended in a Newton step dx keeps that step's estimate
+// as its start when the estimate's predicted error -- quadratic convergence, 4 dx^2 / gap
+// (the Newton constant |f''/2f'| is about 1/gap), plus 2 ulps -- is below both the
+// bracket half-width and the requirement above: those items need no refinement pass.
 template <class R>
 __global__ void k_refine_flags(const NodeInfo *__restrict__ nodes, Items it,
                                const int32_t *__restrict__ list, int cnt, double eps_x,
@@ -743,13 +772,23 @@ __global__ void k_refine_flags(const NodeInfo *__restrict__ nodes, Items it,
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cnt) return;
     const int id = list[t];
-    const int64_t n = nodes[it.node[id]].n;
+    const NodeInfo &nd = nodes[it.node[id]];
+    const int64_t n = nd.n;
     const R a = reinterpret_cast<R *>(it.lo)[id];
     const R b = reinterpret_cast<R *>(it.hi)[id];
     const double gap = fmin(it.lgap[id], it.rgap[id]);
     const double need = gap * sqrt(eps_x * sqrt((double)n) / cconv);
-    it.x0[id] = NAN;
-    flags[t] = (0.5 * hi(sub(b, a)) > need && n >= 2) ? 1 : 0;
+    const double half_w = 0.5 * hi(sub(b, a));
+    const double x0 = it.x0[id], dx = it.dx[id];
+    double err = half_w;  // of the midpoint start
+    if (nd.depth == 0 && x0 > hi(a) && x0 < hi(b) && dx < INFINITY && gap > 0.0) {
+        const double pe = dx < 0.0 ? -dx : 4.0 * dx * dx / gap + eps_x * fabs(x0);
+        if (pe < half_w) err = pe;
+    }
+    if (err == half_w) it.x0[id] = NAN;
+    // the refinement ends at about 2 ulps: below 4 ulps it has nothing to add
+    const double floor_ = 4.0 * eps_x * fmax(fabs(hi(a)), fabs(hi(b)));
+    flags[t] = (err > fmax(need, floor_) && n >= 2) ? 1 : 0;
 }
 
 }  // namespace mr3

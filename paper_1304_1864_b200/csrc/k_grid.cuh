@@ -20,6 +20,8 @@
 namespace mr3 {
 
 constexpr int GRID_L1 = 2048;
+constexpr int GRID_LEVELS = 3;  // adaptive levels after the uniform one
+constexpr int CELL_PMIN = 64;   // points per subdivided cell, at least
 
 struct GridInfo {
     double L, U;       // root enclosure: count(L) = 0, count(U) = n
@@ -90,67 +92,131 @@ __device__ __forceinline__ int grid_search(const int *cnt, int lo, int hi, int k
     return r;
 }
 
-// level-2 plan from the level-1 counts.  k_lo..k_hi: global index set; k_first..k_last: slice.
-__global__ void k_grid_setup(GridInfo *gi, const double *brk, const int *cnt1, int n, int k_lo,
-                             int k_hi, int k_first, int k_last, int m2) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    GridInfo g;
-    g.L = brk[0] + brk[1];
-    g.U = brk[2] + brk[3];
-    auto pt1 = [&](int j) -> double {
-        return j < 0 ? g.L : (j >= GRID_L1 ? g.U : grid_pt(g.L, g.U, j, GRID_L1));
-    };
-    auto c1 = [&](int j) -> int { return j < 0 ? 0 : (j >= GRID_L1 ? n : cnt1[j]); };
-    // global interval: left end = last point with count < k_lo, right end = first with count >= k_hi
-    int r = grid_search(cnt1, 0, GRID_L1 - 1, k_lo);
-    g.xa = pt1(r - 1);
-    r = grid_search(cnt1, 0, GRID_L1 - 1, k_hi);
-    g.xb = pt1(r);
-    r = grid_search(cnt1, 0, GRID_L1 - 1, k_first);
-    g.sa = pt1(r - 1);
-    g.csa = c1(r - 1);
-    r = grid_search(cnt1, 0, GRID_L1 - 1, k_last);
-    g.sb = pt1(r);
-    g.csb = c1(r);
-    g.m2 = m2;
-    // level-2 points strictly inside (sa, sb)
-    const double span = g.xb - g.xa;
-    int j0 = 0, j1 = m2 - 1;
-    if (span > 0) {
-        j0 = (int)floor((g.sa - g.xa) / span * (m2 + 1)) - 1;
-        j1 = (int)ceil((g.sb - g.xa) / span * (m2 + 1)) - 1;
-        j0 = max(j0, 0);
-        j1 = min(j1, m2 - 1);
-        while (j0 <= j1 && !(grid_pt(g.xa, g.xb, j0, m2) > g.sa)) j0++;
-        while (j1 >= j0 && !(grid_pt(g.xa, g.xb, j1, m2) < g.sb)) j1--;
-    } else {
-        j1 = -1;
-    }
-    g.j0 = j0;
-    g.j1 = j1;
-    g.pad = 0;
-    *gi = g;
+// ---- adaptive levels: cells holding two or more eigenvalues are subdivided ----------
+//
+// After level 1 every requested index k has a cell [lo, hi] with counts clo < k <= chi.
+// A cell holding c = chi - clo >= 2 eigenvalues is cut by P = max(2c + 1, 64) uniform points; every
+// index of the cell finds its sub-cell by binary search in their counts.  Repeated for a
+// few levels this isolates the eigenvalues at the ends of spectra whose density grows
+// there (Gauss nodes cluster quadratically at +-1), where one uniform grid cannot.
+// The points of a cell are a function of (lo, hi, clo, chi) only -- global quantities --
+// so every rank of the two-phase form computes the same cells for its slice.
+
+struct CellSet {      // per slice item t (item first + t)
+    double *lo, *hi;  // cell bounds
+    int *clo, *chi;   // counts at lo, hi
+    double *lo2, *hi2;  // next level (k_cell_assign writes here; the host swaps)
+    int *clo2, *chi2;
+    int *P;           // points this item's cell gets (leaders only, else 0)
+    int *off;         // exclusive prefix of P
+    int *lead;        // slice position of the item's cell leader
+    int *total;       // device: sum of P
+};
+
+__device__ __forceinline__ double cell_pt(double lo, double hi, int i, int P) {
+    return lo + (hi - lo) * ((double)(i + 1) / (double)(P + 1));
 }
 
-// brackets of the slice's items [first, first + cnt) from the level-2 counts
-template <class R>
-__global__ void k_grid_assign(Items it, int first, int cnt, const GridInfo *__restrict__ gi,
-                              const int *__restrict__ cnt2) {
+// level 1: cells from the uniform level-1 grid
+__global__ void k_cell_init(CellSet cs, const GridInfo *__restrict__ gi, const int *__restrict__ cnt1,
+                            int n, const int32_t *__restrict__ kk, int mine) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= cnt) return;
+    if (t >= mine) return;
     const GridInfo g = *gi;
-    const int id = first + t;
-    const int k = it.k[id];
-    double lo = g.sa, hi = g.sb;
-    if (g.csa < k && k <= g.csb) {
-        const int r = grid_search(cnt2, g.j0, g.j1, k);
-        if (r - 1 >= g.j0) lo = grid_pt(g.xa, g.xb, r - 1, g.m2);
-        if (r <= g.j1) hi = grid_pt(g.xa, g.xb, r, g.m2);
-    } else {
-        return;  // keep the root enclosure (counts inconsistent with the slice plan)
+    const int k = kk[t];
+    const int r = grid_search(cnt1, 0, GRID_L1 - 1, k);
+    cs.lo[t] = r - 1 < 0 ? g.L : grid_pt(g.L, g.U, r - 1, GRID_L1);
+    cs.hi[t] = r >= GRID_L1 ? g.U : grid_pt(g.L, g.U, r, GRID_L1);
+    cs.clo[t] = r - 1 < 0 ? 0 : cnt1[r - 1];
+    cs.chi[t] = r >= GRID_L1 ? n : cnt1[r];
+}
+
+// leaders (first slice item of each cell) and their point counts
+__global__ void k_cell_plan(CellSet cs, int *lead0, int mine, double rtol, double absfloor) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= mine) return;
+    const double lo = cs.lo[t], hi = cs.hi[t];
+    const bool lead = t == 0 || cs.lo[t - 1] != lo || cs.hi[t - 1] != hi;
+    const int c = cs.chi[t] - cs.clo[t];
+    const double tol = fmax(2.0 * rtol * fmax(fabs(lo), fabs(hi)), absfloor);
+    cs.P[t] = (lead && c >= 2 && hi - lo > tol) ? max(2 * c + 1, CELL_PMIN) : 0;
+    lead0[t] = lead ? t : -1;  // (max-scanned into cs.lead)
+}
+
+__global__ void k_cell_total(CellSet cs, int mine) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cs.total = cs.off[mine - 1] + cs.P[mine - 1];
+}
+
+// counts at the points (one per thread, CTA-collective staged counts on the root node)
+template <class R, bool XMODE>
+__global__ void __launch_bounds__(BS_TPB) k_cell_counts(const NodeInfo *__restrict__ nodes,
+                                                        CellSet cs, int mine, int *cnt,
+                                                        double pivmin, double pivmin_x) {
+    __shared__ __align__(16) double sbuf[2 * BS_TILE];
+    const int total = *cs.total;
+    const NodeInfo nd = nodes[0];
+    // grid-stride over the points (uniform trip count per CTA: the counts are collective)
+    for (int base = blockIdx.x * BS_TPB; base < total; base += gridDim.x * BS_TPB) {
+        const int t = base + threadIdx.x;
+        const bool need = t < total;
+        double x = 0.0;
+        if (need) {
+            int l = 0, r = mine;  // last L with off[L] <= t (it owns t: off[L] + P[L] > t)
+            while (r - l > 1) {
+                const int mid = (l + r) >> 1;
+                if (cs.off[mid] <= t)
+                    l = mid;
+                else
+                    r = mid;
+            }
+            x = cell_pt(cs.lo[l], cs.hi[l], t - cs.off[l], cs.P[l]);
+        }
+        int c;
+        if (XMODE) {
+            c = count_x_cta(sbuf, nd, need, x, pivmin_x);
+        } else {
+            int dummy;
+            count_y_cta<R, false>(sbuf, nd, need, mk<R>(x), mk<R>(x), pivmin, c, dummy);
+        }
+        if (need) cnt[t] = c;
     }
-    reinterpret_cast<R *>(it.lo)[id] = mk<R>(lo);
-    reinterpret_cast<R *>(it.hi)[id] = mk<R>(hi);
+}
+
+// every item: its sub-cell in its leader's points (keeps clo < k <= chi with virtual ends)
+__global__ void k_cell_assign(CellSet cs, int mine, const int32_t *__restrict__ kk,
+                              const int *__restrict__ cnt) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= mine) return;
+    const int L = cs.lead[t];
+    const int P = cs.P[L];
+    const double lo = cs.lo[t], hi = cs.hi[t];  // = the leader's (same cell)
+    const int clo = cs.clo[t], chi = cs.chi[t];
+    double nlo = lo, nhi = hi;
+    int nclo = clo, nchi = chi;
+    const int k = kk[t];
+    const int *c = cnt + cs.off[L];
+    const int r = P > 0 ? grid_search(c, 0, P - 1, k) : 0;
+    if (P > 0 && r - 1 >= 0) {
+        nlo = cell_pt(lo, hi, r - 1, P);
+        nclo = c[r - 1];
+    }
+    if (P > 0 && r <= P - 1) {
+        nhi = cell_pt(lo, hi, r, P);
+        nchi = c[r];
+    }
+    cs.lo2[t] = nlo;
+    cs.hi2[t] = nhi;
+    cs.clo2[t] = nclo;
+    cs.chi2[t] = nchi;
+}
+
+// final cells -> item brackets
+template <class R>
+__global__ void k_cell_final(Items it, int first, int mine, CellSet cs) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= mine) return;
+    reinterpret_cast<R *>(it.lo)[first + t] = mk<R>(cs.lo[t]);
+    reinterpret_cast<R *>(it.hi)[first + t] = mk<R>(cs.hi[t]);
 }
 
 }  // namespace mr3

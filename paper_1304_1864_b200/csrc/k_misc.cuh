@@ -63,6 +63,8 @@ __global__ void k_init_items(Items it, int cnt, int k0, int il, int iu, int node
     reinterpret_cast<R *>(it.hi)[t] = mk2<R>(brk[2], brk[3]);
     it.lgap[t] = 1e300;
     it.rgap[t] = 1e300;
+    it.x0[t] = NAN;
+    it.dx[t] = INFINITY;
 }
 
 // split case: items for every eigenvalue of every block
@@ -88,6 +90,8 @@ __global__ void k_init_items_blocks(Items it, int total, const BlockDesc *blocks
     reinterpret_cast<R *>(it.hi)[t] = mk2<R>(brk[4 * b + 2], brk[4 * b + 3]);
     it.lgap[t] = 1e300;
     it.rgap[t] = 1e300;
+    it.x0[t] = NAN;
+    it.dx[t] = INFINITY;
 }
 
 __global__ void k_iota(int32_t *list, int cnt, int start) {
@@ -95,25 +99,31 @@ __global__ void k_iota(int32_t *list, int cnt, int start) {
     if (t < cnt) list[t] = start + t;
 }
 
-// bracket exchange buffer <-> items (4 doubles per record: lo.hi lo.lo hi.hi hi.lo)
+// bracket exchange buffer <-> items (MR3_BRK_REC doubles per record: lo.hi lo.lo hi.hi
+// hi.lo x0 dx -- the bracket and the Newton estimate behind the RQI start)
 template <class R>
 __global__ void k_items_to_brk(Items it, int first, int cnt, double *brk) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cnt) return;
     R l = reinterpret_cast<R *>(it.lo)[first + t], h = reinterpret_cast<R *>(it.hi)[first + t];
-    brk[4 * (int64_t)t + 0] = hi(l);
-    brk[4 * (int64_t)t + 1] = lo_part(l);
-    brk[4 * (int64_t)t + 2] = hi(h);
-    brk[4 * (int64_t)t + 3] = lo_part(h);
+    double *p = brk + MR3_BRK_REC * (int64_t)t;
+    p[0] = hi(l);
+    p[1] = lo_part(l);
+    p[2] = hi(h);
+    p[3] = lo_part(h);
+    p[4] = it.x0[first + t];
+    p[5] = it.dx[first + t];
 }
 template <class R>
 __global__ void k_brk_to_items(Items it, int cnt, int slice_cap, int world, const double *brk) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cnt) return;
     // item t lives in rank t / slice_cap's slice at offset t % slice_cap
-    const double *p = brk + 4 * (int64_t)t;
+    const double *p = brk + MR3_BRK_REC * (int64_t)t;
     reinterpret_cast<R *>(it.lo)[t] = mk2<R>(p[0], p[1]);
     reinterpret_cast<R *>(it.hi)[t] = mk2<R>(p[2], p[3]);
+    it.x0[t] = p[4];
+    it.dx[t] = p[5];
 }
 
 // output columns for the split case: global rank of each item by its midpoint

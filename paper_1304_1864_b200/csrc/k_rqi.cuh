@@ -73,7 +73,14 @@ struct RqiArgs {
     DevStats *st;
     int32_t *dbg_iters;  // optional (MR3_DEBUG): iterations per item
     double *dbg_trace;   // optional (MR3_DEBUG): 8 per item: x0 used, gap, r, res/tol per iteration
+    unsigned long long *dbg_clk;  // optional (MR3_DEBUG): 4 per CTA: start, end (ns), rmin, rmax
 };
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
 
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     const bool active = tid < task.cnt;
     int id = -1, k = 0;
     R lam = mk<R>(0.0), a = lam, b = lam, gr = lam, lam_out = lam;
+    R A_a0 = lam, A_b0 = lam;  // incoming bracket (diagnostics)
     double nz2 = 1.0, gap = INFINITY;
     int64_t r = 0;
     unsigned long long rows = 0;
@@ -269,13 +277,15 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         a = reinterpret_cast<const R *>(A.it.lo)[id];
         b = reinterpret_cast<const R *>(A.it.hi)[id];
         lam = half(add(a, b));
-        const double x0 = A.it.x0[id];
-        if (!isnan(x0) && lt(a, mk<R>(x0)) && lt(mk<R>(x0), b)) lam = mk<R>(x0);
+        A_a0 = a;
+        A_b0 = b;
         if (A.root_widen > 0.0 && nd.depth == 0) {
             const double wd = A.root_widen * (double)n * fmax(fabs(hi(a)), fabs(hi(b)));
             a = sub(a, mk<R>(wd));
             b = add(b, mk<R>(wd));
         }
+        const double x0 = A.it.x0[id];  // refined start (K2'), inside the (widened) guard
+        if (!isnan(x0) && lt(a, mk<R>(x0)) && lt(mk<R>(x0), b)) lam = mk<R>(x0);
         gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0)) gap = fmax(hi(sub(b, a)), 1e-300);
         r = A.it.twist[id];
@@ -299,6 +309,12 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     __syncthreads();
     const int cta_rmin = s_rmin <= s_rmax ? s_rmin : 0;
     const int cta_rmax = s_rmin <= s_rmax ? s_rmax : (int)n - 1;
+    if (A.dbg_clk && tid == 0) {
+        A.dbg_clk[4 * blockIdx.x] = gtimer_ns();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        A.dbg_clk[4 * blockIdx.x + 2] = smid;
+    }
 
     // output column of this eigenpair (rows of its block) and the factors for k_zscale
     const int64_t col0 = active ? A.it.col[id] : -1;
@@ -625,10 +641,15 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 
 #pragma unroll 1
     for (iters = 1; iters <= A.maxit; iters++) {
-        const bool need = !done;
+        // an eigenpair that converged in the first (non-storing) pass joins the next
+        // pass of its CTA at the same shift to write z (instead of an extra pass later)
+        const bool store_only =
+            A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;
+        const bool need = !done || store_only;
         if (!__syncthreads_or(need)) break;
         int c = twisted_fixed(need, A.jobz_v && iters >= 2);
-        if (need) {
+        if (store_only) zfinal = zwritten;
+        if (need && !store_only) {
             if (c >= k) {
                 if (lt(lam, b)) b = lam;
             } else {
@@ -641,7 +662,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                 double *tr = A.dbg_trace + 8 * (int64_t)id;
                 if (iters == 1) {
                     const double x0 = A.it.x0[id];
-                    tr[0] = isnan(x0) ? 0.0 : 1.0;
+                    tr[0] = isnan(x0) ? -0.5 * hi(sub(A_b0, A_a0)) : 1.0;  // -(half-width) if unrefined
                     tr[1] = gap;
                     tr[2] = (double)r;
                 }
@@ -707,6 +728,10 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         reinterpret_cast<R *>(A.it.lo)[id] = lam_out;  // keep lambda[M] for diagnostics
         atomicMax(&A.st->rqi_iters_max, iters);
         if (A.dbg_iters) A.dbg_iters[id] = iters;
+    }
+    if (A.dbg_clk) {
+        atomicMax(&A.dbg_clk[4 * blockIdx.x + 1], gtimer_ns());
+        atomicMax(&A.dbg_clk[4 * blockIdx.x + 3], (unsigned long long)iters);
     }
     if (!A.jobz_v) {
         if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
@@ -898,12 +923,25 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 //   w_k = 1 + 3 |2k - n| / n in [1, 4]: the chosen |gamma_r| is within 4x of the minimum
 //   (Dhillon-Parlett: any twist with |gamma_r| = O(min) gives the same quality of z;
 //   the stopping test is applied to the binary_y gamma_r actually used)
-// s is checkpointed every RQ_C rows (binary64, in ck_W) and recomputed per block
-// during B; rows of M_x are staged through shared memory like k_rqi's.
+// Evaluated without the cancellation in s_k + p_k + lam: with theta_k = prod_{j<k} d+_j
+// (leading minor of M - lam, = the projective qF before row k) and phi_k = prod_{j>k} D-_j
+// (trailing minor, = QB at row k), gamma_k = det(M - lam) / (theta_k phi_k) (Cramer's rule
+// on [(M - lam)^-1]_kk), so argmin_k |gamma_k| w_k = argmax_k log2|theta_k phi_k| - log2 w_k.
+// One sweep: F (top-down, theta) and B (bottom-up, phi) interleaved over all rows,
+// meeting at the middle.  A 32-row tile is reached first by one stream, which keeps its
+// candidate row there -- the row where its half of the eigenvector, y_k = theta_k / PP_k
+// (F) or x_k = phi_k PP_k (B) (k_zprod.cuh), is largest -- and its log2 magnitude; the
+// other stream evaluates the score at that row when it arrives.  Candidates cost 8 bytes
+// per tile and eigenpair (in ck_W); the log2 magnitudes are the exponent-mantissa bits
+// of the binary64 values read as fixed point (error < 0.09, irrelevant for a factor-4
+// tolerant choice).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float flog2_abs(double v) {  // log2|v| (piecewise linear)
+    return (float)(__double2hiint(v) & 0x7fffffff) * 0x1p-20f - 1023.0f;
+}
 template <class R>
 __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
-    __shared__ __align__(16) double sx[2 * StageG<2>::TILE];
+    __shared__ __align__(16) double sx[4 * (StageG<2>::TILE + PP_TILE)];
     const int tid = threadIdx.x;
     const RqiTask task = A.tasks[blockIdx.x];
     const NodeInfo nd = A.nodes[task.node];
@@ -911,7 +949,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     const int64_t slot = (int64_t)blockIdx.x * RQ_TPB + tid;
     const bool active = tid < task.cnt && n > 1;
     int id = -1;
-    double lam = 0.0, pivmin = A.pivmin;
+    double lam = 0.0;
     if (tid < task.cnt) {
         id = A.list[task.first + tid];
         const double a = hi(reinterpret_cast<const R *>(A.it.lo)[id]);
@@ -919,20 +957,25 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         double gap = fmin(A.it.lgap[id], A.it.rgap[id]);
         if (!(gap > 0.0) || !(gap < INFINITY)) gap = fmax(b - a, 1e-300);
         const double x0 = A.it.x0[id];
-        lam = (!isnan(x0) && x0 > a && x0 < b) ? x0 : 0.5 * (a + b);
+        const double wd = (A.root_widen > 0.0 && nd.depth == 0)
+                              ? A.root_widen * (double)n * fmax(fabs(a), fabs(b))
+                              : 0.0;  // as k_rqi's guard
+        lam = (!isnan(x0) && x0 > a - wd && x0 < b + wd) ? x0 : 0.5 * (a + b);
         lam += 1e-4 * gap;
         if (n <= 1) A.it.twist[id] = 0;
     }
-    auto xr = [&](const double *buf, int64_t t0, int64_t k) -> double2 {
-        return *reinterpret_cast<const double2 *>(buf + (k - t0 + RQ_HALO) * 2);
+    if (n <= 1) return;  // (uniform over the CTA: one node per CTA)
+    const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
+    float2 *cand = reinterpret_cast<float2 *>(A.ck_W);  // (log2 magnitude, row) per tile
+    // log2|PP| of the tile's row tr (staged PP rows; slot 3 holds {-1023 - log2|PP|,
+    // -1023 + log2|PP|} as two floats, k_node_pp)
+    auto lppm = [](const double *buf, int tr) -> float {
+        return reinterpret_cast<const float *>(buf + StageG<2>::TILE + (tr + RQ_HALO) * 4 + 3)[0];
     };
-    // projective states (division-free recurrences, as negcount_x): F: s_k = pf/qf,
-    //   D = d qf + pf, pf <- lld pf - lam D, qf <- D;  B: p_k = pb/qb,
-    //   E = lld_{k-1} qb + pb, pb <- d_{k-1} pb - lam E, qb <- E.
-    // The chains are two DFMAs per row; the ratios gamma_k needs are formed off-chain.
-    // Checkpoints (pf, qf) every RQ_C rows in ck_W / ck_p (binary64).
-    double* ckq = reinterpret_cast<double *>(A.ck_p);
-    auto rescale2 = [](double &x, double &y) {
+    auto lppp = [](const double *buf, int tr) -> float {
+        return reinterpret_cast<const float *>(buf + StageG<2>::TILE + (tr + RQ_HALO) * 4 + 3)[1];
+    };
+    auto rescale2 = [](double &x, double &y, int &E) {
         const unsigned ex = (unsigned)__double2hiint(x) & 0x7ff00000u;
         const unsigned ey = (unsigned)__double2hiint(y) & 0x7ff00000u;
         const unsigned em = ex > ey ? ex : ey;
@@ -940,77 +983,178 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
         x *= sc;
         y *= sc;
+        E += (int)(em >> 20) - 1023;
     };
-    double pf = -lam, qf = 1.0;
-    staged_pass_g<2>(sx, nd.repx, n, false, [&](const double *buf, int64_t t0) {
-        if (!active) return;
+    const float wfac = (float)(A.twist_w / (double)n);
+    auto logw = [&](int64_t k) -> float {  // log2 of the twist weight 1 + w |2k - n| / n
+        return __log2f(fmaf(wfac, fabsf(2.0f * (float)k - (float)n), 1.0f));
+    };
+    // F: theta (projective pf/qf, exponent EF); B: phi (pb/qb, EB)
+    double pf = -lam, qf = 1.0, pb = 0.0, qb = 1.0;
+    int EF = 0, EB = 0;
+    if (active) pb = __ldg(nd.repx + 2 * (n - 1)) - lam;
+    float best = -INFINITY;
+    int64_t rr = n / 2;  // (kept if every score is -inf: no usable twist information)
+    // tile i is reached first by F iff 2 i < ntile - 1, by B iff 2 i > ntile - 1, by both
+    // at the same step iff 2 i == ntile - 1 (F's rows of that tile are run first then)
+    // First half of the sweep (F below the middle tile, B above it): each stream keeps
+    // per tile the row where its half-vector is largest (log2|y_k| = log2|theta_k| -
+    // log2|PP_k|, log2|x_k| = log2|phi_k| + log2|PP_k|).  Second half: each stream
+    // captures its own value at the other stream's candidate row of the tile and scores
+    // it once per tile: log2|gamma_k|^-1 + const = log2|y_k| + log2|x_k| - log2 w_k.
+    // The mode is uniform over the CTA at every step (a function of the tile only).
+    float EFf = 0.0f, EBf = 0.0f;  // EF, EB as float (log2 bookkeeping)
+    // one row of F / B; MODE 0: keep the candidate (cv, ci); MODE 1: capture the state at
+    // row ci (into qc, ec); GUARD: rows may reach n
+    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, float &cv, int &ci,
+                    double &qc, float &ec) {
+        constexpr int MODE = decltype(mode)::value;
+        constexpr bool GUARD = decltype(guard)::value;
+        if (GUARD && kk >= n) return;
+        if (MODE == 0) {
+            const float lt = fmaf((float)(__double2hiint(qf) & 0x7fffffff), 0x1p-20f,
+                                  EFf + lppm(bA, tr));  // log2|y_kk|
+            const bool up = lt > cv;
+            cv = up ? lt : cv;
+            ci = up ? kk : ci;
+        } else {
+            const bool at = kk == ci;
+            qc = at ? qf : qc;
+            ec = at ? EFf : ec;
+        }
+        if (!GUARD || kk < n - 1) {
+            const double2 rw = *reinterpret_cast<const double2 *>(bA + (tr + RQ_HALO) * 2);
+            const double D = fma_rn(rw.x, qf, pf);
+            pf = fma_rn(-lam, D, mul_rn(rw.y, pf));
+            qf = D;
+        }
+    };
+    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, float &cv, int &ci,
+                    double &qc, float &ec) {
+        constexpr int MODE = decltype(mode)::value;
+        constexpr bool GUARD = decltype(guard)::value;
+        if (GUARD && kk >= n) return;
+        if (MODE == 0) {
+            const float lp = fmaf((float)(__double2hiint(qb) & 0x7fffffff), 0x1p-20f,
+                                  EBf + lppp(bD, tr));  // log2|x_kk|
+            const bool up = lp > cv;
+            cv = up ? lp : cv;
+            ci = up ? kk : ci;
+        } else {
+            const bool at = kk == ci;
+            qc = at ? qb : qc;
+            ec = at ? EBf : ec;
+        }
+        if (kk > 0) {
+            const double2 rw = *reinterpret_cast<const double2 *>(bD + (tr - 1 + RQ_HALO) * 2);
+            const double E = fma_rn(rw.y, qb, pb);
+            pb = fma_rn(-lam, E, mul_rn(rw.x, pb));
+            qb = E;
+        }
+    };
+    auto rescale2f = [&](double &x, double &y, int &E, float &Ef) {
+        rescale2(x, y, E);
+        Ef = (float)E;
+    };
+    using M0 = std::integral_constant<int, 0>;
+    using M1 = std::integral_constant<int, 1>;
+    using G0 = std::integral_constant<bool, false>;
+    using G1 = std::integral_constant<bool, true>;
+    // both streams over one step's tiles, rows interleaved
+    auto step = [&](auto mode, auto guard, const double *bA, int64_t tA, const double *bD,
+                    int64_t tD, float &cvf, int &cif, double &qcf, float &ecf, float &cvb, int &cib,
+                    double &qcb, float &ecb) {
 #pragma unroll 1
         for (int q = 0; q < RQ_TR / RQ_C; q++) {
-            const int64_t b0 = t0 + q * RQ_C;
-            if (b0 >= n) break;
-            A.ck_W[(b0 / RQ_C) * A.S + slot] = pf;
-            ckq[(b0 / RQ_C) * A.S + slot] = qf;
+            const int oF = q * RQ_C, oB = (RQ_TR / RQ_C - 1 - q) * RQ_C;
 #pragma unroll
             for (int j = 0; j < RQ_C; j++) {
-                const int64_t kk = b0 + j;
-                if (kk < n - 1) {
-                    const double2 rw = xr(buf, t0, kk);
-                    const double D = fma_rn(rw.x, qf, pf);
-                    pf = fma_rn(-lam, D, mul_rn(rw.y, pf));
-                    qf = D;
-                }
+                frow(mode, guard, bA, oF + j, (int)tA + oF + j, cvf, cif, qcf, ecf);
+                brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, cvb, cib,
+                     qcb, ecb);
             }
-            rescale2(pf, qf);
+            rescale2f(pf, qf, EF, EFf);
+            rescale2f(pb, qb, EB, EBf);
         }
-    });
-    double pb = 0.0, qb = 1.0, best = INFINITY;
-    const double wfac = A.twist_w / (double)n;
-    int64_t rr = n - 1;
-    if (active) pb = __ldg(nd.repx + 2 * (n - 1)) - lam;
-    staged_pass_g<2>(sx, nd.repx, n, true, [&](const double *buf, int64_t t0) {
-        if (!active) return;
+    };
+    dual_staged_pass<2>(
+        sx, nd.repx, n, 0, ntile, ntile - 1, ntile,
+        [&](const double *bA, int64_t tA, const double *bD, int64_t tD) {
+            if (!active) return;
+            const int iA = (int)(tA / RQ_TR), iD = (int)(tD / RQ_TR);
+            const bool guard = tA + RQ_TR > n - 1 || tD + RQ_TR > n - 1 || tD == 0;
+            float cvf = -INFINITY, cvb = -INFINITY, ecf = 0.0f, ecb = 0.0f;
+            int cif = -1, cib = -1;
+            double qcf = 0.0, qcb = 0.0;
+            if (2 * iA < ntile - 1) {  // first half: keep candidates
+                if (guard)
+                    step(M0{}, G1{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+                else
+                    step(M0{}, G0{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+                cand[(int64_t)iA * A.S + slot] = make_float2(cvf, __int_as_float(cif));
+                cand[(int64_t)iD * A.S + slot] = make_float2(cvb, __int_as_float(cib));
+                return;
+            }
+            if (2 * iA == ntile - 1) {  // middle tile (odd ntile): F keeps, then B scores
 #pragma unroll 1
-        for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
-            const int64_t b0 = t0 + q * RQ_C;
-            if (b0 >= n) continue;
-            double sb[RQ_C];
-            double p2 = A.ck_W[(b0 / RQ_C) * A.S + slot];
-            double q2 = ckq[(b0 / RQ_C) * A.S + slot];
+                for (int q = 0; q < RQ_TR / RQ_C; q++) {
 #pragma unroll
-            for (int j = 0; j < RQ_C; j++) {
-                const int64_t kk = b0 + j;
-                sb[j] = div(p2, q2);  // s_kk (off the chain)
-                if (kk < n - 1) {
-                    const double2 rw = xr(buf, t0, kk);
-                    const double D = fma_rn(rw.x, q2, p2);
-                    p2 = fma_rn(-lam, D, mul_rn(rw.y, p2));
-                    q2 = D;
+                    for (int j = 0; j < RQ_C; j++)
+                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, cvf, cif, qcf,
+                             ecf);
+                    rescale2f(pf, qf, EF, EFf);
                 }
-            }
+                cib = cif;
+#pragma unroll 1
+                for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
 #pragma unroll
-            for (int j = RQ_C - 1; j >= 0; j--) {
-                const int64_t kk = b0 + j;
-                if (kk < n) {
-                    // |gamma_k| weighted by 1 + 3 |2k - n| / n: among twists within a
-                    // factor 4 of the optimum, prefer one near the middle, where the
-                    // top-down and bottom-up halves of k_rqi's sweeps are balanced
-                    const double g = fabs(sb[j] + div(pb, qb) + lam) *
-                                     fma(wfac, fabs(2.0 * (double)kk - (double)n), 1.0);
-                    if (g <= best) {
-                        best = g;
-                        rr = kk;
-                    }
-                    if (kk > 0) {
-                        const double2 rw = xr(buf, t0, kk - 1);
-                        const double E = fma_rn(rw.y, qb, pb);
-                        pb = fma_rn(-lam, E, mul_rn(rw.x, pb));
-                        qb = E;
+                    for (int j = RQ_C - 1; j >= 0; j--)
+                        brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, cvb, cib, qcb,
+                             ecb);
+                    rescale2f(pb, qb, EB, EBf);
+                }
+                if (cib >= 0) {  // log2|y| (F's candidate) + log2|x| at that row
+                    const float lx = fmaf((float)(__double2hiint(qcb) & 0x7fffffff), 0x1p-20f,
+                                          ecb + lppp(bD, cib - (int)tD));
+                    const float sc = cvf + lx - logw(cib);
+                    if (sc > best) {
+                        best = sc;
+                        rr = cib;
                     }
                 }
+                return;
             }
-            rescale2(pb, qb);
-        }
-    });
+            // second half: capture the values at the other stream's candidate rows
+            const float2 oF = cand[(int64_t)iA * A.S + slot];  // B's candidate of F's tile
+            const float2 oB = cand[(int64_t)iD * A.S + slot];  // F's candidate of B's tile
+            cif = __float_as_int(oF.y);
+            cib = __float_as_int(oB.y);
+            if (guard)
+                step(M1{}, G1{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+            else
+                step(M1{}, G0{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+            if (cif >= 0) {  // log2|y| at F's row + B's stored log2|x|
+                const float ly = fmaf((float)(__double2hiint(qcf) & 0x7fffffff), 0x1p-20f,
+                                      ecf + lppm(bA, cif - (int)tA));
+                const float sc = ly + oF.x - logw(cif);
+                if (sc > best) {
+                    best = sc;
+                    rr = cif;
+                }
+            }
+            if (cib >= 0) {
+                const float lx = fmaf((float)(__double2hiint(qcb) & 0x7fffffff), 0x1p-20f,
+                                      ecb + lppp(bD, cib - (int)tD));
+                const float sc = oB.x + lx - logw(cib);
+                if (sc > best) {
+                    best = sc;
+                    rr = cib;
+                }
+            }
+        },
+        nd.pp);
+    // F's candidates (tiles reached by F first) scored against B: B evaluated those in
+    // its own later tiles; B's candidates scored by F likewise.  Rows scored: one per tile.
     if (active) A.it.twist[id] = (int32_t)rr;
 }
 

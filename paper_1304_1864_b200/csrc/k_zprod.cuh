@@ -22,7 +22,8 @@
 
 namespace mr3 {
 
-// per row of a node: {PPm, IPPm, E, 0} (binary64): PP_k = PPm 2^E, 1/PP_k = IPPm 2^-E.
+// per row of a node: {PPm, IPPm, E, (two floats: -1023 -+ log2|PP_k|)}: PP_k = PPm 2^E,
+// 1/PP_k = IPPm 2^-E.
 // The mantissas are products of the representation's ld in pair arithmetic, rounded
 // once: z components come out to binary64 accuracy (the output precision).
 constexpr int PP_STRIDE = 4;
@@ -97,7 +98,11 @@ __global__ void __launch_bounds__(256) k_node_pp(NodeInfo *nodes, int first, dou
         o[0] = hi(pm);
         o[1] = hi(ipm);
         o[2] = (double)pe;
-        o[3] = 0.0;
+        {  // {-1023 - log2|PP_j|, -1023 + log2|PP_j|} as floats (k_rqi_locate)
+            const float l = (float)(log2(fabs(hi(pm))) + (double)pe);
+            float2 *f = reinterpret_cast<float2 *>(o + 3);
+            *f = make_float2(-1023.0f - l, -1023.0f + l);
+        }
         if (j <= n - 2) {
             pm = mul(pm, neg(load_row4<R>(nd.rep, j).ld));
             normalize_me(pm, pe);

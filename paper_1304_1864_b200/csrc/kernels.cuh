@@ -32,6 +32,7 @@ struct Items {  // eigenvalue slots, SoA over the requested index set (+ guards)
     void *lo, *hi;   // R brackets [lo, hi] in node coordinates
     double *lgap, *rgap;  // absolute gaps to the neighbours (node coordinates)
     double *x0;           // RQI starting point (binary64, node coordinates) or NaN: midpoint
+    double *dx;           // |last Newton step| of the root binary_x phase behind x0 (INF: none)
     int32_t *twist;       // RQI twist index r (0-based row of the node), from k_rqi_locate
 };
 

@@ -50,6 +50,7 @@ struct Cfg {  // per-mode parameters
 struct mr3_ctx_s {
     double t_last = 0.0;  // host wall time of the last synchronisation point (MR3_DEBUG & 2)
     int dump = 0;         // MR3_DEBUG & 1: items to dump
+    size_t mem_free = 0;  // device free memory seen by the first solve (RQI scratch budget)
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -113,6 +114,8 @@ static const double kDefaults[2][MR3_NPARAM] = {
 #define CKL(name)                                                                         \
     do {                                                                                  \
         cudaError_t _e = cudaGetLastError();                                              \
+        if (_e == cudaSuccess && (ctx->debug & 8)) /* MR3_DEBUG & 8: check every launch */ \
+            _e = cudaStreamSynchronize(ctx->stream);                                      \
         if (_e != cudaSuccess) {                                                          \
             ctx->err = std::string("launch ") + name + ": " + cudaGetErrorString(_e);      \
             return MR3_ERR_CUDA;                                                          \
@@ -238,7 +241,8 @@ static int choose_tpb(mr3_ctx ctx, int64_t thr, int tpb_max) {
 template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x,
-                         const char *tname = "k_bisect", int ycert = 1, char *tailflag = nullptr) {
+                         const char *tname = "k_bisect", int ycert = 1, char *tailflag = nullptr,
+                         double widen = 0.0) {
     if (cnt <= 0) return 0;
     int rc = 0;
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
@@ -265,11 +269,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
         if (xphase)                                                                           \
             k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, tailflag, maxpass, W.st);                               \
+                certify, xpts, ycert, tailflag, maxpass, widen, W.st);                               \
         else                                                                                  \
             k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, tailflag, maxpass, W.st);                               \
+                certify, xpts, ycert, tailflag, maxpass, widen, W.st);                               \
         break;
     switch (G) {
         BIS(1)
@@ -501,6 +505,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
         it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
+        it.dx = (double *)getbuf(ctx, "it_dx", cnt * 8, &rc);
         it.twist = (int32_t *)getbuf(ctx, "it_twist", cnt * 4, &rc);
         if (rc) return rc;
         k_init_items<R><<<(cnt + 255) / 256, 256, 0, s>>>(it, cnt, (int)k_lo, (int)ilw, (int)iuw, 0,
@@ -526,6 +531,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         it.lgap = (double *)getbuf(ctx, "it_lgap", cnt * 8, &rc);
         it.rgap = (double *)getbuf(ctx, "it_rgap", cnt * 8, &rc);
         it.x0 = (double *)getbuf(ctx, "it_x0", cnt * 8, &rc);
+        it.dx = (double *)getbuf(ctx, "it_dx", cnt * 8, &rc);
         it.twist = (int32_t *)getbuf(ctx, "it_twist", cnt * 4, &rc);
         if (rc) return rc;
         CK(cudaMemcpyAsync(ditem0, item0.data(), item0.size() * 8, cudaMemcpyHostToDevice, s));
@@ -539,7 +545,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     int64_t first = std::min<int64_t>((int64_t)rank * cap, cnt);
     int64_t mine = std::min<int64_t>(cap, cnt - first);
     ctx->slice_cap = cap;
-    double *dbrk = (double *)getbuf(ctx, "brk", (size_t)world * cap * 4 * 8, &rc);
+    double *dbrk = (double *)getbuf(ctx, "brk", (size_t)world * cap * MR3_BRK_REC * 8, &rc);
     int32_t *list = (int32_t *)getbuf(ctx, "list0", (size_t)cnt * 4, &rc);
     DevStats *dst = (DevStats *)getbuf(ctx, "devstats", sizeof(DevStats), &rc);
     if (rc) return rc;
@@ -553,6 +559,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
     W.it.x0 = (double *)ctx->bufs["it_x0"].p;
+    W.it.dx = (double *)ctx->bufs["it_dx"].p;
     W.it.twist = (int32_t *)ctx->bufs["it_twist"].p;
     W.nodes = dnodes;
     W.st = dst;
@@ -564,40 +571,75 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         ctx->G0 = choose_groups(ctx, cnt, (int)P[MR3_GROUPS]);
         const bool xphase = words == 2 && P[MR3_XPHASE] != 0;
         if (!ctx->split && P[MR3_GRID] != 0 && cnt >= 512) {
-            // shared top of the bisection tree: brackets from two grids of counts
-            // level-2 points per requested index: MR3_GRID (1 = default 1.5)
-            const double gfac = P[MR3_GRID] == 1.0 ? 1.5 : P[MR3_GRID];
-            const int m2 = (int)std::min<int64_t>((int64_t)(gfac * cnt) + 64, 1 << 30);
+            // shared top of the bisection tree: a uniform grid of counts, then cells with
+            // two or more eigenvalues subdivided level by level (k_grid.cuh)
             GridInfo *gi = (GridInfo *)getbuf(ctx, "grid_info", sizeof(GridInfo), &rc);
             int *c1 = (int *)getbuf(ctx, "grid_c1", GRID_L1 * 4, &rc);
-            int *c2 = (int *)getbuf(ctx, "grid_c2", (size_t)m2 * 4, &rc);
+            // points of one level: sum over cells of max(2c + 1, CELL_PMIN), c <= n for the
+            // (at most two) cells reaching past the slice, one leader per slice item at most
+            const int64_t bound = (2 + CELL_PMIN + 1) * mine + 4 * n + 64;
+            int *cp = (int *)getbuf(ctx, "grid_cp", (size_t)bound * 4, &rc);
+            CellSet cs;
+            cs.lo = (double *)getbuf(ctx, "cell_lo", (size_t)mine * 8, &rc);
+            cs.hi = (double *)getbuf(ctx, "cell_hi", (size_t)mine * 8, &rc);
+            cs.lo2 = (double *)getbuf(ctx, "cell_lo2", (size_t)mine * 8, &rc);
+            cs.hi2 = (double *)getbuf(ctx, "cell_hi2", (size_t)mine * 8, &rc);
+            cs.clo = (int *)getbuf(ctx, "cell_clo", (size_t)mine * 4, &rc);
+            cs.chi = (int *)getbuf(ctx, "cell_chi", (size_t)mine * 4, &rc);
+            cs.clo2 = (int *)getbuf(ctx, "cell_clo2", (size_t)mine * 4, &rc);
+            cs.chi2 = (int *)getbuf(ctx, "cell_chi2", (size_t)mine * 4, &rc);
+            cs.P = (int *)getbuf(ctx, "cell_P", (size_t)mine * 4, &rc);
+            cs.off = (int *)getbuf(ctx, "cell_off", (size_t)mine * 4, &rc);
+            cs.lead = (int *)getbuf(ctx, "cell_lead", (size_t)mine * 4, &rc);
+            cs.total = (int *)getbuf(ctx, "cell_total", 16, &rc);
             if (rc) return rc;
-            const int k_lo = (int)std::max<int64_t>(1, ilw - 1);
-            const int k_hi = k_lo + cnt - 1;
+            size_t tb1 = 0, tb2 = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb1, cs.P, cs.off, (int)mine, s);
+            int *lead0 = (int *)getbuf(ctx, "cell_lead0", (size_t)mine * 4, &rc);
+            cub::DeviceScan::InclusiveScan(nullptr, tb2, lead0, cs.lead, cub::Max(), (int)mine, s);
+            void *ctmp = getbuf(ctx, "cubtmp_cell", std::max(tb1, tb2), &rc);
+            if (rc) return rc;
+            const int32_t *kslice = W.it.k + first;
+            const int ib = (int)((mine + 255) / 256);
             KTime *tg = kt_begin(ctx, "k_grid");
             k_grid_init<<<1, 32, 0, s>>>(gi, dbrk0);
             CKL("k_grid_init");
-            auto counts = [&](int level, int npts) -> int {
-                const int g = (npts + BS_TPB - 1) / BS_TPB;
+            if (xphase)
+                k_grid_counts<R, true><<<GRID_L1 / BS_TPB, BS_TPB, 0, s>>>(dnodes, 0, 1, gi, c1,
+                                                                         ctx->pivmin, 0x1p-900);
+            else
+                k_grid_counts<R, false><<<GRID_L1 / BS_TPB, BS_TPB, 0, s>>>(dnodes, 0, 1, gi, c1,
+                                                                          ctx->pivmin, 0x1p-900);
+            CKL("k_grid_counts");
+            k_cell_init<<<ib, 256, 0, s>>>(cs, gi, c1, (int)n, kslice, (int)mine);
+            CKL("k_cell_init");
+            for (int lev = 0; lev < GRID_LEVELS; lev++) {
+                k_cell_plan<<<ib, 256, 0, s>>>(cs, lead0, (int)mine, rtol, absfloor);
+                CKL("k_cell_plan");
+                size_t t1 = tb1, t2 = tb2;
+                cub::DeviceScan::ExclusiveSum(ctmp, t1, cs.P, cs.off, (int)mine, s);
+                cub::DeviceScan::InclusiveScan(ctmp, t2, lead0, cs.lead, cub::Max(), (int)mine, s);
+                CKL("cell scans");
+                k_cell_total<<<1, 32, 0, s>>>(cs, (int)mine);
+                CKL("k_cell_total");
+                const int g = (int)std::min<int64_t>((bound + BS_TPB - 1) / BS_TPB,
+                                                     (int64_t)ctx->nsm * 8);
                 if (xphase)
-                    k_grid_counts<R, true><<<g, BS_TPB, 0, s>>>(dnodes, 0, level, gi,
-                                                                 level == 1 ? c1 : c2,
-                                                                 ctx->pivmin, 0x1p-900);
+                    k_cell_counts<R, true><<<g, BS_TPB, 0, s>>>(dnodes, cs, (int)mine, cp,
+                                                               ctx->pivmin, 0x1p-900);
                 else
-                    k_grid_counts<R, false><<<g, BS_TPB, 0, s>>>(dnodes, 0, level, gi,
-                                                                  level == 1 ? c1 : c2,
-                                                                  ctx->pivmin, 0x1p-900);
-                CKL("k_grid_counts");
-                return 0;
-            };
-            if ((rc = counts(1, GRID_L1))) return rc;
-            k_grid_setup<<<1, 32, 0, s>>>(gi, dbrk0, c1, (int)n, k_lo, k_hi, k_lo + (int)first,
-                                          k_lo + (int)(first + mine - 1), m2);
-            CKL("k_grid_setup");
-            if ((rc = counts(2, m2))) return rc;
-            k_grid_assign<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
-                                                                       gi, c2);
-            CKL("k_grid_assign");
+                    k_cell_counts<R, false><<<g, BS_TPB, 0, s>>>(dnodes, cs, (int)mine, cp,
+                                                                ctx->pivmin, 0x1p-900);
+                CKL("k_cell_counts");
+                k_cell_assign<<<ib, 256, 0, s>>>(cs, (int)mine, kslice, cp);
+                CKL("k_cell_assign");
+                std::swap(cs.lo, cs.lo2);
+                std::swap(cs.hi, cs.hi2);
+                std::swap(cs.clo, cs.clo2);
+                std::swap(cs.chi, cs.chi2);
+            }
+            k_cell_final<R><<<ib, 256, 0, s>>>(W.it, (int)first, (int)mine, cs);
+            CKL("k_cell_final");
             kt_end(ctx, tg);
         }
         // definite roots: binary_x brackets are enclosed rigorously after widening by the
@@ -628,16 +670,34 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             int ht = 0;
             CK(cudaMemcpyAsync(&ht, tc, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#6");
+            if (ctx->dump) {
+                fprintf(stderr, "[mr3] Newton tail: %d of %d items:", ht, (int)mine);
+                std::vector<int32_t> htl(ht);
+                cudaMemcpy(htl.data(), tl, ht * 4, cudaMemcpyDeviceToHost);
+                std::vector<int> hclo(mine), hchi(mine);
+                if (ctx->bufs.count("cell_clo")) {
+                    // final cells: after GRID_LEVELS swaps the current arrays alternate
+                    const char *a = (GRID_LEVELS % 2) ? "cell_clo2" : "cell_clo";
+                    const char *b = (GRID_LEVELS % 2) ? "cell_chi2" : "cell_chi";
+                    cudaMemcpy(hclo.data(), ctx->bufs[a].p, mine * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(hchi.data(), ctx->bufs[b].p, mine * 4, cudaMemcpyDeviceToHost);
+                }
+                for (int i = 0; i < ht; i++)
+                    fprintf(stderr, " %d(%d)", htl[i], hchi[htl[i] - first] - hclo[htl[i] - first]);
+                fprintf(stderr, "\n");
+            }
             if (ht > 0) {
+                // to the RQI-start precision (2 ulps) at once: the midpoints are the starts
+                // and the refinement pass (K2') has nothing left to do for these items
                 int G = choose_groups(ctx, ht, 0);
                 if (G < 8) G = 8;
-                rc = launch_bisect<R>(ctx, W, tl, ht, G, rtol, absfloor, 0, true, eps_x, "k_bisect",
-                                      0, nullptr);
+                rc = launch_bisect<R>(ctx, W, tl, ht, G, 2.0 * eps_x, absfloor, 0, true, eps_x,
+                                      "k_bisect", 0, nullptr);
             }
         }
         if (rc) return rc;
         k_items_to_brk<R><<<(int)((mine + 255) / 256), 256, 0, s>>>(W.it, (int)first, (int)mine,
-                                                                    dbrk + 4 * first);
+                                                                    dbrk + MR3_BRK_REC * first);
         CKL("k_items_to_brk");
     }
     CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#7");
@@ -681,6 +741,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.it.lgap = (double *)ctx->bufs["it_lgap"].p;
     W.it.rgap = (double *)ctx->bufs["it_rgap"].p;
     W.it.x0 = (double *)ctx->bufs["it_x0"].p;
+    W.it.dx = (double *)ctx->bufs["it_dx"].p;
     W.it.twist = (int32_t *)ctx->bufs["it_twist"].p;
     W.nodes = (NodeInfo *)ctx->bufs["nodes"].p;
     W.st = (DevStats *)ctx->bufs["devstats"].p;
@@ -774,27 +835,6 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#10");
     int nsing = hc[0], nclus = hc[1], nmem = hc[2];
-    if (ctx->dump && P[MR3_XPTS] == 3) {  // passes per item of the Newton x-phase
-        std::vector<double> ps(cnt);
-        cudaMemcpy(ps.data(), W.it.x0, cnt * 8, cudaMemcpyDeviceToHost);
-        int hist[41] = {0};
-        for (int i = 0; i < cnt; i++) hist[std::min(40, std::max(0, (int)ps[i]))]++;
-        fprintf(stderr, "[mr3] newton passes histogram:");
-        for (int i = 0; i <= 40; i++)
-            if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
-        fprintf(stderr, "\n");
-        // per 128-item CTA: max passes histogram
-        int chist[41] = {0};
-        for (int b0 = 0; b0 < cnt; b0 += 128) {
-            int mx = 0;
-            for (int i = b0; i < std::min(cnt, b0 + 128); i++) mx = std::max(mx, (int)ps[i]);
-            chist[std::min(40, mx)]++;
-        }
-        fprintf(stderr, "[mr3] newton CTA-max passes histogram:");
-        for (int i = 0; i <= 40; i++)
-            if (chist[i]) fprintf(stderr, " %d:%d", i, chist[i]);
-        fprintf(stderr, "\n");
-    }
     if (ctx->dump) fprintf(stderr, "[mr3] level 0: %d singles %d clusters %d members\n", nsing, nclus, nmem);
 
     // multi-rank: cluster-whole partition of the output columns
@@ -873,8 +913,14 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     }
 
     // RQI scratch sizing: checkpoints of (s, W, p) every RQ_C rows per eigenpair
-    size_t freeb = 0, totb = 0;
-    cudaMemGetInfo(&freeb, &totb);
+    // (cudaMemGetInfo once per context: the call can stall the host for tens of ms
+    // while the device works; a failed allocation below halves the chunk instead)
+    if (ctx->mem_free == 0) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        ctx->mem_free = std::max<size_t>(fr, 1);
+    }
+    const size_t freeb = ctx->mem_free;
     const int64_t nmaxb = ctx->n;
     const int64_t nblk = (nmaxb + RQ_C - 1) / RQ_C;
     size_t budget = std::min<size_t>((size_t)(freeb * 0.6), (size_t)48 << 30);
@@ -909,13 +955,37 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             int hr = 0;
             CK(cudaMemcpyAsync(&hr, rcnt, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#13");
+            if (ctx->dump) fprintf(stderr, "[mr3] refine: %d of %d singletons\n", hr, ncount);
             if (hr > 0) {
                 // many lanes per item: few items, short dependent chains (log2(G+1) bits/round)
                 int G = choose_groups(ctx, hr, 0);
                 if (G < 16) G = 16;
                 rc2 = launch_bisect<R>(ctx, W, rlist, hr, G, 2.0 * eps_x, 1e-300, 2, true, eps_x,
-                                       "k_refine_x0");
+                                       "k_refine_x0", 1, nullptr, ctx->root_widen);
                 if (rc2) return rc2;
+                if (ctx->dump) {
+                    cudaStreamSynchronize(s);
+                    std::vector<int32_t> hl(hr);
+                    cudaMemcpy(hl.data(), rlist, hr * 4, cudaMemcpyDeviceToHost);
+                    int mid = 0;
+                    for (int i = 0; i < hr; i++) mid = std::max(mid, hl[i]);
+                    std::vector<double> hx(mid + 1), hd(mid + 1), hg(mid + 1);
+                    cudaMemcpy(hx.data(), W.it.x0, hx.size() * 8, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(hd.data(), W.it.dx, hd.size() * 8, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(hg.data(), W.it.lgap, hg.size() * 8, cudaMemcpyDeviceToHost);
+                    int nn = 0, ninf = 0;
+                    for (int i = 0; i < hr; i++) {
+                        nn += std::isnan(hx[hl[i]]) ? 1 : 0;
+                        ninf += std::isinf(hd[hl[i]]) ? 1 : 0;
+                    }
+                    fprintf(stderr, "[mr3] refine: %d NaN x0 of %d, %d without a Newton step; dx/lgap:", nn, hr, ninf);
+                    for (int i = 0; i < hr; i += std::max(1, hr / 40))
+                        fprintf(stderr, " %d:%.2g/%.2g", hl[i], hd[hl[i]], hg[hl[i]]);
+                    fprintf(stderr, "\n[mr3] ids:");
+                    for (int i = 0; i < hr; i++)
+                        if (hl[i] >= 49500) fprintf(stderr, " %d%s", hl[i], std::isnan(hx[hl[i]]) ? "n" : "");
+                    fprintf(stderr, "\n");
+                }
             }
             kt_end(ctx, tr);
         } else {
@@ -947,7 +1017,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             }
             return 0;
         };
-        const int64_t tmax = std::max<int64_t>(1, Smax / rtpb);
+        int64_t tmax = std::max<int64_t>(1, Smax / rtpb);
         auto launch_chunks = [&](bool locate, const int32_t *lst, int ntasks) -> int {
             for (int off = 0; off < ntasks;) {
                 const int nb = (int)std::min<int64_t>(tmax, ntasks - off);
@@ -955,6 +1025,11 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 int rc3 = 0;
                 char *ck =
                     (char *)getbuf(ctx, "rqi_ck", (size_t)nblk * S * (2 * sizeof(R) + 8), &rc3);
+                if (rc3 == MR3_ERR_NOMEM && tmax > 1) {  // memory got tighter: smaller chunks
+                    tmax = std::max<int64_t>(1, tmax / 2);
+                    ctx->mem_free = 0;
+                    continue;
+                }
                 if (rc3) return rc3;
                 RqiArgs<R> A;
                 A.nodes = W.nodes;
@@ -982,6 +1057,11 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.st = W.st;
                 A.dbg_iters = nullptr;
                 A.dbg_trace = nullptr;
+                A.dbg_clk = nullptr;
+                if (ctx->dump && !locate) {
+                    A.dbg_clk = (unsigned long long *)getbuf(ctx, "dbg_clk", (size_t)nb * 32, &rc3);
+                    cudaMemsetAsync(A.dbg_clk, 0, (size_t)nb * 32, s);
+                }
                 if (ctx->dump) {
                     A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
                     A.dbg_trace = (double *)getbuf(ctx, "dbg_trace", (size_t)cnt * 64, &rc3);
@@ -992,11 +1072,44 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 else
                 {
                     constexpr size_t smem = rqi_smem_bytes<R, OutT>();
-                    cudaFuncSetAttribute(k_rqi<R, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                    static bool attr_set = false;  // per instantiation, once per process
+                    if (!attr_set) {
+                        cudaFuncSetAttribute(k_rqi<R, OutT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                        attr_set = true;
+                    }
                     k_rqi<R, OutT><<<nb, rtpb, smem, s>>>(A);
                 }
                 kt_end(ctx, t);
+                if (A.dbg_clk) {  // per-CTA durations against the CTA's sweep length
+                    std::vector<unsigned long long> hc((size_t)nb * 4);
+                    cudaMemcpyAsync(hc.data(), A.dbg_clk, (size_t)nb * 32, cudaMemcpyDeviceToHost, s);
+                    cudaStreamSynchronize(s);
+                    unsigned long long t0 = ~0ull, t1 = 0;
+                    for (int b = 0; b < nb; b++) {
+                        t0 = std::min(t0, hc[4 * b]);
+                        t1 = std::max(t1, hc[4 * b + 1]);
+                    }
+                    std::map<unsigned long long, int> per_sm;
+                    for (int b = 0; b < nb; b++) per_sm[hc[4 * b + 2]]++;
+                    // duration histogram (2 ms bins) split by CTAs on the SM and max iterations
+                    std::map<std::pair<int, int>, std::vector<double>> grp;
+                    double busy = 0;
+                    for (int b = 0; b < nb; b++) {
+                        const double dur = 1e-6 * (double)(hc[4 * b + 1] - hc[4 * b]);
+                        grp[{per_sm[hc[4 * b + 2]], (int)hc[4 * b + 3]}].push_back(dur);
+                        busy += dur;
+                    }
+                    fprintf(stderr, "[mr3] k_rqi CTAs %d on %zu SMs span %.3f ms mean %.3f ms\n", nb,
+                            per_sm.size(), 1e-6 * (double)(t1 - t0), busy / std::max(nb, 1));
+                    for (auto &g : grp) {
+                        auto v = g.second;
+                        std::sort(v.begin(), v.end());
+                        fprintf(stderr, "[mr3]   %d CTAs/SM, iters %d: %zu CTAs, min %.2f med %.2f max %.2f ms\n",
+                                g.first.first, g.first.second, v.size(), v.front(), v[v.size() / 2],
+                                v.back());
+                    }
+                }
                 cudaError_t e2 = cudaGetLastError();
                 if (e2 != cudaSuccess) {
                     ctx->err = std::string(locate ? "k_rqi_locate: " : "k_rqi: ") +

@@ -18,6 +18,8 @@ import ctypes
 import torch
 import torch.distributed as dist
 
+BRK_REC = 6  # doubles per bracket record (MR3_BRK_REC in include/mr3.h)
+
 
 class _DevPtr:
     """__cuda_array_interface__ view of a library-owned device buffer."""
@@ -32,10 +34,10 @@ def wrap_device(ptr: int, n: int, device) -> torch.Tensor:
 
 
 def exchange_brackets(buf: torch.Tensor, rank: int, world: int, cap: int, group=None):
-    """All-gather equal slices of `buf` (world*cap records of 4 float64) in place."""
+    """All-gather equal slices of `buf` (world*cap records of BRK_REC float64) in place."""
     if world == 1:
         return buf
-    rec = 4 * cap
+    rec = BRK_REC * cap
     mine = buf[rank * rec:(rank + 1) * rec].clone()
     dist.all_gather_into_tensor(buf[:world * rec], mine, group=group)
     return buf
@@ -83,7 +85,7 @@ def solve_distributed(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, gro
                         ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap), ctypes.byref(cnt))
     _err(c, rc, "mr3_plan")
     if brk.value and world > 1:
-        buf = wrap_device(brk.value, world * cap.value * 4, d.device)
+        buf = wrap_device(brk.value, world * cap.value * BRK_REC, d.device)
         exchange_brackets(buf, rank, world, cap.value, group)
         torch.cuda.current_stream(d.device).synchronize()
     w = torch.zeros(max(n, 1), dtype=d.dtype, device=d.device)

@@ -87,3 +87,11 @@ def test_no_cpu_fallback_without_gpu():
     d = torch.ones(4, dtype=torch.float64)
     with pytest.raises((RuntimeError, TypeError)):
         mr3.mr3_dstemr_dd(d, torch.ones(3, dtype=torch.float64))
+
+
+def test_bracket_record_size_matches_header():
+    src = open(os.path.join(ROOT, "include", "mr3.h")).read()
+    m = re.search(r"#define\s+MR3_BRK_REC\s+(\d+)", src)
+    assert m is not None
+    from paper_1304_1864_b200.distributed import BRK_REC
+    assert int(m.group(1)) == BRK_REC

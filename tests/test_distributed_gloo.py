@@ -29,22 +29,25 @@ def _worker(rank, world, port, q):
         import oracle
         import paper_1304_1864_b200 as mr3
         import synth
+        from paper_1304_1864_b200.distributed import BRK_REC as RB
         from paper_1304_1864_b200.distributed import exchange_brackets, gather_columns
 
         p = synth.glued_wilkinson(6, 21)
         n = p.n
         cap = (n + world - 1) // world
-        buf = torch.full((world * cap * 4,), float("nan"), dtype=torch.float64)
+        buf = torch.full((world * cap * RB,), float("nan"), dtype=torch.float64)
         # this rank's static slice: brackets from the oracle's eigenvalues (stand-in for K2)
         first, cnt = rank * cap, min(cap, n - rank * cap)
         lh, ll = oracle.eigvals(p.d, p.e, np.arange(first + 1, first + cnt + 1))
-        rec = buf[rank * cap * 4:(rank * cap + cnt) * 4].view(cnt, 4)
+        rec = buf[rank * cap * RB:(rank * cap + cnt) * RB].view(cnt, RB)
         rec[:, 0] = torch.from_numpy(lh - 1e-12 * np.abs(lh))
         rec[:, 2] = torch.from_numpy(lh + 1e-12 * np.abs(lh))
         rec[:, 1] = 0
         rec[:, 3] = 0
+        rec[:, 4] = torch.from_numpy(lh)  # Newton estimate
+        rec[:, 5] = 0
         exchange_brackets(buf, rank, world, cap, None)
-        allrec = buf[:n * 4].view(n, 4).numpy()
+        allrec = buf[:n * RB].view(n, RB).numpy()
         assert np.all(np.isfinite(allrec))
         # classification (reldist >= gaptol) of the gathered brackets, identical on all ranks
         lo, hi = allrec[:, 0], allrec[:, 2]

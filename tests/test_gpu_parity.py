@@ -190,9 +190,10 @@ def test_two_phase_world_emulation_bitwise(world):
                         ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap), ctypes.byref(cnt))
         assert rc == 0
         torch.cuda.synchronize()
-        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * 4, d.device))
+        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * mr3.distributed.BRK_REC,
+                                                   d.device))
         caps.append(cap.value)
-    rec = 4 * caps[0]
+    rec = mr3.distributed.BRK_REC * caps[0]
     full = torch.cat([bufs[r][r * rec:(r + 1) * rec] for r in range(world)])
     for r in range(world):
         bufs[r][:world * rec].copy_(full)
@@ -335,8 +336,10 @@ def test_host_buffer_abi_matches_device_abi(io):
                                   lambda: synth.legendre(3000)])
 def test_root_certification_modes_agree(make):
     """Reading R8d: the binary_x root brackets widened by the definite root's relative
-    robustness bound (MR3_YCERT = 0, default) give the same eigenpairs, bit for bit, as
-    certifying every bracket with binary_y Sturm counts (MR3_YCERT = 1)."""
+    robustness bound (MR3_YCERT = 0, default) give the same eigenvalues, bit for bit, as
+    certifying every bracket with binary_y Sturm counts (MR3_YCERT = 1), and the same
+    eigenvectors up to the last bit (reading R10: the RQI of the default path starts from
+    the Newton estimate of its binary_x phase, the certified path from the midpoint)."""
     p = make()
     d = torch.from_numpy(p.d).cuda()
     e = torch.from_numpy(p.e).cuda()
@@ -349,7 +352,8 @@ def test_root_certification_modes_agree(make):
         mr3.set_param("YCERT", -1)
     assert s1["bisect_rows"] > s0["bisect_rows"]
     np.testing.assert_array_equal(w1.cpu().numpy(), w0.cpu().numpy())
-    np.testing.assert_array_equal(Z1.cpu().numpy(), Z0.cpu().numpy())
+    dz = np.abs(Z1.cpu().numpy() - Z0.cpu().numpy())
+    assert dz.max() <= 8 * 2.0**-53, dz.max()
 
 
 def _with_params(params, fn):
