@@ -313,7 +313,9 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         A.dbg_clk[4 * blockIdx.x] = gtimer_ns();
         unsigned smid;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-        A.dbg_clk[4 * blockIdx.x + 2] = smid;
+        A.dbg_clk[4 * blockIdx.x + 2] = (unsigned long long)smid |
+                                        ((unsigned long long)(cta_rmin & 0xffffff) << 8) |
+                                        ((unsigned long long)(cta_rmax & 0xffffff) << 32);
     }
 
     // output column of this eigenpair (rows of its block) and the factors for k_zscale
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
             pm = a0.x;
             ipm = a0.y;
-            e = (int)a1.x;
+            e = __double2loint(a1.x);  // exponent stored as int bits (k_node_pp)
         };
         // the PP row of kk from the staged tile (rows follow the representation rows)
         auto sppr = [&](const double *buf, int64_t t0, int64_t kk, double &pm, double &ipm,
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double2 a0 = q[0], a1 = q[1];
             pm = a0.x;
             ipm = a0.y;
-            e = (int)a1.x;
+            e = __double2loint(a1.x);  // exponent stored as int bits (k_node_pp)
         };
         // value * 2^k (k <= 1023; results below the normal range flush to zero)
         auto pow2mul = [](double v, int k) -> double {
@@ -731,7 +733,8 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     }
     if (A.dbg_clk) {
         atomicMax(&A.dbg_clk[4 * blockIdx.x + 1], gtimer_ns());
-        atomicMax(&A.dbg_clk[4 * blockIdx.x + 3], (unsigned long long)iters);
+        atomicMax(&A.dbg_clk[4 * blockIdx.x + 3],
+                  (unsigned long long)iters | ((unsigned long long)(tid == 0 ? id : 0) << 8));
     }
     if (!A.jobz_v) {
         if (active && rows) atomicAdd(&A.st->rqi_rows, rows);

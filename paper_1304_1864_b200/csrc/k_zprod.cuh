@@ -22,7 +22,7 @@
 
 namespace mr3 {
 
-// per row of a node: {PPm, IPPm, E, (two floats: -1023 -+ log2|PP_k|)}: PP_k = PPm 2^E,
+// per row of a node: {PPm, IPPm, E (int bits), (two floats: -1023 -+ log2|PP_k|)}: PP_k = PPm 2^E,
 // 1/PP_k = IPPm 2^-E.
 // The mantissas are products of the representation's ld in pair arithmetic, rounded
 // once: z components come out to binary64 accuracy (the output precision).
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) k_node_pp(NodeInfo *nodes, int first, dou
         double *o = pp + j * PP_STRIDE;
         o[0] = hi(pm);
         o[1] = hi(ipm);
-        o[2] = (double)pe;
+        o[2] = __hiloint2double(0, pe);  // E as int bits (no F2I on the readers' path)
         {  // {-1023 - log2|PP_j|, -1023 + log2|PP_j|} as floats (k_rqi_locate)
             const float l = (float)(log2(fabs(hi(pm))) + (double)pe);
             float2 *f = reinterpret_cast<float2 *>(o + 3);

@@ -1091,13 +1091,26 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                         t1 = std::max(t1, hc[4 * b + 1]);
                     }
                     std::map<unsigned long long, int> per_sm;
-                    for (int b = 0; b < nb; b++) per_sm[hc[4 * b + 2]]++;
+                    for (int b = 0; b < nb; b++) per_sm[hc[4 * b + 2] & 0xff]++;
+                    {  // the slowest CTAs
+                        std::vector<std::pair<double, int>> dv;
+                        for (int b = 0; b < nb; b++)
+                            dv.push_back({1e-6 * (double)(hc[4 * b + 1] - hc[4 * b]), b});
+                        std::sort(dv.rbegin(), dv.rend());
+                        for (int q = 0; q < std::min(nb, 12); q++) {
+                            const int b = dv[q].second;
+                            const unsigned long long w2 = hc[4 * b + 2], w3 = hc[4 * b + 3];
+                            fprintf(stderr, "[mr3]   slow CTA %d: %.2f ms sm %llu (%d CTAs) twist %llu..%llu iters %llu first item %llu\n",
+                                    b, dv[q].first, w2 & 0xff, per_sm[w2 & 0xff], (w2 >> 8) & 0xffffff,
+                                    (w2 >> 32) & 0xffffff, w3 & 0xff, w3 >> 8);
+                        }
+                    }
                     // duration histogram (2 ms bins) split by CTAs on the SM and max iterations
                     std::map<std::pair<int, int>, std::vector<double>> grp;
                     double busy = 0;
                     for (int b = 0; b < nb; b++) {
                         const double dur = 1e-6 * (double)(hc[4 * b + 1] - hc[4 * b]);
-                        grp[{per_sm[hc[4 * b + 2]], (int)hc[4 * b + 3]}].push_back(dur);
+                        grp[{per_sm[hc[4 * b + 2] & 0xff], (int)(hc[4 * b + 3] & 0xff)}].push_back(dur);
                         busy += dur;
                     }
                     fprintf(stderr, "[mr3] k_rqi CTAs %d on %zu SMs span %.3f ms mean %.3f ms\n", nb,
