@@ -92,8 +92,9 @@ enum mr3_param {
                           counts; 0: rigorous widening by the definite root's relative
                           robustness bound instead (R8d); 0 */
     MR3_NEWTON = 15,   /* Newton passes per item before the many-lane multisection tail; 6 */
-    MR3_TWISTW = 16,   /* twist weight slope w: r = argmin |gamma_k| (1 + w |2k - n| / n); 3 */
-    MR3_NPARAM = 17
+    MR3_TWISTW = 16,   /* twist weight slope w: r = argmin |gamma_k| (1 + w |2k - n| / n); 100 */
+    MR3_SPLIT = 17,    /* 1: RQI iterations >= 3 as split (chunked) passes, reading R9d; 1 */
+    MR3_NPARAM = 18
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

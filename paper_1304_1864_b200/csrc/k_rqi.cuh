@@ -66,6 +66,7 @@ struct RqiArgs {
                         // by root_widen * n * |lambda| (relative robustness of the root, R8d)
     int maxit;
     int jobz_v;
+    int split;  // RQI iterations >= 3 as split passes (R9d)
     void *w;          // eigenvalue output (global positions)
     void *Z;          // eigenvector output (columns col - zcol0)
     int64_t ldz, zcol0;
@@ -83,6 +84,23 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 }
 
 __device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
+
+// sign(x) != sign(y) as 0/1 (the inertia of a projective step)
+template <class R>
+__device__ __forceinline__ int sgn_ne_R(R x, R y) {
+    return (int)((unsigned)(__double2hiint(hi(x)) ^ __double2hiint(hi(y))) >> 31);
+}
+// v * 2^k (k <= 1023; results below the normal range flush to zero)
+__device__ __forceinline__ double pow2mul_d(double v, int k) {
+    return k < -1022 ? 0.0 : v * __hiloint2double((k + 1023) << 20, 0);
+}
+// compensated (Kahan) sum of squares: sum += x^2
+__device__ __forceinline__ void kahan_sq(double x, double &sum, double &comp) {
+    const double y = fma(x, x, -comp);
+    const double t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+}
 
 // ss += x^2 in pair arithmetic (two-prod + two-sum)
 __device__ __forceinline__ void accum_sq(double x, double &sh, double &sl) {
@@ -641,6 +659,329 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         return negc;
     };
 
+    // ---- split pass (third and later RQI iterations): one eigenpair, the whole CTA ----
+    // By then at most a few eigenpairs of the CTA are still iterating, and a CTA-wide
+    // serial pass would cost a full n-row chain for them.  The projective transforms are
+    // linear in (p, q): F row k maps (p, q) -> (lld_k p - lam (d_k q + p), d_k q + p) and
+    // B row k -> (d_{k-1} p - lam (lld_{k-1} q + p), lld_{k-1} q + p).  The F rows [0, r)
+    // and B rows (r, n) are cut into chunks (one per thread, proportional to length);
+    // each thread forms its chunk's 2x2 transfer matrix (two basis solutions, pair
+    // arithmetic), one thread per direction chains them into the chunk start states,
+    // and every thread re-runs the true recurrence from its start (z in product form,
+    // compensated norms, inertia).  The re-run end state of a chunk must equal the next
+    // chunk's start to 2^-84 relative; otherwise the pass is redone serially.  Chain:
+    // about 3 n / 128 rows instead of n / 2.
+    struct SplitIO {
+        R lam, gr;
+        int64_t r, zoff;
+        int erefF, erefB, wz, negc, bad, eyr, exr;
+        double yr, xr, sF, cF, sB, cB, jF, jB;
+    };
+    __shared__ SplitIO sio;
+    __shared__ int s_need[RQ_TPB];
+    __shared__ int s_dbg_rel;  // (MR3_DEBUG) worst continuity of the last split pass, log2 * 16
+    __shared__ double s_red[2 * (RQ_TPB / 32)][2];
+    __shared__ int s_redi[RQ_TPB / 32][2];
+    __shared__ double s_redj[RQ_TPB / 32][2];
+    auto rescale_pq2 = [](R &x, R &y, int &E) {
+        const unsigned ex = (unsigned)__double2hiint(hi(x)) & 0x7ff00000u;
+        const unsigned ey = (unsigned)__double2hiint(hi(y)) & 0x7ff00000u;
+        const unsigned em = ex > ey ? ex : ey;
+        if (em == 0x7ff00000u || em == 0u) return;
+        const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+        x = scale_pow2(x, sc);
+        y = scale_pow2(y, sc);
+        E += (int)(em >> 20) - 1023;
+    };
+    auto rescale_4 = [](R &a1, R &a2, R &a3, R &a4, int &E) {
+        unsigned em = (unsigned)__double2hiint(hi(a1)) & 0x7ff00000u;
+        unsigned t = (unsigned)__double2hiint(hi(a2)) & 0x7ff00000u;
+        em = t > em ? t : em;
+        t = (unsigned)__double2hiint(hi(a3)) & 0x7ff00000u;
+        em = t > em ? t : em;
+        t = (unsigned)__double2hiint(hi(a4)) & 0x7ff00000u;
+        em = t > em ? t : em;
+        if (em == 0x7ff00000u || em == 0u) return;
+        const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
+        a1 = scale_pow2(a1, sc);
+        a2 = scale_pow2(a2, sc);
+        a3 = scale_pow2(a3, sc);
+        a4 = scale_pow2(a4, sc);
+        E += (int)(em >> 20) - 1023;
+    };
+    auto split_pass = [&]() {  // collective; inputs and outputs in sio
+        const R lam_s = sio.lam, mlam = neg(sio.lam);
+        const int64_t rs = sio.r;
+        OutT *zc = sio.wz ? reinterpret_cast<OutT *>(A.Z) + sio.zoff : nullptr;
+        const int64_t LF = rs, LB = n - 1 - rs;
+        int tF = (int)((RQ_TPB * LF + (LF + LB) / 2) / (LF + LB));
+        if (LF > 0 && tF < 1) tF = 1;
+        if (LB > 0 && tF > RQ_TPB - 1) tF = RQ_TPB - 1;
+        const int tB = RQ_TPB - tF;
+        const bool isF = tid < tF;
+        const int c = isF ? tid : tid - tF, nc = isF ? tF : tB;
+        // F: rows k0 .. k1-1 ascending; B: rows k0 .. k1+1 descending
+        const int64_t k0 = isF ? LF * c / nc : n - 1 - LB * c / nc;
+        const int64_t k1 = isF ? LF * (c + 1) / nc : n - 1 - LB * (c + 1) / nc;
+        const int64_t len = isF ? k1 - k0 : k0 - k1;
+        R *Mx = reinterpret_cast<R *>(sstage);  // 4 per thread: u = M (1, 0), v = M (0, 1)
+        R *Sx = Mx + 4 * RQ_TPB;                // 2 per thread: start state (p, q)
+        int *ME = reinterpret_cast<int *>(Sx + 2 * RQ_TPB);
+        int *SE = ME + RQ_TPB;
+        // phase 1: transfer matrix of the chunk
+        {
+            R up = mk<R>(1.0), uq = mk<R>(0.0), vp = mk<R>(0.0), vq = mk<R>(1.0);
+            int EM = 0;
+#pragma unroll 1
+            for (int64_t j0 = 0; j0 < len; j0 += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    if (j0 + j < len) {
+                        const int64_t kk = isF ? k0 + j0 + j : k0 - j0 - j;
+                        const Row4<R> rw = load_row4<R>(nd.rep, isF ? kk : kk - 1);
+                        const R m1 = isF ? rw.d : rw.lld, m2 = isF ? rw.lld : rw.d;
+                        const R U = fma_dd(m1, uq, up), V = fma_dd(m1, vq, vp);
+                        up = fma_dd(mlam, U, mul(m2, up));
+                        vp = fma_dd(mlam, V, mul(m2, vp));
+                        uq = U;
+                        vq = V;
+                    }
+                }
+                rescale_4(up, uq, vp, vq, EM);
+            }
+            Mx[4 * tid] = up;
+            Mx[4 * tid + 1] = uq;
+            Mx[4 * tid + 2] = vp;
+            Mx[4 * tid + 3] = vq;
+            ME[tid] = EM;
+        }
+        __syncthreads();
+        // phase 2: chunk start states, chained by one thread per direction
+        if ((tid == 0 && tF > 0) || (tid == tF && tB > 0)) {
+            R p = isF ? mlam : sub(load_row4<R>(nd.rep, n - 1).d, lam_s), q = mk<R>(1.0);
+            int E = 0;
+#pragma unroll 1
+            for (int j = 0; j < nc; j++) {
+                const int t = tid + j;
+                Sx[2 * t] = p;
+                Sx[2 * t + 1] = q;
+                SE[t] = E;
+                const R np = add(mul(p, Mx[4 * t]), mul(q, Mx[4 * t + 2]));
+                const R nq = add(mul(p, Mx[4 * t + 1]), mul(q, Mx[4 * t + 3]));
+                p = np;
+                q = nq;
+                E += ME[t];
+                rescale_pq2(p, q, E);
+            }
+        }
+        __syncthreads();
+        // phase 3: the true recurrence from the start state
+        R p = Sx[2 * tid], q = Sx[2 * tid + 1];
+        int E = SE[tid];
+        double s = 0.0, cmp = 0.0;
+        int ng = 0;
+        double zlast = 0.0, rnorm = 0.0;  // |z| and row norm at the chunk's last row
+        const int eref = isF ? sio.erefF : sio.erefB;
+#pragma unroll 1
+        for (int64_t j0 = 0; j0 < len; j0 += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (j0 + j < len) {
+                    const int64_t kk = isF ? k0 + j0 + j : k0 - j0 - j;
+                    const Row4<R> rw = load_row4<R>(nd.rep, isF ? kk : kk - 1);
+                    double pm = 1.0, ipm = 1.0;
+                    int e = 0;
+                    if (nd.pp != nullptr) {
+                        const double2 *qq = reinterpret_cast<const double2 *>(nd.pp + kk * PP_STRIDE);
+                        const double2 a0 = __ldg(qq), a1 = __ldg(qq + 1);
+                        pm = a0.x;
+                        ipm = a0.y;
+                        e = __double2loint(a1.x);
+                    }
+                    // F: y_kk = qF / PP_kk; B: x_kk = QB PP_kk (written scaled by 2^-eref)
+                    const double zv = isF ? pow2mul_d(hi(q) * ipm, E - e - eref)
+                                          : pow2mul_d(hi(q) * pm, E + e - eref);
+                    const OutT zo = (OutT)zv;
+                    if (zc != nullptr) zc[kk] = zo;
+                    kahan_sq((double)zo, s, cmp);
+                    zlast = fabs(zv);
+                    rnorm = fabs(hi(rw.d)) + fabs(hi(rw.lld)) + 2.0 * fabs(hi(rw.ld)) +
+                            fabs(hi(lam_s));
+                    const R m1 = isF ? rw.d : rw.lld, m2 = isF ? rw.lld : rw.d;
+                    const R D = fma_dd(m1, q, p);
+                    ng += sgn_ne_R<R>(D, q);
+                    p = fma_dd(mlam, D, mul(m2, p));
+                    q = D;
+                }
+            }
+            rescale_pq2(p, q, E);
+        }
+        // continuity with the next chunk's start: a relative jump delta of the state at a
+        // chunk boundary perturbs the recurrence there, i.e. adds about delta |z_k| ||row_k||
+        // to the residual of the (scaled) vector; summed in squares per direction and
+        // checked against the stopping tolerance by the owner
+        int bad = 0;
+        double jres = 0.0;
+        if (c + 1 < nc) {
+            const int t = tid + 1;
+            const int dE = SE[t] - E;
+            if (dE > 60 || dE < -60) {
+                bad = 1;
+            } else {
+                const double sc = __hiloint2double((dE + 1023) << 20, 0);
+                const R p2 = scale_pow2(Sx[2 * t], sc), q2 = scale_pow2(Sx[2 * t + 1], sc);
+                const double mag = fmax(fabs(hi(p)), fabs(hi(q)));
+                const double dif = fmax(fabs(hi(sub(p, p2))), fabs(hi(sub(q, q2))));
+                const double rel = dif / mag;
+                bad = !(rel <= 0x1p-60) ? 1 : 0;  // (beyond: the chunk chain is unusable)
+                const double j1 = rel * fmax(zlast, 1e-300) * rnorm;
+                jres = j1 * j1;
+                if (A.dbg_trace) atomicMax(&s_dbg_rel, (int)(log2(dif / mag + 1e-300) * 16.0) + 32768);
+            }
+        } else {  // last chunk of its direction: the state at r
+            if (isF) {
+                sio.gr = div(p, q);  // s_r (F part of gamma_r)
+                sio.yr = hi(q);
+                sio.eyr = E;
+            } else {
+                sio.lam = div(p, q);  // p_r (B part); lam is no longer needed
+                sio.xr = hi(q);
+                sio.exr = E;
+            }
+        }
+        // reductions: Kahan sums per direction, inertia, continuity
+        const int warp = tid >> 5, lane = tid & 31;
+        double sFv = isF ? s : 0.0, cFv = isF ? cmp : 0.0, sBv = isF ? 0.0 : s, cBv = isF ? 0.0 : cmp;
+        double jF = isF ? jres : 0.0, jB = isF ? 0.0 : jres;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sFv += __shfl_down_sync(0xffffffffu, sFv, o);
+            cFv += __shfl_down_sync(0xffffffffu, cFv, o);
+            sBv += __shfl_down_sync(0xffffffffu, sBv, o);
+            cBv += __shfl_down_sync(0xffffffffu, cBv, o);
+            ng += __shfl_down_sync(0xffffffffu, ng, o);
+            bad += __shfl_down_sync(0xffffffffu, bad, o);
+            jF += __shfl_down_sync(0xffffffffu, jF, o);
+            jB += __shfl_down_sync(0xffffffffu, jB, o);
+        }
+        if (lane == 0) {
+            s_red[2 * warp][0] = sFv;
+            s_red[2 * warp][1] = cFv;
+            s_red[2 * warp + 1][0] = sBv;
+            s_red[2 * warp + 1][1] = cBv;
+            s_redi[warp][0] = ng;
+            s_redi[warp][1] = bad;
+            s_redj[warp][0] = jF;
+            s_redj[warp][1] = jB;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+            int i1 = 0, i2 = 0;
+            for (int w = 0; w < RQ_TPB / 32; w++) {
+                a1 += s_red[2 * w][0];
+                a2 += s_red[2 * w][1];
+                a3 += s_red[2 * w + 1][0];
+                a4 += s_red[2 * w + 1][1];
+                i1 += s_redi[w][0];
+                i2 += s_redi[w][1];
+                sio.jF = (w == 0 ? 0.0 : sio.jF) + s_redj[w][0];
+                sio.jB = (w == 0 ? 0.0 : sio.jB) + s_redj[w][1];
+            }
+            sio.sF = a1;
+            sio.cF = a2;
+            sio.sB = a3;
+            sio.cB = a4;
+            sio.negc = i1;
+            sio.bad = i2;
+            if (tF == 0) {  // r = 0: no F rows, s_0 = -lam, qF = 1
+                sio.gr = mlam;
+                sio.yr = 1.0;
+                sio.eyr = 0;
+            }
+            if (tB == 0) {  // r = n - 1: p_{n-1} = d_{n-1} - lam, QB = 1
+                sio.lam = sub(load_row4<R>(nd.rep, n - 1).d, lam_s);
+                sio.xr = 1.0;
+                sio.exr = 0;
+            }
+        }
+        __syncthreads();
+    };
+    // all eigenpairs of the CTA with `need`, one split pass each; returns the inertia
+    auto split_all = [&](bool need, bool store) -> int {
+        if (need) zwritten = false;
+        s_need[tid] = need ? 1 : 0;
+        __syncthreads();
+        int myc = 0;
+        bool redo = false;
+#pragma unroll 1
+        for (int j = 0; j < RQ_TPB; j++) {
+            if (!s_need[j]) continue;  // (uniform)
+            const bool wzj = store && zcol != nullptr;
+            if (tid == j) {
+                sio.lam = lam;
+                sio.r = r;
+                sio.erefF = erefF;
+                sio.erefB = erefB;
+                sio.wz = wzj ? 1 : 0;
+                sio.zoff = wzj ? (col0 - A.zcol0) * A.ldz + nd.row0 : 0;
+            }
+            if (tid == 0) s_dbg_rel = 0;
+            __syncthreads();
+            split_pass();
+            if (tid == j && A.dbg_trace) A.dbg_trace[8 * (int64_t)id + 7] = (s_dbg_rel - 32768) / 16.0;
+            if (tid == j) {
+                if (sio.bad) {
+                    redo = true;
+                } else {
+                    const R sr = sio.gr, pr = sio.lam;
+                    gr = add(add(sr, pr), lam);
+                    myc = sio.negc + (is_neg(gr) ? 1 : 0);
+                    rows += n;
+                    double pm = 1.0, ipm = 1.0;
+                    int e = 0;
+                    if (nd.pp != nullptr) {
+                        const double2 *qq = reinterpret_cast<const double2 *>(nd.pp + r * PP_STRIDE);
+                        pm = qq[0].x;
+                        ipm = qq[0].y;
+                        e = __double2loint(qq[1].x);
+                    }
+                    const double yr = sio.yr * ipm, xr = sio.xr * pm;
+                    const int eyr = sio.eyr - e, exr = sio.exr + e;
+                    double sF = sio.sF, cF_ = sio.cF;
+                    const OutT zo = (OutT)pow2mul_d(yr, eyr - erefF);
+                    kahan_sq((double)zo, sF, cF_);
+                    const double fF = ldexp(1.0, erefF - eyr) / yr;
+                    const double fB = ldexp(1.0, erefB - exr) / xr;
+                    nz2 = fF * fF * (sF - cF_) + fB * fB * (sio.sB - sio.cB);
+                    // residual added by the chunk-boundary jumps (normalised vector)
+                    const double jr = sqrt(fF * fF * sio.jF + fB * fB * sio.jB) / sqrt(nz2);
+                    if (!(jr <= 0.125 * tol)) redo = true;
+                    if (wzj && !redo) {
+                        zcol[r] = zo;
+                        zinfo.cF = fF;
+                        zinfo.cB = fB;
+                        zinfo.ss = nz2;
+                        zwritten = true;
+                    }
+                    if (!redo) {
+                        erefF = eyr + expo_of(yr);
+                        erefB = exr + expo_of(xr);
+                    } else {
+                        rows -= n;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // a chunk chain that lost accuracy: the serial pass for those eigenpairs
+        if (__syncthreads_or(redo)) {
+            const int c2 = twisted_fixed(redo, store);
+            if (redo) myc = c2;
+        }
+        return myc;
+    };
+
 #pragma unroll 1
     for (iters = 1; iters <= A.maxit; iters++) {
         // an eigenpair that converged in the first (non-storing) pass joins the next
@@ -649,7 +990,9 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;
         const bool need = !done || store_only;
         if (!__syncthreads_or(need)) break;
-        int c = twisted_fixed(need, A.jobz_v && iters >= 2);
+        const int c = (iters <= 2 || n < 4 * RQ_TPB || !A.split)
+                          ? twisted_fixed(need, A.jobz_v && iters >= 2)
+                                                     : split_all(need, A.jobz_v && iters >= 2);
         if (store_only) zfinal = zwritten;
         if (need && !store_only) {
             if (c >= k) {
@@ -999,31 +1342,39 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     float best = -INFINITY;
     int64_t rr = n / 2;  // (kept if every score is -inf: no usable twist information)
     // tile i is reached first by F iff 2 i < ntile - 1, by B iff 2 i > ntile - 1, by both
-    // at the same step iff 2 i == ntile - 1 (F's rows of that tile are run first then)
-    // First half of the sweep (F below the middle tile, B above it): each stream keeps
-    // per tile the row where its half-vector is largest (log2|y_k| = log2|theta_k| -
-    // log2|PP_k|, log2|x_k| = log2|phi_k| + log2|PP_k|).  Second half: each stream
-    // captures its own value at the other stream's candidate row of the tile and scores
-    // it once per tile: log2|gamma_k|^-1 + const = log2|y_k| + log2|x_k| - log2 w_k.
-    // The mode is uniform over the CTA at every step (a function of the tile only).
+    // at the same step iff 2 i == ntile - 1 (F's rows of that tile are run first then).
+    // The stream that reaches a row first stores its log2 half-vector magnitude
+    // (log2|y_k| = log2|theta_k| - log2|PP_k| for F, log2|x_k| = log2|phi_k| + log2|PP_k|
+    // for B) as int16 in 1/16 units relative to the tile's first value (per tile, float);
+    // the other stream adds its own at the same row: log2|gamma_k|^-1 + const =
+    // log2|y_k| + log2|x_k|, minus log2 w (the tile's).  Every row is scored (localised
+    // eigenvectors peak within a few rows).  The mode is uniform over the CTA at every step.
+    // [tile][slot][32 rows] int16: one 64-byte record per tile and eigenpair (4 x 16 B)
+    uint4 *hist = reinterpret_cast<uint4 *>(A.ck_s);
     float EFf = 0.0f, EBf = 0.0f;  // EF, EB as float (log2 bookkeeping)
-    // one row of F / B; MODE 0: keep the candidate (cv, ci); MODE 1: capture the state at
-    // row ci (into qc, ec); GUARD: rows may reach n
-    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, float &cv, int &ci,
-                    double &qc, float &ec) {
+    // MODE 0: store (into h); MODE 1: score against h; GUARD: rows may reach n
+    auto put16 = [](uint32_t (&h)[16], int i, float v) {
+        const unsigned u = (unsigned)(unsigned short)(short)fminf(fmaxf(rintf(v), -32767.0f), 32767.0f);
+        h[i >> 1] = (i & 1) ? ((h[i >> 1] & 0x0000ffffu) | (u << 16)) : ((h[i >> 1] & 0xffff0000u) | u);
+    };
+    auto get16 = [](const uint32_t (&h)[16], int i) -> float {
+        return (float)(short)((i & 1) ? (h[i >> 1] >> 16) : (h[i >> 1] & 0xffffu));
+    };
+    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, float &ref,
+                    float base, uint32_t (&h)[16]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
+        const float l = fmaf((float)(__double2hiint(qf) & 0x7fffffff), 0x1p-20f,
+                             EFf + lppm(bA, tr));  // log2|y_kk|
         if (MODE == 0) {
-            const float lt = fmaf((float)(__double2hiint(qf) & 0x7fffffff), 0x1p-20f,
-                                  EFf + lppm(bA, tr));  // log2|y_kk|
-            const bool up = lt > cv;
-            cv = up ? lt : cv;
-            ci = up ? kk : ci;
+            ref = ref == -INFINITY ? l : ref;
+            put16(h, tr, (l - ref) * 16.0f);
         } else {
-            const bool at = kk == ci;
-            qc = at ? qf : qc;
-            ec = at ? EFf : ec;
+            const float sc = l + fmaf(get16(h, tr), 0.0625f, base);
+            const bool up = sc > best;
+            best = up ? sc : best;
+            rr = up ? kk : rr;
         }
         if (!GUARD || kk < n - 1) {
             const double2 rw = *reinterpret_cast<const double2 *>(bA + (tr + RQ_HALO) * 2);
@@ -1032,21 +1383,21 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             qf = D;
         }
     };
-    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, float &cv, int &ci,
-                    double &qc, float &ec) {
+    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, float &ref,
+                    float base, uint32_t (&h)[16]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
+        const float l = fmaf((float)(__double2hiint(qb) & 0x7fffffff), 0x1p-20f,
+                             EBf + lppp(bD, tr));  // log2|x_kk|
         if (MODE == 0) {
-            const float lp = fmaf((float)(__double2hiint(qb) & 0x7fffffff), 0x1p-20f,
-                                  EBf + lppp(bD, tr));  // log2|x_kk|
-            const bool up = lp > cv;
-            cv = up ? lp : cv;
-            ci = up ? kk : ci;
+            ref = ref == -INFINITY ? l : ref;
+            put16(h, tr, (l - ref) * 16.0f);
         } else {
-            const bool at = kk == ci;
-            qc = at ? qb : qc;
-            ec = at ? EBf : ec;
+            const float sc = l + fmaf(get16(h, tr), 0.0625f, base);
+            const bool up = sc > best;
+            best = up ? sc : best;
+            rr = up ? kk : rr;
         }
         if (kk > 0) {
             const double2 rw = *reinterpret_cast<const double2 *>(bD + (tr - 1 + RQ_HALO) * 2);
@@ -1063,18 +1414,36 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     using M1 = std::integral_constant<int, 1>;
     using G0 = std::integral_constant<bool, false>;
     using G1 = std::integral_constant<bool, true>;
-    // both streams over one step's tiles, rows interleaved
+    auto hload = [&](int t, uint32_t (&h)[16]) {
+        const uint4 *src = hist + ((int64_t)t * A.S + slot) * 4;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint4 v = src[u];
+            h[4 * u] = v.x;
+            h[4 * u + 1] = v.y;
+            h[4 * u + 2] = v.z;
+            h[4 * u + 3] = v.w;
+        }
+    };
+    auto hstore = [&](int t, const uint32_t (&h)[16]) {
+        uint4 *dst = hist + ((int64_t)t * A.S + slot) * 4;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            dst[u] = make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+    };
+    // both streams over one step's tiles, rows interleaved (fully unrolled: the packed
+    // int16 rows live in registers)
     auto step = [&](auto mode, auto guard, const double *bA, int64_t tA, const double *bD,
-                    int64_t tD, float &cvf, int &cif, double &qcf, float &ecf, float &cvb, int &cib,
-                    double &qcb, float &ecb) {
-#pragma unroll 1
+                    int64_t tD, float &reff, float &refb, float basef, float baseb,
+                    uint32_t (&hf)[16], uint32_t (&hb)[16]) {
+#pragma unroll
         for (int q = 0; q < RQ_TR / RQ_C; q++) {
             const int oF = q * RQ_C, oB = (RQ_TR / RQ_C - 1 - q) * RQ_C;
 #pragma unroll
             for (int j = 0; j < RQ_C; j++) {
-                frow(mode, guard, bA, oF + j, (int)tA + oF + j, cvf, cif, qcf, ecf);
-                brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, cvb, cib,
-                     qcb, ecb);
+                frow(mode, guard, bA, oF + j, (int)tA + oF + j, reff, basef, hf);
+                brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, refb,
+                     baseb, hb);
             }
             rescale2f(pf, qf, EF, EFf);
             rescale2f(pb, qb, EB, EBf);
@@ -1086,74 +1455,48 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             if (!active) return;
             const int iA = (int)(tA / RQ_TR), iD = (int)(tD / RQ_TR);
             const bool guard = tA + RQ_TR > n - 1 || tD + RQ_TR > n - 1 || tD == 0;
-            float cvf = -INFINITY, cvb = -INFINITY, ecf = 0.0f, ecb = 0.0f;
-            int cif = -1, cib = -1;
-            double qcf = 0.0, qcb = 0.0;
-            if (2 * iA < ntile - 1) {  // first half: keep candidates
+            float reff = -INFINITY, refb = -INFINITY;
+            uint32_t hf[16], hb[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) hf[u] = hb[u] = 0u;
+            if (2 * iA < ntile - 1) {  // first half: store
                 if (guard)
-                    step(M0{}, G1{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+                    step(M0{}, G1{}, bA, tA, bD, tD, reff, refb, 0.0f, 0.0f, hf, hb);
                 else
-                    step(M0{}, G0{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
-                cand[(int64_t)iA * A.S + slot] = make_float2(cvf, __int_as_float(cif));
-                cand[(int64_t)iD * A.S + slot] = make_float2(cvb, __int_as_float(cib));
+                    step(M0{}, G0{}, bA, tA, bD, tD, reff, refb, 0.0f, 0.0f, hf, hb);
+                hstore(iA, hf);
+                hstore(iD, hb);
+                cand[(int64_t)iA * A.S + slot] = make_float2(reff, 0.0f);
+                cand[(int64_t)iD * A.S + slot] = make_float2(refb, 0.0f);
                 return;
             }
-            if (2 * iA == ntile - 1) {  // middle tile (odd ntile): F keeps, then B scores
-#pragma unroll 1
+            if (2 * iA == ntile - 1) {  // middle tile (odd ntile): F stores, then B scores
+#pragma unroll
                 for (int q = 0; q < RQ_TR / RQ_C; q++) {
 #pragma unroll
                     for (int j = 0; j < RQ_C; j++)
-                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, cvf, cif, qcf,
-                             ecf);
+                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, reff, 0.0f, hf);
                     rescale2f(pf, qf, EF, EFf);
                 }
-                cib = cif;
-#pragma unroll 1
+                const float baseb = reff - logw(tD + RQ_TR / 2);
+#pragma unroll
                 for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
 #pragma unroll
                     for (int j = RQ_C - 1; j >= 0; j--)
-                        brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, cvb, cib, qcb,
-                             ecb);
+                        brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, refb, baseb, hf);
                     rescale2f(pb, qb, EB, EBf);
-                }
-                if (cib >= 0) {  // log2|y| (F's candidate) + log2|x| at that row
-                    const float lx = fmaf((float)(__double2hiint(qcb) & 0x7fffffff), 0x1p-20f,
-                                          ecb + lppp(bD, cib - (int)tD));
-                    const float sc = cvf + lx - logw(cib);
-                    if (sc > best) {
-                        best = sc;
-                        rr = cib;
-                    }
                 }
                 return;
             }
-            // second half: capture the values at the other stream's candidate rows
-            const float2 oF = cand[(int64_t)iA * A.S + slot];  // B's candidate of F's tile
-            const float2 oB = cand[(int64_t)iD * A.S + slot];  // F's candidate of B's tile
-            cif = __float_as_int(oF.y);
-            cib = __float_as_int(oB.y);
+            // second half: score every row against the other stream's stored value
+            hload(iA, hf);
+            hload(iD, hb);
+            const float basef = cand[(int64_t)iA * A.S + slot].x - logw(tA + RQ_TR / 2);
+            const float baseb = cand[(int64_t)iD * A.S + slot].x - logw(tD + RQ_TR / 2);
             if (guard)
-                step(M1{}, G1{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
+                step(M1{}, G1{}, bA, tA, bD, tD, reff, refb, basef, baseb, hf, hb);
             else
-                step(M1{}, G0{}, bA, tA, bD, tD, cvf, cif, qcf, ecf, cvb, cib, qcb, ecb);
-            if (cif >= 0) {  // log2|y| at F's row + B's stored log2|x|
-                const float ly = fmaf((float)(__double2hiint(qcf) & 0x7fffffff), 0x1p-20f,
-                                      ecf + lppm(bA, cif - (int)tA));
-                const float sc = ly + oF.x - logw(cif);
-                if (sc > best) {
-                    best = sc;
-                    rr = cif;
-                }
-            }
-            if (cib >= 0) {
-                const float lx = fmaf((float)(__double2hiint(qcb) & 0x7fffffff), 0x1p-20f,
-                                      ecb + lppp(bD, cib - (int)tD));
-                const float sc = oB.x + lx - logw(cib);
-                if (sc > best) {
-                    best = sc;
-                    rr = cib;
-                }
-            }
+                step(M1{}, G0{}, bA, tA, bD, tD, reff, refb, basef, baseb, hf, hb);
         },
         nd.pp);
     // F's candidates (tiles reached by F first) scored against B: B evaluated those in

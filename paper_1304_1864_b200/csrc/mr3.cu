@@ -97,9 +97,9 @@ static void hsync_note(mr3_ctx ctx, const char *where) {
 }
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 3.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 3.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0},
 };
 
 #define CK(call)                                                                  \
@@ -1047,6 +1047,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.gaptol = gaptol;
                 A.root_widen = ctx->root_widen;
                 A.twist_w = P[MR3_TWISTW];
+                A.split = P[MR3_SPLIT] != 0 ? 1 : 0;
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
                 A.w = w;
@@ -1312,9 +1313,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             if (itv[i] >= 4 && tr[5] != 0.0) {
                 fprintf(stderr,
                         "  item %d iters %d lam %.17g lgap %.3g rgap %.3g | x0 %g gap %.3g r %g "
-                        "res/tol %.3g %.3g %.3g %.3g\n",
+                        "res/tol %.3g %.3g %.3g %.3g | split log2 rel %.1f\n",
                         i, itv[i], hi_of(lam[i]), lg[i], rg[i], tr[0], tr[1], tr[2], tr[3], tr[4],
-                        tr[5], tr[6]);
+                        tr[5], tr[6], tr[7]);
                 shown++;
             }
         }
