@@ -370,10 +370,23 @@ def _with_params(params, fn):
             mr3.set_param(k, -1)
 
 
+def test_default_needs_no_rqi_fallback():
+    """The located twists and RQI starts converge for representative matrices without the
+    bisection fallback (P:L720-L727 keep it for the rare failures): a regression guard for
+    the twist location (R9b) -- a poor twist leaves |gamma_r| large at every iteration."""
+    for p in (synth.random_uniform(900, 11), synth.glued_wilkinson(12, 21), synth.legendre(3000),
+              synth.one_two_one(700)):
+        _, _, st = run(p)
+        assert st["rqi_fallbacks"] == 0, (p.name, st["rqi_fallbacks"])
+
+
 @pytest.mark.parametrize("params", [
     {"MAX_RQI": 1},            # every singleton takes the bisection fallback + sweep-form z
     {"REFINE": 1e12},          # all starts refined: many converge in the first (non-storing)
-                               # pass, whose z then comes from an extra storing pass
+                               # pass and join the second as store-only
+    {"KRS": 1e-4},             # tighter stopping: third and later iterations, as split passes
+    {"KRS": 1e-4, "SPLIT": 0},  # the same iterations as serial passes
+    {"TWISTW": 0},             # unweighted argmin twist
     {"NEWTON": 1},             # almost every item through the many-lane multisection tail
     {"XPTS": 1},               # plain bisection in the binary_x phase
     {"XPTS": 2},               # two points per lane
