@@ -171,9 +171,11 @@ __device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, boo
 // scale-free).  Six FP64 instructions per row; the derivative chain runs beside the
 // value chain.
 __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, bool need, double x,
-                                             double pivmin, int &cnt, double &ratio) {
+                                             double pivmin, int &cnt, double &ratio, double &f2) {
     const int64_t n = nd.n;
-    double p = -x, q = 1.0, pd = -1.0, qd = 0.0;
+    // (p, q) and their first and second x-derivatives: f = det(M_x - x I) (scaled) is the
+    // last D, f' and f'' the last D' and D''
+    double p = -x, q = 1.0, pd = -1.0, qd = 0.0, pdd = 0.0, qdd = 0.0;
     unsigned c = 0;
     bool bad = false;
     tile_pass(
@@ -186,12 +188,15 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
             auto row = [&](const double2 r) {
                 const double D = fma_rn(r.x, q, p);
                 const double Dd = fma_rn(r.x, qd, pd);
+                const double Ddd = fma_rn(r.x, qdd, pdd);
                 c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
                 const double pn = fma_rn(-x, D, mul_rn(r.y, p));
+                pdd = fma_rn(-x, Ddd, fma_rn(r.y, pdd, -2.0 * Dd));
                 pd = fma_rn(-x, Dd, fma_rn(r.y, pd, -D));
                 p = pn;
                 q = D;
                 qd = Dd;
+                qdd = Ddd;
             };
             int j = 0;
 #pragma unroll 1
@@ -208,25 +213,33 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
                 em = max(em, (unsigned)__double2hiint(q) & 0x7ff00000u);
                 em = max(em, (unsigned)__double2hiint(pd) & 0x7ff00000u);
                 em = max(em, (unsigned)__double2hiint(qd) & 0x7ff00000u);
+                em = max(em, (unsigned)__double2hiint(pdd) & 0x7ff00000u);
+                em = max(em, (unsigned)__double2hiint(qdd) & 0x7ff00000u);
                 if (em == 0x7ff00000u) {
                     bad = true;  // overflow: count and ratio unreliable -> caller bisects
                     p = -x;
                     q = 1.0;
                     pd = -1.0;
                     qd = 0.0;
+                    pdd = 0.0;
+                    qdd = 0.0;
                 } else {
                     const double sc = __hiloint2double((int)(0x7fe00000u - em), 0);
                     p *= sc;
                     q *= sc;
                     pd *= sc;
                     qd *= sc;
+                    pdd *= sc;
+                    qdd *= sc;
                 }
             }
             if (last) {
                 const double D = fma_rn(t[rows - 1].x, q, p);
                 const double Dd = fma_rn(t[rows - 1].x, qd, pd);
+                const double Ddd = fma_rn(t[rows - 1].x, qdd, pdd);
                 c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
                 ratio = D / Dd;
+                f2 = Ddd / D;
             }
         });
     cnt = (int)c;
@@ -234,6 +247,7 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
         const int c2 = count_x_cta(smem, nd, need && bad, x, pivmin);
         if (bad) {
             ratio = NAN;
+            f2 = NAN;
             cnt = c2;
         }
     }
@@ -287,8 +301,8 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
         }
         if (!__syncthreads_or(!mdone)) break;
         int c = 0;
-        double ratio = NAN;
-        count_xn_cta(smem, nd, need, x, pivmin, c, ratio);
+        double ratio = NAN, f2 = NAN;
+        count_xn_cta(smem, nd, need, x, pivmin, c, ratio, f2);
         if (need) {
             rows += n;
             passes++;
@@ -300,15 +314,27 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
             est_last = NAN;
             step_last = INFINITY;
             if (fabs(ratio) < INFINITY) {
-                const double est = x - ratio;
+                // Laguerre's step when the nearest eigenvalue on the side the count points
+                // to is lambda_k itself (count(x) = k: the largest root <= x; count(x) =
+                // k - 1: the smallest root > x): for a polynomial with real roots it then
+                // converges monotonically (cubically) to that root; Newton's otherwise
+                double step = ratio;
+                if ((c == k || c == k - 1) && fabs(f2) < INFINITY) {
+                    const double G = 1.0 / ratio, N = (double)n;
+                    const double H = G * G - f2;  // sum 1 / (x - lambda_j)^2
+                    const double sq = sqrt(fmax((N - 1.0) * (N * H - G * G), 0.0));
+                    const double den = c == k ? G + sq : G - sq;  // left: > 0, right: < 0
+                    if (den != 0.0 && (c == k ? den > 0.0 : den < 0.0)) step = N / den;
+                }
+                const double est = x - step;
                 est_last = est;
-                step_last = fabs(ratio);
+                step_last = fabs(step);
                 if (took_newton || nnewton == 0) {
                     nnewton++;
                     r2 = r1;
-                    r1 = fabs(ratio);
+                    r1 = fabs(step);
                 }
-                if (fabs(ratio) <= 0.25 * tol)
+                if (fabs(step) <= 0.25 * tol)
                     xn = est + (c >= k ? -0.25 * tol : 0.25 * tol);
                 else
                     xn = est;

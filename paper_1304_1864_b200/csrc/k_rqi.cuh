@@ -467,6 +467,8 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     // pB <- d_{k-1} pB - lam E, qB <- E.  Every row is two pair FMAs and a pair product
     // (no division on the dependent chain); l+ and u- enter only the binary64 norm
     // identities, formed off-chain.  Ratios s_b0, p_b0 are formed once per checkpoint.
+    using G0 = std::integral_constant<bool, false>;
+    using G1 = std::integral_constant<bool, true>;
     auto twisted_fixed = [&](bool need, bool store) -> int {
         if (need) zwritten = false;
         double sF = 0.0, cF_ = 0.0, sB = 0.0, cB_ = 0.0;  // Kahan sums of written squares
@@ -528,14 +530,17 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         };
         // one F row (rows < r) and one B row (rows > r); predicated commits keep the two
         // recurrences in one basic block so their dependent chains interleave
-        auto frow = [&](const double *bA, int64_t tA, int64_t kk) {
+        // GUARD: rows may lie on the other side of some thread's twist (else every row of
+        // the call commits: the block is below / above the whole CTA's twist range)
+        auto frow = [&](auto guard, const double *bA, int64_t tA, int64_t kk) {
+            constexpr bool GUARD = decltype(guard)::value;
             Row4<R> rw = srow<R>(bA, tA, kk);
             const R D = fma_dd(rw.d, qF, pF);
             const double lpx = hi(rw.ld) * hi(qF) * rcp(hi(D));  // l+ = ld / d+
             const double l2 = lpx * lpx;
             const double W2 = clampbig(fma(l2, W, l2));
             const R p2 = fma_dd(mlam, D, mul(rw.lld, pF));
-            if (kk < r) {
+            if (!GUARD || (int)kk < (int)r) {
                 if (wz) {
                     double pm, ipm;
                     int e;
@@ -550,14 +555,15 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                 qF = D;
             }
         };
-        auto brow = [&](const double *bD, int64_t tD, int64_t kk) {
+        auto brow = [&](auto guard, const double *bD, int64_t tD, int64_t kk) {
+            constexpr bool GUARD = decltype(guard)::value;
             Row4<R> rw = srow<R>(bD, tD, kk - 1);
             const R E = fma_dd(rw.lld, qB, pB);
             const double ux = hi(rw.l) * hi(rw.d) * hi(qB) * rcp(hi(E));  // u- = l d / D-
             const double u2 = ux * ux;
             const double V2 = clampbig(fma(u2, V, u2));
             const R P2 = fma_dd(mlam, E, mul(rw.d, pB));
-            if (kk > r && kk < n) {
+            if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
                 if (wz) {
                     double pm, ipm;
                     int e;
@@ -609,20 +615,29 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                         for (int q = 2 * h; q < 2 * h + 2; q++) {
                             const int64_t b0F = tA + q * RQ_C;
                             const int64_t b0B = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
+                            // (CTA-uniform) blocks entirely below / above the twist range
+                            const bool fastF = bA != nullptr && b0F + RQ_C <= cta_rmin;
+                            const bool fastB = bD != nullptr && b0B > cta_rmax && b0B + RQ_C <= n;
                             const bool fF = bA != nullptr && b0F < r;
                             const bool fB = bD != nullptr && b0B + RQ_C > r && b0B < n;
-                            if (fF && fB) {
+                            if (fastF && fastB) {
 #pragma unroll
                                 for (int j = 0; j < RQ_C; j++) {
-                                    frow(bA, tA, b0F + j);
-                                    brow(bD, tD, b0B + RQ_C - 1 - j);
+                                    frow(G0{}, bA, tA, b0F + j);
+                                    brow(G0{}, bD, tD, b0B + RQ_C - 1 - j);
+                                }
+                            } else if (fF && fB) {
+#pragma unroll
+                                for (int j = 0; j < RQ_C; j++) {
+                                    frow(G1{}, bA, tA, b0F + j);
+                                    brow(G1{}, bD, tD, b0B + RQ_C - 1 - j);
                                 }
                             } else if (fF) {
 #pragma unroll
-                                for (int j = 0; j < RQ_C; j++) frow(bA, tA, b0F + j);
+                                for (int j = 0; j < RQ_C; j++) frow(G1{}, bA, tA, b0F + j);
                             } else if (fB) {
 #pragma unroll
-                                for (int j = 0; j < RQ_C; j++) brow(bD, tD, b0B + RQ_C - 1 - j);
+                                for (int j = 0; j < RQ_C; j++) brow(G1{}, bD, tD, b0B + RQ_C - 1 - j);
                             }
                             if (fF) rescale_pq(pF, qF, EqF);
                             if (fB) rescale_pq(pB, qB, EqB);
