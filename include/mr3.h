@@ -84,7 +84,8 @@ enum mr3_param {
     MR3_XPHASE = 9,    /* fp64 I/O: approximate eigenvalues in binary_x first (L1064-L1111); 1 */
     MR3_REFINE = 10,   /* RQI start refinement constant C (0 = off): singletons whose bracket
                           half-width exceeds gap*sqrt(eps_x sqrt(n)/C) get a binary_x start; 4 */
-    MR3_GRID = 11,     /* 1: start the bisection from a shared grid of Sturm counts (k_grid); 1 */
+    MR3_GRID = 11,     /* 0: no shared grid; 1: uniform grid + 3 adaptive levels (k_grid);
+                          v >= 2: v - 2 adaptive levels; 1 */
     MR3_CTA = 12,      /* threads per CTA of the staged kernels, 32..128 (0 = 128) */
     MR3_XPTS = 13,     /* binary_x root phase: 1 bisection / multisection, 2 two points per lane,
                           3 Newton-accelerated bisection (G = 1; R8e); 3 */

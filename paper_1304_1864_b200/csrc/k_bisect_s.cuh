@@ -170,13 +170,18 @@ __device__ __forceinline__ int count_x_cta(double *smem, const NodeInfo &nd, boo
 // (p'_0 = -1, q'_0 = 0), rescaled with (p, q) by the same power of two (the ratio is
 // scale-free).  Six FP64 instructions per row; the derivative chain runs beside the
 // value chain.
+// mode 0: count at x with f'/f and f''/f (three chains: the state and its first and second
+// x-derivatives); mode 1: counts at x and at x2 (the second chain runs the count at x2,
+// the third idles) -- the same per-row cost, chosen per thread
 __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, bool need, double x,
-                                             double pivmin, int &cnt, double &ratio, double &f2) {
+                                             double pivmin, int &cnt, double &ratio, double &f2,
+                                             int mode = 0, double x2 = 0.0, int *cnt2 = nullptr) {
     const int64_t n = nd.n;
     // (p, q) and their first and second x-derivatives: f = det(M_x - x I) (scaled) is the
     // last D, f' and f'' the last D' and D''
-    double p = -x, q = 1.0, pd = -1.0, qd = 0.0, pdd = 0.0, qdd = 0.0;
-    unsigned c = 0;
+    const double sB = mode ? 0.0 : 1.0, xB = mode ? x2 : x;
+    double p = -x, q = 1.0, pd = mode ? -x2 : -1.0, qd = mode ? 1.0 : 0.0, pdd = 0.0, qdd = 0.0;
+    unsigned c = 0, cB = 0;
     bool bad = false;
     tile_pass(
         smem, n, [&](double *buf, int64_t t0) { stage_x_tile(buf, nd.repx, n, t0); },
@@ -190,9 +195,10 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
                 const double Dd = fma_rn(r.x, qd, pd);
                 const double Ddd = fma_rn(r.x, qdd, pdd);
                 c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+                cB += (unsigned)(__double2hiint(Dd) ^ __double2hiint(qd)) >> 31;
                 const double pn = fma_rn(-x, D, mul_rn(r.y, p));
-                pdd = fma_rn(-x, Ddd, fma_rn(r.y, pdd, -2.0 * Dd));
-                pd = fma_rn(-x, Dd, fma_rn(r.y, pd, -D));
+                pdd = fma_rn(-x, Ddd, fma_rn(r.y, pdd, (-2.0 * sB) * Dd));  // (mode 1: stays 0)
+                pd = fma_rn(-xB, Dd, fma_rn(r.y, pd, -sB * D));
                 p = pn;
                 q = D;
                 qd = Dd;
@@ -219,8 +225,8 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
                     bad = true;  // overflow: count and ratio unreliable -> caller bisects
                     p = -x;
                     q = 1.0;
-                    pd = -1.0;
-                    qd = 0.0;
+                    pd = mode ? -x2 : -1.0;
+                    qd = mode ? 1.0 : 0.0;
                     pdd = 0.0;
                     qdd = 0.0;
                 } else {
@@ -238,17 +244,21 @@ __device__ __forceinline__ void count_xn_cta(double *smem, const NodeInfo &nd, b
                 const double Dd = fma_rn(t[rows - 1].x, qd, pd);
                 const double Ddd = fma_rn(t[rows - 1].x, qdd, pdd);
                 c += (unsigned)(__double2hiint(D) ^ __double2hiint(q)) >> 31;
+                cB += (unsigned)(__double2hiint(Dd) ^ __double2hiint(qd)) >> 31;
                 ratio = D / Dd;
                 f2 = Ddd / D;
             }
         });
     cnt = (int)c;
-    if (__syncthreads_or(bad)) {  // rare: recount the affected threads (collective call)
+    if (cnt2) *cnt2 = (int)cB;
+    if (__syncthreads_or(bad)) {  // rare: recount the affected threads (collective calls)
         const int c2 = count_x_cta(smem, nd, need && bad, x, pivmin);
+        const int c3 = count_x_cta(smem, nd, need && bad && mode == 1, x2, pivmin);
         if (bad) {
             ratio = NAN;
             f2 = NAN;
             cnt = c2;
+            if (cnt2) *cnt2 = c3;
         }
     }
 }
@@ -275,12 +285,14 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
     double xn = NAN;
     double r1 = INFINITY, r2 = INFINITY;  // |Newton step| of the last two Newton passes
     int nnewton = 0;
+    bool close = false;  // next pass: counts at xn -+ tol/4 (closes the bracket around xn)
 #pragma unroll 1
     for (int round = 0; round < 4000; round++) {
-        double x = a;
+        double x = a, x2 = a;
         bool need = false;
         double tol = 0.0;
         bool took_newton = false;
+        int mode = 0;
         if (!mdone) {
             const double w = b - a;
             tol = tolmul * fmax(2.0 * rtol * fmax(fabs(a), fabs(b)), absfloor);
@@ -289,6 +301,12 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
                 converged = true;
             } else if (passes >= maxpass) {
                 mdone = true;  // left to the many-lane multisection (tail launch)
+            } else if (close && !isnan(xn)) {
+                mode = 1;
+                x = xn - 0.25 * tol;
+                x2 = xn + 0.25 * tol;
+                need = (a < x && x < b) || (a < x2 && x2 < b);
+                if (!need) mdone = true;
             } else {
                 // Newton while its steps contract (|step| at least halves every round)
                 // and stay inside the bracket; bisection otherwise
@@ -300,10 +318,23 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
             }
         }
         if (!__syncthreads_or(!mdone)) break;
-        int c = 0;
+        int c = 0, c2 = 0;
         double ratio = NAN, f2 = NAN;
-        count_xn_cta(smem, nd, need, x, pivmin, c, ratio, f2);
-        if (need) {
+        count_xn_cta(smem, nd, need, x, pivmin, c, ratio, f2, mode, x2, &c2);
+        if (need && mode == 1) {  // closing pass: two counts
+            rows += n;
+            passes++;
+            if (c >= k)
+                b = fmin(b, x);
+            else
+                a = fmax(a, x);
+            if (c2 >= k)
+                b = fmin(b, x2);
+            else
+                a = fmax(a, x2);
+            close = false;
+            xn = NAN;
+        } else if (need) {
             rows += n;
             passes++;
             if (c >= k)
@@ -311,6 +342,7 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
             else
                 a = x;
             xn = NAN;
+            close = false;
             est_last = NAN;
             step_last = INFINITY;
             if (fabs(ratio) < INFINITY) {
@@ -334,10 +366,17 @@ __device__ __forceinline__ void newton_cta(double *smem, const NodeInfo &nd, dou
                     r2 = r1;
                     r1 = fabs(step);
                 }
-                if (fabs(step) <= 0.25 * tol)
-                    xn = est + (c >= k ? -0.25 * tol : 0.25 * tol);
-                else
-                    xn = est;
+                // close the bracket around the estimate in one two-count pass once the step
+                // is below tol/4, or once the error after it -- cubic convergence, with the
+                // constant from the last two steps: r1^4 / r2^3 -- is predicted below tol/8
+                xn = est;
+                const bool cubic = nnewton >= 2 && r2 < INFINITY && r1 < 0.5 * r2;
+                const double perr = cubic ? r1 * (r1 / r2) * (r1 / r2) * (r1 / r2) : INFINITY;
+                close = fabs(step) <= 0.25 * tol || perr <= 0.125 * tol;
+                // error estimate of est for the RQI start (k_refine_flags): a direct bound
+                // (negative) from the observed cubic contraction, with a factor 4 and an
+                // ulp floor; else the step (the quadratic model there)
+                if (cubic) step_last = -fmax(4.0 * perr, 2.0 * 1.1102230246251565e-16 * fabs(est));
             }
         }
     }
@@ -719,6 +758,7 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
             if (active) {  // the last Newton estimate: RQI start unless k_refine_flags rejects it
                 it.x0[id] = conv ? est : NAN;
                 it.dx[id] = conv ? step : INFINITY;
+                it.twist[id] = passes;  // (diagnostics only: k_rqi_locate sets the twist)
             }
             if (tailflag && active) tailflag[local + task.first] = conv ? 0 : 1;
             if (tailflag && active && !conv) {
@@ -812,9 +852,12 @@ __global__ void k_refine_flags(const NodeInfo *__restrict__ nodes, Items it,
         if (pe < half_w) err = pe;
     }
     if (err == half_w) it.x0[id] = NAN;
-    // the refinement ends at about 2 ulps: below 4 ulps it has nothing to add
+    // the refinement ends at about 2 ulps: below 4 ulps it has nothing to add; and a start
+    // up to 1024x worse than `need` costs one or two more RQI iterations, which run as split
+    // passes (k_rqi, R9d) at a few percent of the refinement launch's latency (≈ 4 ms even
+    // for a handful of items: its multisection rounds are serial n-row chains)
     const double floor_ = 4.0 * eps_x * fmax(fabs(hi(a)), fabs(hi(b)));
-    flags[t] = (err > fmax(need, floor_) && n >= 2) ? 1 : 0;
+    flags[t] = (err > 1024.0 * fmax(need, floor_) && n >= 2) ? 1 : 0;
 }
 
 }  // namespace mr3

@@ -50,6 +50,7 @@ struct Cfg {  // per-mode parameters
 struct mr3_ctx_s {
     double t_last = 0.0;  // host wall time of the last synchronisation point (MR3_DEBUG & 2)
     int dump = 0;         // MR3_DEBUG & 1: items to dump
+    int grid_levels = 0;  // adaptive grid levels of the last plan (diagnostics)
     size_t mem_free = 0;  // device free memory seen by the first solve (RQI scratch budget)
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -613,7 +614,10 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             CKL("k_grid_counts");
             k_cell_init<<<ib, 256, 0, s>>>(cs, gi, c1, (int)n, kslice, (int)mine);
             CKL("k_cell_init");
-            for (int lev = 0; lev < GRID_LEVELS; lev++) {
+            // MR3_GRID = 1: GRID_LEVELS adaptive levels; v >= 2: v - 2 adaptive levels
+            const int levels = P[MR3_GRID] >= 2.0 ? (int)P[MR3_GRID] - 2 : GRID_LEVELS;
+            ctx->grid_levels = levels;
+            for (int lev = 0; lev < levels; lev++) {
                 k_cell_plan<<<ib, 256, 0, s>>>(cs, lead0, (int)mine, rtol, absfloor);
                 CKL("k_cell_plan");
                 size_t t1 = tb1, t2 = tb2;
@@ -671,14 +675,30 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             CK(cudaMemcpyAsync(&ht, tc, 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#6");
             if (ctx->dump) {
+                std::vector<int32_t> ps(mine);
+                cudaMemcpy(ps.data(), W.it.twist + first, mine * 4, cudaMemcpyDeviceToHost);
+                int hist[64] = {0}, chist[64] = {0};
+                for (int64_t i = 0; i < mine; i++) hist[std::min(63, std::max(0, ps[i]))]++;
+                for (int64_t b0 = 0; b0 < mine; b0 += 128) {
+                    int mx = 0;
+                    for (int64_t i = b0; i < std::min<int64_t>(mine, b0 + 128); i++) mx = std::max(mx, ps[i]);
+                    chist[std::min(63, mx)]++;
+                }
+                fprintf(stderr, "[mr3] Newton passes (items):");
+                for (int i = 0; i < 64; i++)
+                    if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
+                fprintf(stderr, "\n[mr3] Newton passes (CTA max, 128-item groups):");
+                for (int i = 0; i < 64; i++)
+                    if (chist[i]) fprintf(stderr, " %d:%d", i, chist[i]);
+                fprintf(stderr, "\n");
                 fprintf(stderr, "[mr3] Newton tail: %d of %d items:", ht, (int)mine);
                 std::vector<int32_t> htl(ht);
                 cudaMemcpy(htl.data(), tl, ht * 4, cudaMemcpyDeviceToHost);
                 std::vector<int> hclo(mine), hchi(mine);
                 if (ctx->bufs.count("cell_clo")) {
                     // final cells: after GRID_LEVELS swaps the current arrays alternate
-                    const char *a = (GRID_LEVELS % 2) ? "cell_clo2" : "cell_clo";
-                    const char *b = (GRID_LEVELS % 2) ? "cell_chi2" : "cell_chi";
+                    const char *a = (ctx->grid_levels % 2) ? "cell_clo2" : "cell_clo";
+                    const char *b = (ctx->grid_levels % 2) ? "cell_chi2" : "cell_chi";
                     cudaMemcpy(hclo.data(), ctx->bufs[a].p, mine * 4, cudaMemcpyDeviceToHost);
                     cudaMemcpy(hchi.data(), ctx->bufs[b].p, mine * 4, cudaMemcpyDeviceToHost);
                 }
