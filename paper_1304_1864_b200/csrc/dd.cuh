@@ -168,6 +168,23 @@ MR3_HD dd fma_dd(dd a, dd b, dd c) {
     return mkdd(s, l);
 }
 MR3_HD double fma_dd(double a, double b, double c) { return fma_rn(a, b, c); }
+// a x + b y in pair arithmetic: two two-prods, one two-sum (error ~ eps_y (|a x| + |b y|));
+// the two products are independent, so its dependent chain is one product + one two-sum
+MR3_HD dd dot2_dd(dd a, dd x, dd b, dd y) {
+    const double p1 = mul_rn(a.hi, x.hi), p2 = mul_rn(b.hi, y.hi);
+    double e1 = fma_rn(a.hi, x.hi, -p1), e2 = fma_rn(b.hi, y.hi, -p2);
+    e1 = fma_rn(a.hi, x.lo, e1);
+    e2 = fma_rn(b.hi, y.lo, e2);
+    e1 = fma_rn(a.lo, x.hi, e1);
+    e2 = fma_rn(b.lo, y.hi, e2);
+    double es;
+    const double s = two_sum(p1, p2, es);
+    const double t = add_rn(es, add_rn(e1, e2));
+    double l;
+    const double h = quick_two_sum(s, t, l);
+    return mkdd(h, l);
+}
+MR3_HD double dot2_dd(double a, double x, double b, double y) { return fma_rn(a, x, mul_rn(b, y)); }
 // exact scaling by a power of two
 MR3_HD dd scale_pow2(dd a, double sc) { return mkdd(mul_rn(a.hi, sc), mul_rn(a.lo, sc)); }
 MR3_HD double scale_pow2(double a, double sc) { return mul_rn(a, sc); }

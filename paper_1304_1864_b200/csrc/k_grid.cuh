@@ -95,7 +95,8 @@ __device__ __forceinline__ int grid_search(const int *cnt, int lo, int hi, int k
 // ---- adaptive levels: cells holding two or more eigenvalues are subdivided ----------
 //
 // After level 1 every requested index k has a cell [lo, hi] with counts clo < k <= chi.
-// A cell holding c = chi - clo >= 2 eigenvalues is cut by P = max(2c + 1, 64) uniform points; every
+// A cell holding c = chi - clo >= 2 eigenvalues is cut by P = 2c + 1 uniform points (at least
+// 64 from the second adaptive level on, where only clusters are left); every
 // index of the cell finds its sub-cell by binary search in their counts.  Repeated for a
 // few levels this isolates the eigenvalues at the ends of spectra whose density grows
 // there (Gauss nodes cluster quadratically at +-1), where one uniform grid cannot.
@@ -132,14 +133,15 @@ __global__ void k_cell_init(CellSet cs, const GridInfo *__restrict__ gi, const i
 }
 
 // leaders (first slice item of each cell) and their point counts
-__global__ void k_cell_plan(CellSet cs, int *lead0, int mine, double rtol, double absfloor) {
+__global__ void k_cell_plan(CellSet cs, int *lead0, int mine, double rtol, double absfloor,
+                            int pmin) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= mine) return;
     const double lo = cs.lo[t], hi = cs.hi[t];
     const bool lead = t == 0 || cs.lo[t - 1] != lo || cs.hi[t - 1] != hi;
     const int c = cs.chi[t] - cs.clo[t];
     const double tol = fmax(2.0 * rtol * fmax(fabs(lo), fabs(hi)), absfloor);
-    cs.P[t] = (lead && c >= 2 && hi - lo > tol) ? max(2 * c + 1, CELL_PMIN) : 0;
+    cs.P[t] = (lead && c >= 2 && hi - lo > tol) ? max(2 * c + 1, pmin) : 0;
     lead0[t] = lead ? t : -1;  // (max-scanned into cs.lead)
 }
 

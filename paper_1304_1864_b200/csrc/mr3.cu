@@ -618,7 +618,10 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             const int levels = P[MR3_GRID] >= 2.0 ? (int)P[MR3_GRID] - 2 : GRID_LEVELS;
             ctx->grid_levels = levels;
             for (int lev = 0; lev < levels; lev++) {
-                k_cell_plan<<<ib, 256, 0, s>>>(cs, lead0, (int)mine, rtol, absfloor);
+                // first adaptive level: 2c + 1 points per cell (about 2 per eigenvalue, one
+                // wave of counts); later levels: at least CELL_PMIN (the dense ends)
+                k_cell_plan<<<ib, 256, 0, s>>>(cs, lead0, (int)mine, rtol, absfloor,
+                                               lev == 0 ? 3 : CELL_PMIN);
                 CKL("k_cell_plan");
                 size_t t1 = tb1, t2 = tb2;
                 cub::DeviceScan::ExclusiveSum(ctmp, t1, cs.P, cs.off, (int)mine, s);
