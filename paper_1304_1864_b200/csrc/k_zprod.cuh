@@ -18,6 +18,8 @@
 // factors 1 / y_r, 1 / x_r and the exact 1 / ||z|| afterwards.  PP and 1/PP are
 // computed once per representation (k_node_pp) as mantissa-exponent pairs.
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace mr3 {
@@ -121,30 +123,42 @@ struct ZCol {
 };
 
 // Normalise each column: Z <- Z c / ||z|| (one read, one write of the block; ||z||^2 was
-// accumulated by k_rqi while writing).  Grid-stride over (column, 1024-row chunk).
+// accumulated by k_rqi while writing).  Grid-stride over (column, chunk of ZS_CHUNK rows);
+// 16-byte vector accesses (4 per thread in flight) when the column segment is aligned.
+constexpr int ZS_TPB = 256;
 template <class OutT>
-__global__ void __launch_bounds__(256) k_zscale(OutT *Z, int64_t ldz, int64_t ncols,
-                                                const ZCol *__restrict__ zc, int64_t maxn) {
-    const int64_t per_col = (maxn + 1023) / 1024;
+__global__ void __launch_bounds__(ZS_TPB) k_zscale(OutT *Z, int64_t ldz, int64_t ncols,
+                                                 const ZCol *__restrict__ zc, int64_t maxn) {
+    constexpr int V = 16 / sizeof(OutT);                  // elements per 16-byte vector
+    constexpr int64_t CHUNK = (int64_t)ZS_TPB * 4 * V;    // rows per work unit
+    using Vec = typename std::conditional<sizeof(OutT) == 8, double2, float4>::type;
+    const int64_t per_col = (maxn + CHUNK - 1) / CHUNK;
     const int64_t total = ncols * per_col;
     for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
         const int64_t c = w / per_col, ch = w - c * per_col;
         const ZCol z = zc[c];
-        const int64_t i0 = ch * 1024;
+        const int64_t i0 = ch * CHUNK;
         if (z.n <= 0 || i0 >= z.n) continue;
         const double inv = 1.0 / sqrt(z.ss);
         const double fF = z.cF * inv, fB = z.cB * inv;
         OutT *col = Z + c * ldz + z.row0;
-        OutT v[4];
+        const bool aligned = (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+        if (aligned && i0 + CHUNK <= z.n) {
+            Vec *cv = reinterpret_cast<Vec *>(col + i0);
+            Vec v[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int64_t i = i0 + threadIdx.x + u * 256;
-            v[u] = i < z.n ? col[i] : (OutT)0;
-        }
+            for (int u = 0; u < 4; u++) v[u] = cv[threadIdx.x + u * ZS_TPB];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int64_t i = i0 + threadIdx.x + u * 256;
-            if (i < z.n) col[i] = (OutT)((double)v[u] * (i <= z.r ? fF : fB));
+            for (int u = 0; u < 4; u++) {
+                const int64_t b = i0 + (int64_t)(threadIdx.x + u * ZS_TPB) * V;
+                OutT *e = reinterpret_cast<OutT *>(&v[u]);
+#pragma unroll
+                for (int q = 0; q < V; q++) e[q] = (OutT)((double)e[q] * (b + q <= z.r ? fF : fB));
+                cv[threadIdx.x + u * ZS_TPB] = v[u];
+            }
+        } else {  // ragged tail or misaligned segment: element-wise
+            for (int64_t i = i0 + threadIdx.x; i < min(i0 + CHUNK, (int64_t)z.n); i += ZS_TPB)
+                col[i] = (OutT)((double)col[i] * (i <= z.r ? fF : fB));
         }
     }
 }
