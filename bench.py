@@ -33,10 +33,10 @@ import synth  # noqa: E402
 #   Sturm row, binary_y projective (2 pair fma + 1 pair mul)          37
 #   Sturm row, binary_x projective (2 DFMA + 1 DMUL + rescale/8)      3.25
 #   Sturm row, fp64-internal mode (projective, binary64)              3.25
-#   Newton pass row, binary_x (value + x-derivative, projective)      6.5
+#   Newton/Laguerre pass row, binary_x (value + two x-derivatives)    11
 #   RQI row (rqi_rows: 2 fixed-twist passes of n rows each; projective F row 45, B row 45,
 #   +10 on the last pass for the product-form z components and their squares)  50
-FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25, "newton": 6.5}
+FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25, "newton": 11.0}
 FP64_INST_PER_RQI_ROW = {"dd": 50.0, "f64": 12.0}
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 

@@ -16,5 +16,6 @@ echo "launch-list exit $?" >> $O/${TAG}_ncu_launch.log
 bash tools/gpu_prof3.sh ${TAG} k_rqi 1
 bash tools/gpu_prof3.sh ${TAG} k_bisect_s 1
 bash tools/gpu_prof3.sh ${TAG} k_rqi_locate 1
+bash tools/gpu_prof3.sh ${TAG} k_cell_counts 3
 rm -f $O/${TAG}_*_sass.csv.gz
 for f in $O/${TAG}_*_sass.csv; do gzip -f $f; done
