@@ -94,7 +94,8 @@ enum mr3_param {
                           robustness bound instead (R8d); 0 */
     MR3_NEWTON = 15,   /* Newton passes per item before the many-lane multisection tail; 6 */
     MR3_TWISTW = 16,   /* twist weight slope w: r = argmin |gamma_k| (1 + w |2k - n| / n); 100 */
-    MR3_SPLIT = 17,    /* 1: RQI iterations >= 3 as split (chunked) passes, reading R9d; 1 */
+    MR3_SPLIT = 17,    /* split (chunked) RQI passes, reading R9d: 0 none, 1 iterations >= 3,
+                          2 also every iteration of small sets (one eigenpair per CTA); 1 */
     MR3_NPARAM = 18
 };
 

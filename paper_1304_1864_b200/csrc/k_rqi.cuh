@@ -66,7 +66,7 @@ struct RqiArgs {
                         // by root_widen * n * |lambda| (relative robustness of the root, R8d)
     int maxit;
     int jobz_v;
-    int split;  // RQI iterations >= 3 as split passes (R9d)
+    int split;  // split passes (R9d): 0 none, 1 iterations >= 3, 2 every iteration (1 item/CTA)
     void *w;          // eigenvalue output (global positions)
     void *Z;          // eigenvector output (columns col - zcol0)
     int64_t ldz, zcol0;
@@ -1005,7 +1005,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;
         const bool need = !done || store_only;
         if (!__syncthreads_or(need)) break;
-        const int c = (iters <= 2 || n < 4 * RQ_TPB || !A.split)
+        const int c = ((iters <= 2 && A.split < 2) || n < 4 * RQ_TPB || !A.split)
                           ? twisted_fixed(need, A.jobz_v && iters >= 2)
                                                      : split_all(need, A.jobz_v && iters >= 2);
         if (store_only) zfinal = zwritten;

@@ -1025,8 +1025,12 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         int32_t *tvals = (int32_t *)getbuf(ctx, "rqi_vals", (size_t)ncount * 4, &rc2);
         int32_t *slist = (int32_t *)getbuf(ctx, "rqi_sorted", (size_t)ncount * 4, &rc2);
         if (rc2) return rc2;
-        auto make_tasks = [&](const int32_t *lst, int *nt) -> int {
-            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, rtpb);
+        // few eigenpairs (fewer than ~16 per SM): one per CTA, every RQI iteration a split
+        // pass of all 128 threads (R9d) -- the serial n-row chains would leave the GPU idle
+        const bool split_all = P[MR3_SPLIT] >= 2 && ncount <= ctx->nsm * 16;
+        bool rqi_split_all = false;  // (set for the k_rqi launch, read by launch_chunks)
+        auto make_tasks = [&](const int32_t *lst, int *nt, int per) -> int {
+            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, per);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
                 ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
@@ -1070,7 +1074,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.gaptol = gaptol;
                 A.root_widen = ctx->root_widen;
                 A.twist_w = P[MR3_TWISTW];
-                A.split = P[MR3_SPLIT] != 0 ? 1 : 0;
+                A.split = P[MR3_SPLIT] != 0 ? (rqi_split_all && !locate ? 2 : 1) : 0;
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
                 A.w = w;
@@ -1161,7 +1165,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         // K5a: twist indices in binary_x, then group the singletons by (node, r) so
         // that the CTAs of the fixed-twist iterations sweep nearly equal row ranges
         int ntasks = 0;
-        if ((rc2 = make_tasks(list, &ntasks))) return rc2;
+        if ((rc2 = make_tasks(list, &ntasks, rtpb))) return rc2;
         if ((rc2 = launch_chunks(true, list, ntasks))) return rc2;
         k_twist_keys<<<(ncount + 255) / 256, 256, 0, s>>>(list, ncount, W.it.node, W.it.twist,
                                                           tkeys, tvals);
@@ -1176,7 +1180,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                                             ncount, 0, 64, s);
             CKL("radix sort (twist)");
         }
-        if ((rc2 = make_tasks(slist, &ntasks))) return rc2;
+        if ((rc2 = make_tasks(slist, &ntasks, split_all ? 1 : rtpb))) return rc2;
+        rqi_split_all = split_all;
         return launch_chunks(false, slist, ntasks);
     };
 
