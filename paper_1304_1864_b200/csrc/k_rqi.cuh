@@ -1297,9 +1297,6 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
 // of the binary64 values read as fixed point (error < 0.09, irrelevant for a factor-4
 // tolerant choice).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float flog2_abs(double v) {  // log2|v| (piecewise linear)
-    return (float)(__double2hiint(v) & 0x7fffffff) * 0x1p-20f - 1023.0f;
-}
 template <class R>
 __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     __shared__ __align__(16) double sx[4 * (StageG<2>::TILE + PP_TILE)];
@@ -1327,15 +1324,15 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     }
     if (n <= 1) return;  // (uniform over the CTA: one node per CTA)
     const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
-    float2 *cand = reinterpret_cast<float2 *>(A.ck_W);  // (log2 magnitude, row) per tile
+    int *cand = reinterpret_cast<int *>(A.ck_W);  // per tile: the reference of its int16 records
     // log2|PP| of the tile's row tr (staged PP rows; slot 3 holds {-1023 - log2|PP|,
     // -1023 + log2|PP|} as two floats, k_node_pp)
-    auto lppm = [](const double *buf, int tr) -> float {
-        return reinterpret_cast<const float *>(buf + StageG<2>::TILE + (tr + RQ_HALO) * 4 + 3)[0];
+    // (PP slot 3: round(16 log2|PP_k|) as int bits, k_node_pp)
+    auto lpp16 = [](const double *buf, int tr) -> int {
+        return reinterpret_cast<const int *>(buf + StageG<2>::TILE + (tr + RQ_HALO) * 4 + 3)[0];
     };
-    auto lppp = [](const double *buf, int tr) -> float {
-        return reinterpret_cast<const float *>(buf + StageG<2>::TILE + (tr + RQ_HALO) * 4 + 3)[1];
-    };
+    // 16 log2|v| + 16 * 1023 (piecewise linear, integer: exponent and top 4 mantissa bits)
+    auto l16 = [](double v) -> int { return (__double2hiint(v) & 0x7fffffff) >> 16; };
     auto rescale2 = [](double &x, double &y, int &E) {
         const unsigned ex = (unsigned)__double2hiint(x) & 0x7ff00000u;
         const unsigned ey = (unsigned)__double2hiint(y) & 0x7ff00000u;
@@ -1347,14 +1344,14 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
         E += (int)(em >> 20) - 1023;
     };
     const float wfac = (float)(A.twist_w / (double)n);
-    auto logw = [&](int64_t k) -> float {  // log2 of the twist weight 1 + w |2k - n| / n
-        return __log2f(fmaf(wfac, fabsf(2.0f * (float)k - (float)n), 1.0f));
+    auto logw = [&](int64_t k) -> int {  // 16 log2 of the twist weight 1 + w |2k - n| / n
+        return __float2int_rn(16.0f * __log2f(fmaf(wfac, fabsf(2.0f * (float)k - (float)n), 1.0f)));
     };
     // F: theta (projective pf/qf, exponent EF); B: phi (pb/qb, EB)
     double pf = -lam, qf = 1.0, pb = 0.0, qb = 1.0;
     int EF = 0, EB = 0;
     if (active) pb = __ldg(nd.repx + 2 * (n - 1)) - lam;
-    float best = -INFINITY;
+    int best = INT_MIN;  // in 1/16 log2 units
     int64_t rr = n / 2;  // (kept if every score is -inf: no usable twist information)
     // tile i is reached first by F iff 2 i < ntile - 1, by B iff 2 i > ntile - 1, by both
     // at the same step iff 2 i == ntile - 1 (F's rows of that tile are run first then).
@@ -1366,27 +1363,26 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     // eigenvectors peak within a few rows).  The mode is uniform over the CTA at every step.
     // [tile][slot][32 rows] int16: one 64-byte record per tile and eigenpair (4 x 16 B)
     uint4 *hist = reinterpret_cast<uint4 *>(A.ck_s);
-    float EFf = 0.0f, EBf = 0.0f;  // EF, EB as float (log2 bookkeeping)
+    int EF16 = 0, EB16 = 0;  // 16 EF, 16 EB (log2 bookkeeping in 1/16 units)
     // MODE 0: store (into h); MODE 1: score against h; GUARD: rows may reach n
-    auto put16 = [](uint32_t (&h)[16], int i, float v) {
-        const unsigned u = (unsigned)(unsigned short)(short)fminf(fmaxf(rintf(v), -32767.0f), 32767.0f);
+    auto put16 = [](uint32_t (&h)[16], int i, int v) {
+        const unsigned u = (unsigned)(v < -32767 ? -32767 : (v > 32767 ? 32767 : v)) & 0xffffu;
         h[i >> 1] = (i & 1) ? ((h[i >> 1] & 0x0000ffffu) | (u << 16)) : ((h[i >> 1] & 0xffff0000u) | u);
     };
-    auto get16 = [](const uint32_t (&h)[16], int i) -> float {
-        return (float)(short)((i & 1) ? (h[i >> 1] >> 16) : (h[i >> 1] & 0xffffu));
+    auto get16 = [](const uint32_t (&h)[16], int i) -> int {
+        return (i & 1) ? ((int)h[i >> 1] >> 16) : ((int)(h[i >> 1] << 16) >> 16);
     };
-    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, float &ref,
-                    float base, uint32_t (&h)[16]) {
+    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, int &ref,
+                    int base, uint32_t (&h)[16]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
-        const float l = fmaf((float)(__double2hiint(qf) & 0x7fffffff), 0x1p-20f,
-                             EFf + lppm(bA, tr));  // log2|y_kk|
+        const int l = l16(qf) + EF16 - lpp16(bA, tr);  // 16 log2|y_kk| (+ const)
         if (MODE == 0) {
-            ref = ref == -INFINITY ? l : ref;
-            put16(h, tr, (l - ref) * 16.0f);
+            ref = ref == INT_MIN ? l : ref;
+            put16(h, tr, l - ref);
         } else {
-            const float sc = l + fmaf(get16(h, tr), 0.0625f, base);
+            const int sc = l + get16(h, tr) + base;
             const bool up = sc > best;
             best = up ? sc : best;
             rr = up ? kk : rr;
@@ -1398,18 +1394,17 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             qf = D;
         }
     };
-    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, float &ref,
-                    float base, uint32_t (&h)[16]) {
+    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, int &ref,
+                    int base, uint32_t (&h)[16]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
-        const float l = fmaf((float)(__double2hiint(qb) & 0x7fffffff), 0x1p-20f,
-                             EBf + lppp(bD, tr));  // log2|x_kk|
+        const int l = l16(qb) + EB16 + lpp16(bD, tr);  // 16 log2|x_kk| (+ const)
         if (MODE == 0) {
-            ref = ref == -INFINITY ? l : ref;
-            put16(h, tr, (l - ref) * 16.0f);
+            ref = ref == INT_MIN ? l : ref;
+            put16(h, tr, l - ref);
         } else {
-            const float sc = l + fmaf(get16(h, tr), 0.0625f, base);
+            const int sc = l + get16(h, tr) + base;
             const bool up = sc > best;
             best = up ? sc : best;
             rr = up ? kk : rr;
@@ -1421,9 +1416,9 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             qb = E;
         }
     };
-    auto rescale2f = [&](double &x, double &y, int &E, float &Ef) {
+    auto rescale2f = [&](double &x, double &y, int &E, int &E16) {
         rescale2(x, y, E);
-        Ef = (float)E;
+        E16 = E << 4;
     };
     using M0 = std::integral_constant<int, 0>;
     using M1 = std::integral_constant<int, 1>;
@@ -1449,7 +1444,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     // both streams over one step's tiles, rows interleaved (fully unrolled: the packed
     // int16 rows live in registers)
     auto step = [&](auto mode, auto guard, const double *bA, int64_t tA, const double *bD,
-                    int64_t tD, float &reff, float &refb, float basef, float baseb,
+                    int64_t tD, int &reff, int &refb, int basef, int baseb,
                     uint32_t (&hf)[16], uint32_t (&hb)[16]) {
 #pragma unroll
         for (int q = 0; q < RQ_TR / RQ_C; q++) {
@@ -1460,8 +1455,8 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                 brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, refb,
                      baseb, hb);
             }
-            rescale2f(pf, qf, EF, EFf);
-            rescale2f(pb, qb, EB, EBf);
+            rescale2f(pf, qf, EF, EF16);
+            rescale2f(pb, qb, EB, EB16);
         }
     };
     dual_staged_pass<2>(
@@ -1470,19 +1465,19 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             if (!active) return;
             const int iA = (int)(tA / RQ_TR), iD = (int)(tD / RQ_TR);
             const bool guard = tA + RQ_TR > n - 1 || tD + RQ_TR > n - 1 || tD == 0;
-            float reff = -INFINITY, refb = -INFINITY;
+            int reff = INT_MIN, refb = INT_MIN;
             uint32_t hf[16], hb[16];
 #pragma unroll
             for (int u = 0; u < 16; u++) hf[u] = hb[u] = 0u;
             if (2 * iA < ntile - 1) {  // first half: store
                 if (guard)
-                    step(M0{}, G1{}, bA, tA, bD, tD, reff, refb, 0.0f, 0.0f, hf, hb);
+                    step(M0{}, G1{}, bA, tA, bD, tD, reff, refb, 0, 0, hf, hb);
                 else
-                    step(M0{}, G0{}, bA, tA, bD, tD, reff, refb, 0.0f, 0.0f, hf, hb);
+                    step(M0{}, G0{}, bA, tA, bD, tD, reff, refb, 0, 0, hf, hb);
                 hstore(iA, hf);
                 hstore(iD, hb);
-                cand[(int64_t)iA * A.S + slot] = make_float2(reff, 0.0f);
-                cand[(int64_t)iD * A.S + slot] = make_float2(refb, 0.0f);
+                cand[(int64_t)iA * A.S + slot] = reff;
+                cand[(int64_t)iD * A.S + slot] = refb;
                 return;
             }
             if (2 * iA == ntile - 1) {  // middle tile (odd ntile): F stores, then B scores
@@ -1490,24 +1485,24 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                 for (int q = 0; q < RQ_TR / RQ_C; q++) {
 #pragma unroll
                     for (int j = 0; j < RQ_C; j++)
-                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, reff, 0.0f, hf);
-                    rescale2f(pf, qf, EF, EFf);
+                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, reff, 0, hf);
+                    rescale2f(pf, qf, EF, EF16);
                 }
-                const float baseb = reff - logw(tD + RQ_TR / 2);
+                const int baseb = reff - logw(tD + RQ_TR / 2);
 #pragma unroll
                 for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
 #pragma unroll
                     for (int j = RQ_C - 1; j >= 0; j--)
                         brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, refb, baseb, hf);
-                    rescale2f(pb, qb, EB, EBf);
+                    rescale2f(pb, qb, EB, EB16);
                 }
                 return;
             }
             // second half: score every row against the other stream's stored value
             hload(iA, hf);
             hload(iD, hb);
-            const float basef = cand[(int64_t)iA * A.S + slot].x - logw(tA + RQ_TR / 2);
-            const float baseb = cand[(int64_t)iD * A.S + slot].x - logw(tD + RQ_TR / 2);
+            const int basef = cand[(int64_t)iA * A.S + slot] - logw(tA + RQ_TR / 2);
+            const int baseb = cand[(int64_t)iD * A.S + slot] - logw(tD + RQ_TR / 2);
             if (guard)
                 step(M1{}, G1{}, bA, tA, bD, tD, reff, refb, basef, baseb, hf, hb);
             else

@@ -24,7 +24,7 @@
 
 namespace mr3 {
 
-// per row of a node: {PPm, IPPm, E (int bits), (two floats: -1023 -+ log2|PP_k|)}: PP_k = PPm 2^E,
+// per row of a node: {PPm, IPPm, E (int bits), round(16 log2|PP_k|) (int bits)}: PP_k = PPm 2^E,
 // 1/PP_k = IPPm 2^-E.
 // The mantissas are products of the representation's ld in pair arithmetic, rounded
 // once: z components come out to binary64 accuracy (the output precision).
@@ -100,11 +100,8 @@ __global__ void __launch_bounds__(256) k_node_pp(NodeInfo *nodes, int first, dou
         o[0] = hi(pm);
         o[1] = hi(ipm);
         o[2] = __hiloint2double(0, pe);  // E as int bits (no F2I on the readers' path)
-        {  // {-1023 - log2|PP_j|, -1023 + log2|PP_j|} as floats (k_rqi_locate)
-            const float l = (float)(log2(fabs(hi(pm))) + (double)pe);
-            float2 *f = reinterpret_cast<float2 *>(o + 3);
-            *f = make_float2(-1023.0f - l, -1023.0f + l);
-        }
+        // round(16 log2|PP_j|) as int bits (k_rqi_locate's 1/16-log2 bookkeeping)
+        o[3] = __hiloint2double(0, (int)lrint(16.0 * (log2(fabs(hi(pm))) + (double)pe)));
         if (j <= n - 2) {
             pm = mul(pm, neg(load_row4<R>(nd.rep, j).ld));
             normalize_me(pm, pe);
