@@ -582,26 +582,27 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         // stream) and leave as coalesced 128-byte column segments
         const bool cta_store = store && A.jobz_v;  // uniform over the CTA
         if (cta_store) {
-            s_wz[tid] = wz ? 1 : 0;
-            s_r[tid] = r;
-            s_zoff[tid] = wz ? (col0 - A.zcol0) * A.ldz + nd.row0 : 0;
+            // per column: the rows each stream writes (F: g < rF, B: g > rB; nothing if the
+            // column is not written) and the column's base pointer
+            reinterpret_cast<int2 *>(s_r)[tid] = wz ? make_int2((int)r, (int)r) : make_int2(-1, INT_MAX);
+            reinterpret_cast<OutT **>(s_zoff)[tid] =
+                wz ? reinterpret_cast<OutT *>(A.Z) + (col0 - A.zcol0) * A.ldz + nd.row0 : nullptr;
         }
         auto flush = [&](const double *bA, int64_t tA, int hA, const double *bD, int64_t tD,
                          int hD) {
             __syncthreads();
-            OutT *Zo = reinterpret_cast<OutT *>(A.Z);
             const int warp = tid >> 5, lane = tid & 31, row = lane & 15;
+            const int2 *rfb = reinterpret_cast<const int2 *>(s_r);
+            OutT *const *zp = reinterpret_cast<OutT *const *>(s_zoff);
+            const int gA = bA != nullptr ? (int)tA + 16 * hA + row : INT_MAX;
+            const int gD = (bD != nullptr && (int)tD + 16 * hD + row < (int)n)
+                               ? (int)tD + 16 * hD + row
+                               : INT_MIN;
+#pragma unroll 4
             for (int c = 2 * warp + (lane >> 4); c < RQ_TPB; c += 2 * (RQ_TPB / 32)) {
-                if (!s_wz[c]) continue;
-                const int64_t rc = s_r[c];
-                if (bA != nullptr) {
-                    const int64_t g = tA + 16 * hA + row;
-                    if (g < rc) Zo[s_zoff[c] + g] = ztF[row][c];
-                }
-                if (bD != nullptr) {
-                    const int64_t g = tD + 16 * hD + row;
-                    if (g > rc && g < n) Zo[s_zoff[c] + g] = ztB[row][c];
-                }
+                const int2 rb = rfb[c];
+                if (gA < rb.x) zp[c][gA] = ztF[row][c];
+                if (gD > rb.y) zp[c][gD] = ztB[row][c];
             }
             __syncthreads();
         };
