@@ -67,6 +67,7 @@ struct RqiArgs {
     int maxit;
     int jobz_v;
     int split;  // split passes (R9d): 0 none, 1 iterations >= 3, 2 every iteration (1 item/CTA)
+    int fuse_scale;  // 1: every CTA normalises its own columns at its end (no k_zscale launch)
     void *w;          // eigenvalue output (global positions)
     void *Z;          // eigenvector output (columns col - zcol0)
     int64_t ldz, zcol0;
@@ -1099,6 +1100,54 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
         return;
     }
+    // K6 epilogue fused (A.fuse_scale): the CTA normalises its own columns as soon as it is
+    // done -- the HBM traffic of the scaling overlaps the other CTAs' arithmetic (collective)
+    auto fused_scale = [&]() {
+        if (!A.fuse_scale) return;
+        ZCol *szc = reinterpret_cast<ZCol *>(sstage);
+        OutT **szp = reinterpret_cast<OutT **>(szc + RQ_TPB);
+        __syncthreads();  // (sstage is free: the last staged pass ended with a barrier)
+        szc[tid] = zinfo;
+        szp[tid] = zcol;  // nullptr: no column
+        __syncthreads();
+        constexpr int V = 16 / sizeof(OutT);
+        using Vec = typename std::conditional<sizeof(OutT) == 8, double2, float4>::type;
+#pragma unroll 1
+        for (int j = 0; j < RQ_TPB; j++) {
+            OutT *col = szp[j];
+            if (col == nullptr) continue;  // (uniform)
+            const ZCol z = szc[j];
+            const double inv = 1.0 / sqrt(z.ss);
+            const double fF = z.cF * inv, fB = z.cB * inv;
+            const int64_t nn = z.n;
+            const bool aligned = (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+            const int64_t nv = aligned ? nn / V : 0;  // whole vectors
+            Vec *cv = reinterpret_cast<Vec *>(col);
+            constexpr int U = 8;
+#pragma unroll 1
+            for (int64_t b0 = 0; b0 < nv; b0 += (int64_t)U * RQ_TPB) {
+                Vec v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t i = b0 + u * RQ_TPB + tid;
+                    if (i < nv) v[u] = cv[i];
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t i = b0 + u * RQ_TPB + tid;
+                    if (i < nv) {
+                        OutT *e = reinterpret_cast<OutT *>(&v[u]);
+#pragma unroll
+                        for (int q = 0; q < V; q++)
+                            e[q] = (OutT)((double)e[q] * (i * V + q <= z.r ? fF : fB));
+                        cv[i] = v[u];
+                    }
+                }
+            }
+            for (int64_t i = nv * V + tid; i < nn; i += RQ_TPB)  // tail / misaligned
+                col[i] = (OutT)((double)col[i] * (i <= z.r ? fF : fB));
+        }
+    };
 
     // ---------------- fallback only: z by sweeps from the checkpoints of twisted() ------
     // (the regular path wrote z in product form during its last fixed-twist pass)
@@ -1106,6 +1155,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     if (!__syncthreads_or(mine)) {
         if (zcol != nullptr) A.zc[col0 - A.zcol0] = zinfo;
         if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
+        fused_scale();
         return;
     }
     const double inv = 1.0 / sqrt(nz2);
@@ -1266,6 +1316,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     (void)ss_hi;
     (void)ss_lo;
     if (active && rows) atomicAdd(&A.st->rqi_rows, rows);
+    fused_scale();
 }
 
 // ---------------------------------------------------------------------------

@@ -51,6 +51,7 @@ struct mr3_ctx_s {
     double t_last = 0.0;  // host wall time of the last synchronisation point (MR3_DEBUG & 2)
     int dump = 0;         // MR3_DEBUG & 1: items to dump
     int grid_levels = 0;  // adaptive grid levels of the last plan (diagnostics)
+    int fuse_scale = 1;   // K6 normalisation inside k_rqi (MR3_FUSE_SCALE=0 in the environment: k_zscale)
     size_t mem_free = 0;  // device free memory seen by the first solve (RQI scratch budget)
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -1075,6 +1076,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.root_widen = ctx->root_widen;
                 A.twist_w = P[MR3_TWISTW];
                 A.split = P[MR3_SPLIT] != 0 ? (rqi_split_all && !locate ? 2 : 1) : 0;
+                A.fuse_scale = ctx->fuse_scale;
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
                 A.w = w;
@@ -1350,7 +1352,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         cudaMemset(ctx->bufs["dbg_iters"].p, 0, cnt * 4);
         cudaMemset(ctx->bufs["dbg_trace"].p, 0, (size_t)cnt * 64);
     }
-    if (dzc) {  // K6 epilogue: per-column factors and exact normalisation (k_zprod.cuh)
+    if (dzc && !ctx->fuse_scale) {  // K6 epilogue: per-column factors and exact normalisation (k_zprod.cuh)
         KTime *tf = kt_begin(ctx, "k_zscale");
         const int64_t nc = c1 - c0;
         k_zscale<OutT><<<ctx->nsm * 16, 256, 0, s>>>(Z, ldz, nc, dzc, ctx->n);
@@ -1410,6 +1412,10 @@ int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     const char *dbg = getenv("MR3_DEBUG");
     ctx->debug = dbg ? atoi(dbg) : 0;
+    {
+        const char *fz = getenv("MR3_FUSE_SCALE");
+        ctx->fuse_scale = fz ? (atoi(fz) != 0) : 1;
+    }
     // MR3_DEBUG bits: 1 = dumps and histograms, 2 = host sync points, 4 = device timeline
     ctx->dump = (ctx->debug & 1) ? (ctx->debug > 8 ? ctx->debug : 40) : 0;
     *out = ctx;
