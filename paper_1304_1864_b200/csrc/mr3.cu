@@ -691,6 +691,9 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                 fprintf(stderr, "[mr3] Newton passes (items):");
                 for (int i = 0; i < 64; i++)
                     if (hist[i]) fprintf(stderr, " %d:%d", i, hist[i]);
+                fprintf(stderr, "\n[mr3] items with >= 5 passes:");
+                for (int64_t i = 0; i < mine; i++)
+                    if (ps[i] >= 5) fprintf(stderr, " %lld", (long long)(first + i));
                 fprintf(stderr, "\n[mr3] Newton passes (CTA max, 128-item groups):");
                 for (int i = 0; i < 64; i++)
                     if (chist[i]) fprintf(stderr, " %d:%d", i, chist[i]);
