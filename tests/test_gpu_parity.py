@@ -386,6 +386,7 @@ def test_default_needs_no_rqi_fallback():
                                # pass and join the second as store-only
     {"KRS": 1e-4},             # tighter stopping: third and later iterations, as split passes
     {"KRS": 1e-4, "SPLIT": 0},  # the same iterations as serial passes
+    {"SPLIT": 2},              # small sets: every iteration a split pass, one eigenpair per CTA
     {"TWISTW": 0},             # unweighted argmin twist
     {"NEWTON": 1},             # almost every item through the many-lane multisection tail
     {"XPTS": 1},               # plain bisection in the binary_x phase
