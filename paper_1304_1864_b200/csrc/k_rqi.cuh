@@ -1416,25 +1416,19 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     // [tile][slot][32 rows] int16: one 64-byte record per tile and eigenpair (4 x 16 B)
     uint4 *hist = reinterpret_cast<uint4 *>(A.ck_s);
     int EF16 = 0, EB16 = 0;  // 16 EF, 16 EB (log2 bookkeeping in 1/16 units)
-    // MODE 0: store (into h); MODE 1: score against h; GUARD: rows may reach n
-    auto put16 = [](uint32_t (&h)[16], int i, int v) {
-        const unsigned u = (unsigned)(v < -32767 ? -32767 : (v > 32767 ? 32767 : v)) & 0xffffu;
-        h[i >> 1] = (i & 1) ? ((h[i >> 1] & 0x0000ffffu) | (u << 16)) : ((h[i >> 1] & 0xffff0000u) | u);
-    };
-    auto get16 = [](const uint32_t (&h)[16], int i) -> int {
-        return (i & 1) ? ((int)h[i >> 1] >> 16) : ((int)(h[i >> 1] << 16) >> 16);
-    };
-    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, int &ref,
-                    int base, uint32_t (&h)[16]) {
+    // MODE 0: keep the tile's values in h (registers; stored at the tile end as int8 in whole
+    // log2 units below the tile maximum, 32 bytes per tile and eigenpair); MODE 1: score
+    // against h (the other stream's values, unpacked to 1/16 units relative to its maximum)
+    auto frow = [&](auto mode, auto guard, const double *bA, int tr, int kk, int base,
+                    int (&h)[32]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
         const int l = l16(qf) + EF16 - lpp16(bA, tr);  // 16 log2|y_kk| (+ const)
         if (MODE == 0) {
-            ref = ref == INT_MIN ? l : ref;
-            put16(h, tr, l - ref);
+            h[tr] = l;
         } else {
-            const int sc = l + get16(h, tr) + base;
+            const int sc = l + h[tr] + base;
             const bool up = sc > best;
             best = up ? sc : best;
             rr = up ? kk : rr;
@@ -1446,17 +1440,16 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             qf = D;
         }
     };
-    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, int &ref,
-                    int base, uint32_t (&h)[16]) {
+    auto brow = [&](auto mode, auto guard, const double *bD, int tr, int kk, int base,
+                    int (&h)[32]) {
         constexpr int MODE = decltype(mode)::value;
         constexpr bool GUARD = decltype(guard)::value;
         if (GUARD && kk >= n) return;
         const int l = l16(qb) + EB16 + lpp16(bD, tr);  // 16 log2|x_kk| (+ const)
         if (MODE == 0) {
-            ref = ref == INT_MIN ? l : ref;
-            put16(h, tr, l - ref);
+            h[tr] = l;
         } else {
-            const int sc = l + get16(h, tr) + base;
+            const int sc = l + h[tr] + base;
             const bool up = sc > best;
             best = up ? sc : best;
             rr = up ? kk : rr;
@@ -1476,36 +1469,53 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     using M1 = std::integral_constant<int, 1>;
     using G0 = std::integral_constant<bool, false>;
     using G1 = std::integral_constant<bool, true>;
-    auto hload = [&](int t, uint32_t (&h)[16]) {
-        const uint4 *src = hist + ((int64_t)t * A.S + slot) * 4;
+    auto hload = [&](int t, int (&h)[32]) {  // -> 16 (value - tile maximum)
+        const uint4 *src = hist + ((int64_t)t * A.S + slot) * 2;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < 2; u++) {
             const uint4 v = src[u];
-            h[4 * u] = v.x;
-            h[4 * u + 1] = v.y;
-            h[4 * u + 2] = v.z;
-            h[4 * u + 3] = v.w;
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+#pragma unroll
+                for (int b = 0; b < 4; b++)
+                    h[16 * u + 4 * q + b] = (int)(signed char)((w[q] >> (8 * b)) & 0xffu) * 16;
         }
     };
-    auto hstore = [&](int t, const uint32_t (&h)[16]) {
-        uint4 *dst = hist + ((int64_t)t * A.S + slot) * 4;
+    auto hstore = [&](int t, const int (&h)[32]) -> int {  // returns the tile maximum
+        int m = INT_MIN;
 #pragma unroll
-        for (int u = 0; u < 4; u++)
-            dst[u] = make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+        for (int r = 0; r < 32; r++) m = max(m, h[r]);
+        uint4 *dst = hist + ((int64_t)t * A.S + slot) * 2;
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            unsigned w[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                unsigned acc = 0;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int hv = h[16 * u + 4 * q + b];
+                    const int d = hv == INT_MIN ? -127 : max((hv - m) >> 4, -127);
+                    acc |= ((unsigned)d & 0xffu) << (8 * b);
+                }
+                w[q] = acc;
+            }
+            dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return m;
     };
     // both streams over one step's tiles, rows interleaved (fully unrolled: the packed
     // int16 rows live in registers)
     auto step = [&](auto mode, auto guard, const double *bA, int64_t tA, const double *bD,
-                    int64_t tD, int &reff, int &refb, int basef, int baseb,
-                    uint32_t (&hf)[16], uint32_t (&hb)[16]) {
+                    int64_t tD, int basef, int baseb, int (&hf)[32], int (&hb)[32]) {
 #pragma unroll
         for (int q = 0; q < RQ_TR / RQ_C; q++) {
             const int oF = q * RQ_C, oB = (RQ_TR / RQ_C - 1 - q) * RQ_C;
 #pragma unroll
             for (int j = 0; j < RQ_C; j++) {
-                frow(mode, guard, bA, oF + j, (int)tA + oF + j, reff, basef, hf);
-                brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, refb,
-                     baseb, hb);
+                frow(mode, guard, bA, oF + j, (int)tA + oF + j, basef, hf);
+                brow(mode, guard, bD, oB + RQ_C - 1 - j, (int)tD + oB + RQ_C - 1 - j, baseb, hb);
             }
             rescale2f(pf, qf, EF, EF16);
             rescale2f(pb, qb, EB, EB16);
@@ -1517,19 +1527,16 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             if (!active) return;
             const int iA = (int)(tA / RQ_TR), iD = (int)(tD / RQ_TR);
             const bool guard = tA + RQ_TR > n - 1 || tD + RQ_TR > n - 1 || tD == 0;
-            int reff = INT_MIN, refb = INT_MIN;
-            uint32_t hf[16], hb[16];
+            int hf[32], hb[32];
 #pragma unroll
-            for (int u = 0; u < 16; u++) hf[u] = hb[u] = 0u;
+            for (int u = 0; u < 32; u++) hf[u] = hb[u] = INT_MIN;
             if (2 * iA < ntile - 1) {  // first half: store
                 if (guard)
-                    step(M0{}, G1{}, bA, tA, bD, tD, reff, refb, 0, 0, hf, hb);
+                    step(M0{}, G1{}, bA, tA, bD, tD, 0, 0, hf, hb);
                 else
-                    step(M0{}, G0{}, bA, tA, bD, tD, reff, refb, 0, 0, hf, hb);
-                hstore(iA, hf);
-                hstore(iD, hb);
-                cand[(int64_t)iA * A.S + slot] = reff;
-                cand[(int64_t)iD * A.S + slot] = refb;
+                    step(M0{}, G0{}, bA, tA, bD, tD, 0, 0, hf, hb);
+                cand[(int64_t)iA * A.S + slot] = hstore(iA, hf);
+                cand[(int64_t)iD * A.S + slot] = hstore(iD, hb);
                 return;
             }
             if (2 * iA == ntile - 1) {  // middle tile (odd ntile): F stores, then B scores
@@ -1537,15 +1544,16 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                 for (int q = 0; q < RQ_TR / RQ_C; q++) {
 #pragma unroll
                     for (int j = 0; j < RQ_C; j++)
-                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, reff, 0, hf);
+                        frow(M0{}, G1{}, bA, q * RQ_C + j, (int)tA + q * RQ_C + j, 0, hf);
                     rescale2f(pf, qf, EF, EF16);
                 }
-                const int baseb = reff - logw(tD + RQ_TR / 2);
+                // (the same tile: F's values as they are, no quantisation)
+                const int baseb = -logw(tD + RQ_TR / 2);
 #pragma unroll
                 for (int q = RQ_TR / RQ_C - 1; q >= 0; q--) {
 #pragma unroll
                     for (int j = RQ_C - 1; j >= 0; j--)
-                        brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, refb, baseb, hf);
+                        brow(M1{}, G1{}, bD, q * RQ_C + j, (int)tD + q * RQ_C + j, baseb, hf);
                     rescale2f(pb, qb, EB, EB16);
                 }
                 return;
@@ -1556,9 +1564,9 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             const int basef = cand[(int64_t)iA * A.S + slot] - logw(tA + RQ_TR / 2);
             const int baseb = cand[(int64_t)iD * A.S + slot] - logw(tD + RQ_TR / 2);
             if (guard)
-                step(M1{}, G1{}, bA, tA, bD, tD, reff, refb, basef, baseb, hf, hb);
+                step(M1{}, G1{}, bA, tA, bD, tD, basef, baseb, hf, hb);
             else
-                step(M1{}, G0{}, bA, tA, bD, tD, reff, refb, basef, baseb, hf, hb);
+                step(M1{}, G0{}, bA, tA, bD, tD, basef, baseb, hf, hb);
         },
         nd.pp);
     // F's candidates (tiles reached by F first) scored against B: B evaluated those in
