@@ -51,6 +51,8 @@ struct mr3_ctx_s {
     double t_last = 0.0;  // host wall time of the last synchronisation point (MR3_DEBUG & 2)
     int dump = 0;         // MR3_DEBUG & 1: items to dump
     int grid_levels = 0;  // adaptive grid levels of the last plan (diagnostics)
+    cudaStream_t side = nullptr;              // internal stream (root PP rows)
+    cudaEvent_t ev_root = nullptr, ev_pp = nullptr;
     int fuse_scale = 1;   // K6 normalisation inside k_rqi (MR3_FUSE_SCALE=0 in the environment: k_zscale)
     size_t mem_free = 0;  // device free memory seen by the first solve (RQI scratch budget)
     int device = 0;
@@ -457,8 +459,13 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     {  // prod_{j<k} (-ld_j) per root (product-form eigenvectors, k_zprod.cuh)
         double *pp = (double *)getbuf(ctx, "pp_root", (size_t)n * PP_STRIDE * 8, &rc);
         if (rc) return rc;
-        k_node_pp<R><<<ctx->nblocks, 256, 0, s>>>(dnodes, 0, pp, 0, 1);
+        // on the side stream: nothing before the RQI phase reads PP, so it overlaps the grid
+        // and bisection (joined in run_rqi)
+        CK(cudaEventRecord(ctx->ev_root, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_root, 0));
+        k_node_pp<R><<<ctx->nblocks, 256, 0, ctx->side>>>(dnodes, 0, pp, 0, 1);
         CKL("k_node_pp");
+        CK(cudaEventRecord(ctx->ev_pp, ctx->side));
     }
     ctx->nodes_used = ctx->nblocks;
 
@@ -964,6 +971,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
         if (ncount <= 0) return 0;
         int rc2 = 0;
+        CK(cudaStreamWaitEvent(s, ctx->ev_pp, 0));  // the root's PP rows (side stream)
         if (P[MR3_REFINE] > 0) {  // K2': binary_x starting points for small-gap singletons
             char *flags = (char *)getbuf(ctx, "ref_flags", (size_t)ncount, &rc2);
             int32_t *rlist = (int32_t *)getbuf(ctx, "ref_list", (size_t)ncount * 4, &rc2);
@@ -1412,6 +1420,14 @@ int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
         }
         ctx->own_stream = true;
     }
+    if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_root, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_pp, cudaEventDisableTiming) != cudaSuccess) {
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+        return MR3_ERR_CUDA;
+    }
+    cudaEventRecord(ctx->ev_pp, ctx->side);  // (completed: nothing to wait for before a plan)
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     const char *dbg = getenv("MR3_DEBUG");
     ctx->debug = dbg ? atoi(dbg) : 0;
@@ -1435,6 +1451,10 @@ int mr3_destroy(mr3_ctx ctx) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
     }
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_root);
+    cudaEventDestroy(ctx->ev_pp);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return 0;
