@@ -96,7 +96,14 @@ enum mr3_param {
     MR3_TWISTW = 16,   /* twist weight slope w: r = argmin |gamma_k| (1 + w |2k - n| / n); 100 */
     MR3_SPLIT = 17,    /* split (chunked) RQI passes, reading R9d: 0 none, 1 iterations >= 3,
                           2 also every iteration of small sets (one eigenpair per CTA); 1 */
-    MR3_NPARAM = 18
+    MR3_FUSE_SCALE = 18, /* 1: every RQI CTA normalises its own Z columns when it is done;
+                            0: one k_zscale launch after the RQI phase (same arithmetic); 1 */
+    MR3_POOL_MB = 19,  /* budget for the child representations of one batch of clusters, MB
+                          (0 = automatic: min(8 GB, 15% of free memory)); clusters beyond it are
+                          processed in depth-first batches */
+    MR3_DEBUG = 20,    /* diagnostics to stderr: bit 1 dumps/histograms, 2 host sync points,
+                          4 device timeline, 8 check every launch; 0 */
+    MR3_NPARAM = 21
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
           "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10, "GRID": 11, "CTA": 12, "XPTS": 13, "YCERT": 14, "NEWTON": 15, "TWISTW": 16,
-          "SPLIT": 17}
+          "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20}
 ERRORS = {1: "NONFINITE", 2: "CUDA", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 
@@ -131,11 +131,15 @@ def _ctx(device=None, stream=None):
         raise RuntimeError("mr3: no CUDA device (the product path has no CPU fallback)")
     dev = torch.cuda.current_device() if device is None else int(device)
     st = torch.cuda.current_stream(dev) if stream is None else stream
-    key = (dev, int(st.cuda_stream))
+    # torch's default stream has handle 0 = the legacy default stream; pass it as
+    # cudaStreamLegacy (1) so the library works on it (ordered after the caller's work)
+    # instead of taking NULL = a stream of its own
+    sh = int(st.cuda_stream) or 1
+    key = (dev, sh)
     c = _ctx_cache.get(key)
     if c is None:
         h = ctypes.c_void_p()
-        rc = lib().mr3_create(ctypes.byref(h), dev, ctypes.c_void_p(int(st.cuda_stream)))
+        rc = lib().mr3_create(ctypes.byref(h), dev, ctypes.c_void_p(sh))
         if rc:
             raise MR3Error(rc, "mr3_create")
         c = h
@@ -200,8 +204,10 @@ def _solve(mode, d, e, jobz, range_, il, iu, vl, vu, w=None, Z=None):
     if w is None:
         w = torch.empty(max(n, 1), dtype=dt, device=d.device)
     if jobz == "V" and Z is None:
-        # column-major n x n: storage as (ncols, n) row-major, returned transposed
-        Zs = torch.empty((max(n, 1), max(n, 1)), dtype=dt, device=d.device)
+        # column-major n x mcap: storage as (mcap, n) row-major, returned transposed; an
+        # index range needs only its iu - il + 1 columns
+        mcap = n if range_ != "I" else max(0, min(iu, n) - max(il, 1) + 1)
+        Zs = torch.empty((max(mcap, 1), max(n, 1)), dtype=dt, device=d.device)
     else:
         Zs = Z
     m = ctypes.c_int64(0)

@@ -1,4 +1,5 @@
-// k_bisect.cuh -- K2 (batched bisection / multisection) and K3 (classification).
+// k_bisect.cuh -- K3 (classification) and helpers shared with the staged bisection
+// (k_bisect_s.cuh, K2).
 #pragma once
 #include "kernels.cuh"
 
@@ -17,203 +18,6 @@ __device__ __forceinline__ dd shfl_R<dd>(unsigned mask, dd v, int src, int width
 template <class R>
 __device__ __forceinline__ bool same(R a, R b) {
     return hi(a) == hi(b) && lo_part(a) == lo_part(b);
-}
-
-__device__ __forceinline__ void warp_add_u64(unsigned long long v, unsigned long long *dst) {
-    unsigned mask = __activemask();
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
-    // lanes of `mask` each hold a (partial) sum; only the lowest active lane adds
-    // when the mask is full, otherwise every lane adds its own (unreduced) value.
-    if (mask == 0xffffffffu) {
-        if ((threadIdx.x & 31) == 0) atomicAdd(dst, v);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2: eigenvalue approximation to relative accuracy rtol (Alg. 1 l.3
-// and l.16, L302-L304, L326-L328; Eq. (2.2); rtol = 1e-2 * gaptol,
-// L1294-L1295) by Sturm counts of the node's representation.
-//
-// A group of G lanes (G | 32) owns one eigenvalue index k: each round the
-// bracket [a, b] (count(a) < k <= count(b)) is cut into G+1 equal parts and
-// lane j counts at a + (b - a)(j+1)/(G+1); the new bracket is the part whose
-// left count is < k and right count >= k.  G = 1 is plain bisection.
-// With certify != 0 the incoming bracket (translated from the parent, Alg. 1
-// l.16) is first checked and widened until count(a) < k <= count(b).
-// The path of every index depends only on (representation, k, bracket, G).
-// ---------------------------------------------------------------------------
-// Multisection rounds of a group of G lanes on [a, b] to width <= tol.
-// Count is a functor (T x) -> count; T is the bracket type (R or double).
-template <class T, int G, class Count>
-__device__ __forceinline__ void multisect(T &a, T &b, int k, int lig, int lane, unsigned gmask,
-                                          double rtol, double absfloor, double tolmul,
-                                          unsigned long long &rows, int64_t n, Count count) {
-#pragma unroll 1
-    for (int round = 0; round < 4000; round++) {
-        T w = sub(b, a);
-        double tol = tolmul * fmax(2.0 * rtol * fmax(fabs(hi(a)), fabs(hi(b))), absfloor);
-        if (hi(w) <= tol) break;
-        T x = add(a, mul(w, (double)(lig + 1) / (double)(G + 1)));
-        bool above = lt(a, x);
-        bool below = lt(x, b);
-        int c;
-        if (above && below) {
-            c = count(x);
-            rows += n;
-        } else {
-            c = above ? k : k - 1;  // x == b counts as "right of lambda_k", x == a as left
-        }
-        bool P = c >= k;
-        unsigned bal = __ballot_sync(gmask, P);
-        bal = (bal >> (lane & ~(G - 1) & 31)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
-        int first = bal ? __ffs(bal) : G + 1;  // 1-based point index of the first P
-        T xb = shfl_R<T>(gmask, x, first <= G ? first - 1 : 0, G);
-        T xa = shfl_R<T>(gmask, x, first >= 2 ? first - 2 : 0, G);
-        T nb = first <= G ? xb : b;
-        T na = first >= 2 ? xa : a;
-        if (same(na, a) && same(nb, b)) break;  // no representable progress
-        a = na;
-        b = nb;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2: eigenvalue approximation to relative accuracy rtol (Alg. 1 l.3
-// and l.16, L302-L304, L326-L328; Eq. (2.2); rtol = 1e-2 * gaptol,
-// L1294-L1295) by Sturm counts of the node's representation.
-//
-// A group of G lanes (G | 32) owns one eigenvalue index k: each round the
-// bracket [a, b] (count(a) < k <= count(b)) is cut into G+1 equal parts and
-// lane j counts at a + (b - a)(j+1)/(G+1); the new bracket is the part whose
-// left count is < k and right count >= k.  G = 1 is plain bisection.
-//
-// XPHASE (fp64 I/O): the rounds run first in binary_x on the narrowed copy M_x
-// (L1064-L1111: "One creates a temporary copy of M_y in binary_x"; the paper's
-// double/quad solver does all approximation and refinement this way,
-// L1318-L1322) to half the target width; the result is widened by
-// delta = 8 eps_x sqrt(n) |lambda| (the M_y -> M_x perturbation, Eq. (3.8)) and
-// certified by two Sturm counts in binary_y; failed ends are widened by 8x until
-// certified, and binary_y rounds finish whatever width is left.  So every
-// returned bracket satisfies count_y(a) < k <= count_y(b) regardless of the
-// fp64 phase.  With certify != 0 the incoming bracket (translated from the
-// parent, Alg. 1 l.16) is first checked the same way.
-// The path of every index depends only on (representation, k, bracket, G).
-// ---------------------------------------------------------------------------
-template <class R, int G>
-__device__ __forceinline__ void certify_bracket(const NodeInfo &nd, R &a, R &b, int k, int lig,
-                                                unsigned gmask, double absfloor, double delta,
-                                                double pivmin, unsigned long long &rows) {
-    for (int tries = 0; tries < 200; tries++) {
-        int ca, cb;
-        if (G == 1) {
-            ca = negcount<R>(nd.rep, nd.n, a, pivmin);
-            cb = negcount<R>(nd.rep, nd.n, b, pivmin);
-            rows += 2 * nd.n;
-        } else {
-            int c = 0;
-            if (lig < 2) {
-                c = negcount<R>(nd.rep, nd.n, lig == 0 ? a : b, pivmin);
-                rows += nd.n;
-            }
-            ca = __shfl_sync(gmask, c, 0, G);
-            cb = __shfl_sync(gmask, c, 1, G);
-        }
-        if (ca < k && cb >= k) break;
-        double w = fmax(delta, fmax(absfloor, 1e-3 * fabs(hi(b)) * (tries > 2 ? 1.0 : 0.0)));
-        w = w * (double)(1ULL << (3 * (tries < 20 ? tries : 20)));
-        if (ca >= k) a = sub(a, mk<R>(w));
-        if (cb < k) b = add(b, mk<R>(w));
-    }
-}
-
-template <class R, int G, bool XPHASE>
-__global__ void __launch_bounds__(128, 6) k_bisect(const NodeInfo *__restrict__ nodes, Items it,
-                                                const int32_t *__restrict__ list, int cnt,
-                                                double rtol, double absfloor, double pivmin,
-                                                double pivmin_x, double eps_x, int certify,
-                                                DevStats *st) {
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int item = gtid / G;
-    const int lig = gtid % G;  // lane in group
-    if (item >= cnt) return;   // a whole group leaves together (G | blockDim)
-    const int lane = threadIdx.x & 31;
-    const unsigned gmask =
-        (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const int id = list[item];
-    const NodeInfo nd = nodes[it.node[id]];
-    const int k = it.k[id];
-    R a = reinterpret_cast<R *>(it.lo)[id];
-    R b = reinterpret_cast<R *>(it.hi)[id];
-    unsigned long long rows = 0, rows_x = 0;
-    const double delta0 = 8.0 * eps_x * sqrt((double)nd.n);
-
-    if (certify) certify_bracket<R, G>(nd, a, b, k, lig, gmask, absfloor, absfloor, pivmin, rows);
-    if (XPHASE) {
-        double ax = hi(a), bx = hi(b);
-        multisect<double, G>(ax, bx, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x, nd.n,
-                             [&](double x) { return negcount_x(nd.repx, nd.n, x, pivmin_x); });
-        double mag = fmax(fabs(ax), fabs(bx));
-        double delta = delta0 * mag + absfloor;
-        R na = mk<R>(ax - delta), nb = mk<R>(bx + delta);
-        // never leave the certified incoming bracket
-        if (lt(na, a)) na = a;
-        if (lt(b, nb)) nb = b;
-        a = na;
-        b = nb;
-        certify_bracket<R, G>(nd, a, b, k, lig, gmask, absfloor, delta, pivmin, rows);
-    }
-    multisect<R, G>(a, b, k, lig, lane, gmask, rtol, absfloor, 1.0, rows, nd.n,
-                    [&](R x) { return negcount<R>(nd.rep, nd.n, x, pivmin); });
-    if (lig == 0) {
-        reinterpret_cast<R *>(it.lo)[id] = a;
-        reinterpret_cast<R *>(it.hi)[id] = b;
-    }
-    if (rows) atomicAdd(&st->bisect_rows, rows);
-    if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
-}
-
-// ---------------------------------------------------------------------------
-// K2': starting points for RQI.  Each RQI step restarts inverse iteration from
-// e_r, so its error contracts like e1 ~ C e0^2 / gap; two iterations (one RQ
-// correction + the converged solve) need e0 <= gap sqrt(eps_x sqrt(n) / C).  A
-// singleton whose certified bracket is wider than that (small gaps near the
-// spectrum ends) gets x0 from a binary_x multisection on M_x to a few ulps; the
-// others keep x0 = NaN (bracket midpoint).  x0 needs no certification: the RQI
-// keeps the certified binary_y bracket as its guard.
-// ---------------------------------------------------------------------------
-template <class R, int G>
-__global__ void __launch_bounds__(128) k_refine_x0(const NodeInfo *__restrict__ nodes, Items it,
-                                                   const int32_t *__restrict__ list, int cnt,
-                                                   double eps_x, double pivmin_x, double cconv,
-                                                   DevStats *st) {
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int item = gtid / G;
-    const int lig = gtid % G;
-    if (item >= cnt) return;
-    const int lane = threadIdx.x & 31;
-    const unsigned gmask =
-        (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const int id = list[item];
-    const NodeInfo nd = nodes[it.node[id]];
-    const int k = it.k[id];
-    const R a = reinterpret_cast<R *>(it.lo)[id];
-    const R b = reinterpret_cast<R *>(it.hi)[id];
-    const double gap = fmin(it.lgap[id], it.rgap[id]);
-    const double need = gap * sqrt(eps_x * sqrt((double)nd.n) / cconv);
-    if (!(0.5 * hi(sub(b, a)) > need) || nd.n < 2) {
-        if (lig == 0) it.x0[id] = NAN;
-        return;
-    }
-    double ax = hi(a), bx = hi(b);
-    unsigned long long rows_x = 0;
-    // to a few ulps: relative 4 eps_x (multisect's tol is 2 rtol max|.|)
-    multisect<double, G>(ax, bx, k, lig, lane, gmask, 2.0 * eps_x, 1e-300, 1.0, rows_x, nd.n,
-                         [&](double x) { return negcount_x(nd.repx, nd.n, x, pivmin_x); });
-    if (lig == 0) {
-        double x = 0.5 * (ax + bx);
-        it.x0[id] = (x > hi(a) && x < hi(b)) ? x : NAN;
-    }
-    if (rows_x) atomicAdd(&st->bisect_rows_x, rows_x);
 }
 
 // ---------------------------------------------------------------------------

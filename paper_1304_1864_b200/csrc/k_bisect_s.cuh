@@ -825,8 +825,12 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
 }
 
 // K2' selection: singletons whose certified bracket half-width exceeds
-// gap sqrt(eps_x sqrt(n) / C) need a refined RQI start (see k_refine_x0 in
-// k_bisect.cuh for the argument); all others start at the bracket midpoint (x0 = NaN).
+// gap sqrt(eps_x sqrt(n) / C) need a refined RQI start: each RQI step restarts inverse
+// iteration from e_r, so its error contracts like e1 ~ C e0^2 / gap, and two iterations
+// (one RQ correction + the converged solve) need e0 <= gap sqrt(eps_x sqrt(n) / C).  The
+// selected items get x0 from a binary_x multisection on M_x (k_bisect_s, certify = 2); all
+// others start at the bracket midpoint (x0 = NaN).  x0 needs no certification: the RQI
+// keeps the certified binary_y bracket as its guard.
 // A root item whose binary_x phase ended in a Newton step dx keeps that step's estimate
 // as its start when the estimate's predicted error -- quadratic convergence, 4 dx^2 / gap
 // (the Newton constant |f''/2f'| is about 1/gap), plus 2 ulps -- is below both the

@@ -1496,7 +1496,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
                     const int hv = h[16 * u + 4 * q + b];
-                    const int d = hv == INT_MIN ? -127 : max((hv - m) >> 4, -127);
+                    const int d = hv == INT_MIN ? -127 : max((hv - m + 8) >> 4, -127);  // nearest
                     acc |= ((unsigned)d & 0xffu) << (8 * b);
                 }
                 w[q] = acc;

@@ -263,31 +263,6 @@ __device__ __forceinline__ int negcount_x(const double *__restrict__ repx, int64
     return (int)c;
 }
 
-// two shifts through the same rows (ILP 2)
-template <class R>
-__device__ __forceinline__ void negcount2(const double *__restrict__ rep, int64_t n, R x0, R x1,
-                                          double pivmin, int &c0, int &c1) {
-    R s0 = neg(x0), s1 = neg(x1);
-    c0 = 0;
-    c1 = 0;
-    Row2<R> cur = load_row2<R>(rep, 0);
-#pragma unroll 1
-    for (int64_t j = 0; j < n - 1; j++) {
-        Row2<R> nxt = load_row2<R>(rep, j + 1);
-        R dp0 = guard(add(cur.d, s0), pivmin);
-        R dp1 = guard(add(cur.d, s1), pivmin);
-        c0 += is_neg(dp0) ? 1 : 0;
-        c1 += is_neg(dp1) ? 1 : 0;
-        s0 = sub(mul(cur.lld, div(s0, dp0)), x0);
-        s1 = sub(mul(cur.lld, div(s1, dp1)), x1);
-        cur = nxt;
-    }
-    R dp0 = guard(add(cur.d, s0), pivmin);
-    R dp1 = guard(add(cur.d, s1), pivmin);
-    c0 += is_neg(dp0) ? 1 : 0;
-    c1 += is_neg(dp1) ? 1 : 0;
-}
-
 // ---------------------------------------------------------------------------
 // counter-based generator for the root perturbation (PAPER.md L901-L909,
 // footnote: "any (fixed) sequence of pseudo-random numbers can be used"):

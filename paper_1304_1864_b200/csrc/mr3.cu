@@ -101,9 +101,9 @@ static void hsync_note(mr3_ctx ctx, const char *where) {
 }
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0},
 };
 
 #define CK(call)                                                                  \
@@ -318,6 +318,11 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     if (world < 1 || rank < 0 || rank >= world) return -11;
     if (n > 0x7fffffffLL) return -3;
     ctx->mode = mode;
+    // MR3_DEBUG bits: 1 = dumps and histograms, 2 = host sync points, 4 = device timeline,
+    // 8 = synchronise after every launch
+    ctx->debug = (int)P[MR3_DEBUG];
+    ctx->dump = (ctx->debug & 1) ? (ctx->debug > 15 ? ctx->debug : 40) : 0;
+    ctx->fuse_scale = P[MR3_FUSE_SCALE] != 0.0 ? 1 : 0;
     ctx->range = range;
     ctx->n = n;
     ctx->d = d;
@@ -336,6 +341,9 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     }
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
+    // the previous solve's side-stream work (root PP rows) reads rep_pool and writes nodes[]:
+    // it must be complete before this plan rewrites them
+    CK(cudaStreamWaitEvent(s, ctx->ev_pp, 0));
     KTime *t_root = kt_begin(ctx, "k_root");
 
     // K1a: norm, Gershgorin, finiteness
@@ -723,8 +731,9 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             if (ht > 0) {
                 // to the RQI-start precision (2 ulps) at once: the midpoints are the starts
                 // and the refinement pass (K2') has nothing left to do for these items
-                int G = choose_groups(ctx, ht, 0);
-                if (G < 8) G = 8;
+                // (a fixed lane count: the bits of a bracket must not depend on how many
+                // items this rank's slice sent to the tail)
+                const int G = 32;
                 rc = launch_bisect<R>(ctx, W, tl, ht, G, 2.0 * eps_x, absfloor, 0, true, eps_x,
                                       "k_bisect", 0, nullptr);
             }
@@ -780,6 +789,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     W.nodes = (NodeInfo *)ctx->bufs["nodes"].p;
     W.st = (DevStats *)ctx->bufs["devstats"].p;
     double *dbrk = (double *)ctx->bufs["brk"].p;
+    // the root's PP rows (side stream, overlapping the plan's grid and bisection) are joined
+    // here: everything below may read or copy nodes[] (node-table growth, RQI)
+    CK(cudaStreamWaitEvent(s, ctx->ev_pp, 0));
     // per-execute counters (bisect_rows of the plan is kept)
     CK(cudaMemsetAsync((char *)W.st + offsetof(DevStats, rqi_rows), 0,
                        sizeof(DevStats) - offsetof(DevStats, rqi_rows), s));
@@ -971,7 +983,6 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     auto run_rqi = [&](const int32_t *list, int ncount) -> int {
         if (ncount <= 0) return 0;
         int rc2 = 0;
-        CK(cudaStreamWaitEvent(s, ctx->ev_pp, 0));  // the root's PP rows (side stream)
         if (P[MR3_REFINE] > 0) {  // K2': binary_x starting points for small-gap singletons
             char *flags = (char *)getbuf(ctx, "ref_flags", (size_t)ncount, &rc2);
             int32_t *rlist = (int32_t *)getbuf(ctx, "ref_list", (size_t)ncount * 4, &rc2);
@@ -993,8 +1004,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             if (ctx->dump) fprintf(stderr, "[mr3] refine: %d of %d singletons\n", hr, ncount);
             if (hr > 0) {
                 // many lanes per item: few items, short dependent chains (log2(G+1) bits/round)
-                int G = choose_groups(ctx, hr, 0);
-                if (G < 16) G = 16;
+                // (fixed lane count: independent of the rank-local number of items)
+                const int G = 32;
                 rc2 = launch_bisect<R>(ctx, W, rlist, hr, G, 2.0 * eps_x, 1e-300, 2, true, eps_x,
                                        "k_refine_x0", 1, nullptr, ctx->root_widen);
                 if (rc2) return rc2;
@@ -1224,101 +1235,154 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         }
     };
 
-    // level loop (Alg. 1 l.5-17, breadth-first)
-    int level = 0;
-    int32_t *cur = listA, *nxt = listB;
+    // Tree traversal (Alg. 1 l.5-17).  Level 0 is one batch; the clusters of a level are
+    // processed breadth-first in batches (one launch per kernel for all clusters of a batch,
+    // reading R12) whose child representations fit the pool budget (MR3_POOL_MB); batches
+    // are taken depth-first from a stack, so a batch's subtree is finished before the next
+    // batch of its level reuses the level's pool (depth-first keeps the
+    // memory at O((depth + batch) n) instead of O(clusters n), SPEC memory contract).
+    struct Frontier {
+        int level;                       // depth of the member items' nodes
+        std::vector<int32_t> cb, ce, mem;  // clusters [cb, ce) into mem (item ids)
+    };
+    std::vector<Frontier> stack;
+    auto push_clusters = [&](int lvl, int nc, int nm) -> int {
+        if (nc <= 0) return 0;
+        Frontier F;
+        F.level = lvl;
+        F.cb.resize(nc);
+        F.ce.resize(nc);
+        F.mem.resize(nm);
+        CK(cudaMemcpyAsync(F.cb.data(), cbeg, nc * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(F.ce.data(), cend, nc * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(F.mem.data(), listB, nm * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        hsync_note(ctx, "sync#14");
+        stack.push_back(std::move(F));
+        return 0;
+    };
     const int maxdepth = (int)P[MR3_MAX_DEPTH];
     const double elg1 = P[MR3_ELG_MAX];
     const double elg2 = std::max(10.0, eps_x / (eps_y * std::sqrt((double)ctx->n)));
-    int Gc = P[MR3_GROUPS] > 0 ? choose_groups(ctx, 0, (int)P[MR3_GROUPS]) : 8;
-    while (true) {
-        if (nsing > 0) {
-            rc = run_rqi(singles, nsing);
-            if (rc) return rc;
+    const int Gc = P[MR3_GROUPS] > 0 ? choose_groups(ctx, 0, (int)P[MR3_GROUPS]) : 8;
+    // child pool budget: rep (4 R) + M_x (2 doubles) + PP rows per row and cluster
+    const size_t row_bytes = (size_t)4 * words * 8 + 16 + (size_t)PP_STRIDE * 8;
+    size_t pool_budget = P[MR3_POOL_MB] > 0 ? (size_t)(P[MR3_POOL_MB] * 1048576.0)
+                                            : std::min<size_t>((size_t)8 << 30, (size_t)(freeb * 0.15));
+    const int64_t batch_max =
+        std::max<int64_t>(1, (int64_t)(pool_budget / std::max<size_t>(1, row_bytes * (size_t)ctx->n)));
+    int dmax = 0;
+    if (nsing > 0) {
+        rc = run_rqi(singles, nsing);
+        if (rc) return rc;
+    }
+    if ((rc = push_clusters(0, nclus, nmem))) return rc;
+    while (!stack.empty()) {
+        Frontier F = std::move(stack.back());
+        stack.pop_back();
+        const int nc = (int)F.cb.size();
+        if (nc > batch_max) {  // split into batches (pushed in reverse: taken in order)
+            std::vector<Frontier> parts;
+            for (int c0b = 0; c0b < nc; c0b += (int)batch_max) {
+                const int c1b = (int)std::min<int64_t>(nc, c0b + batch_max);
+                Frontier Q;
+                Q.level = F.level;
+                const int m0 = F.cb[c0b];
+                for (int c = c0b; c < c1b; c++) {
+                    Q.cb.push_back(F.cb[c] - m0);
+                    Q.ce.push_back(F.ce[c] - m0);
+                }
+                Q.mem.assign(F.mem.begin() + m0, F.mem.begin() + F.ce[c1b - 1]);
+                parts.push_back(std::move(Q));
+            }
+            for (auto it2 = parts.rbegin(); it2 != parts.rend(); ++it2) stack.push_back(std::move(*it2));
+            continue;
         }
-        ctx->stats.levels = level + 1;
-        if (nclus == 0) break;
-        if (level + 1 > maxdepth) {
-            // depth cap: the remaining cluster members get the bisection
-            // fallback + one solve each (the RQI kernel's fallback path)
+        const int nm = (int)F.mem.size();
+        CK(cudaMemcpyAsync(listB, F.mem.data(), nm * 4, cudaMemcpyHostToDevice, s));
+        if (F.level + 1 > maxdepth) {
+            // depth cap: the members get the bisection fallback + one solve each (the RQI
+            // kernel's fallback path)
             double saved = ctx->cfg[mode].v[MR3_MAX_RQI];
             ctx->cfg[mode].v[MR3_MAX_RQI] = 0;
             P = ctx->cfg[mode].v;
-            rc = run_rqi(nxt, nmem);
+            rc = run_rqi(listB, nm);
             ctx->cfg[mode].v[MR3_MAX_RQI] = saved;
             P = ctx->cfg[mode].v;
             if (rc) return rc;
-            break;
+            continue;
         }
+        CK(cudaMemcpyAsync(cbeg, F.cb.data(), nc * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(cend, F.ce.data(), nc * 4, cudaMemcpyHostToDevice, s));
         // K4: child representations (new nodes)
-        if (ctx->nodes_used + nclus > ctx->node_cap) {
+        if (ctx->nodes_used + nc > ctx->node_cap) {
             // grow the node table (keep contents)
-            int newcap = std::max(ctx->node_cap * 2, ctx->nodes_used + nclus + 64);
+            int newcap = std::max(ctx->node_cap * 2, ctx->nodes_used + nc + 64);
             NodeInfo *nn = nullptr;
             CK(cudaMalloc(&nn, newcap * sizeof(NodeInfo)));
             CK(cudaMemcpyAsync(nn, W.nodes, ctx->nodes_used * sizeof(NodeInfo),
                                cudaMemcpyDeviceToDevice, s));
-            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#14");
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#15");
             cudaFree(ctx->bufs["nodes"].p);
             ctx->bufs["nodes"].p = nn;
             ctx->bufs["nodes"].cap = newcap * sizeof(NodeInfo);
             ctx->node_cap = newcap;
             W.nodes = nn;
         }
-        std::string pname = "child_pool" + std::to_string(level);
-        double *pool =
-            (double *)getbuf(ctx, pname, (size_t)nclus * ctx->n * 4 * words * 8, &rc);
-        double *poolx =
-            (double *)getbuf(ctx, pname + "x", ((size_t)nclus * ctx->n + XPAD) * 16, &rc);
+        // pool of this level (children of depth level + 1); reused by the level's later batches
+        std::string pname = "child_pool" + std::to_string(F.level);
+        double *pool = (double *)getbuf(ctx, pname, (size_t)nc * ctx->n * 4 * words * 8, &rc);
+        double *poolx = (double *)getbuf(ctx, pname + "x", ((size_t)nc * ctx->n + XPAD) * 16, &rc);
+        double *ppc = (double *)getbuf(ctx, pname + "pp", (size_t)nc * ctx->n * PP_STRIDE * 8, &rc);
         if (rc) return rc;
-        CK(cudaMemsetAsync(poolx + 2 * (size_t)nclus * ctx->n, 0, XPAD * 16, s));
+        CK(cudaMemsetAsync(poolx + 2 * (size_t)nc * ctx->n, 0, XPAD * 16, s));
         double *cdbg = nullptr;
-        if (ctx->dump) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nclus * 32, &rc);
+        if (ctx->dump) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nc * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
-        k_child<R><<<nclus, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, nxt, cbeg, cend, nclus,
-                                        pool, poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin,
-                                        W.st, cdbg);
+        k_child<R><<<nc, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, listB, cbeg, cend, nc, pool,
+                                     poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st,
+                                     cdbg);
         kt_end(ctx, tch);
         CKL("k_child");
         if (ctx->dump) {
-            std::vector<double> hd(4 * nclus);
+            std::vector<double> hd(4 * nc);
             cudaStreamSynchronize(s);
-            cudaMemcpy(hd.data(), cdbg, nclus * 32, cudaMemcpyDeviceToHost);
-            for (int c = 0; c < nclus && c < ctx->dump; c++)
+            cudaMemcpy(hd.data(), cdbg, nc * 32, cudaMemcpyDeviceToHost);
+            for (int c = 0; c < nc && c < ctx->dump; c++)
                 fprintf(stderr, "[mr3] child %d: lane %g growth %.3g delta %.3g tau %.17g\n", c,
                         hd[4 * c], hd[4 * c + 1], hd[4 * c + 2], hd[4 * c + 3]);
         }
-        {
-            double *ppc = (double *)getbuf(ctx, pname + "pp", (size_t)nclus * ctx->n * PP_STRIDE * 8,
-                                           &rc);
-            if (rc) return rc;
-            k_node_pp<R><<<nclus, 256, 0, s>>>(W.nodes, ctx->nodes_used, ppc, ctx->n, 0);
-            CKL("k_node_pp");
-        }
-        ctx->nodes_used += nclus;
-        dump("after child", nxt, nmem, level + 1);
+        k_node_pp<R><<<nc, 256, 0, s>>>(W.nodes, ctx->nodes_used, ppc, ctx->n, 0);
+        CKL("k_node_pp");
+        ctx->nodes_used += nc;
+        dump("after child", listB, nm, F.level + 1);
         // K2: refine in the child coordinates (certified)
-        rc = launch_bisect<R>(ctx, W, nxt, nmem, Gc, rtol, absfloor, 1,
+        rc = launch_bisect<R>(ctx, W, listB, nm, Gc, rtol, absfloor, 1,
                               words == 2 && P[MR3_XPHASE] != 0, eps_x);
         if (rc) return rc;
-        dump("after refine", nxt, nmem, level + 1);
-        // K3: classify the members
-        std::swap(cur, nxt);
-        so.next_active = nxt;
+        dump("after refine", listB, nm, F.level + 1);
+        // K3: classify the members (singletons, clusters with members in listB)
+        CK(cudaMemcpyAsync(listA, listB, nm * 4, cudaMemcpyDeviceToDevice, s));
+        so.next_active = listB;
         KTime *tc2 = kt_begin(ctx, "k_classify");
-        k_classify<R><<<1, 1024, 0, s>>>(W.it, cur, nmem, gaptol, so);
+        k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, nm, gaptol, so);
         kt_end(ctx, tc2);
         CKL("k_classify");
         CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#15");
-        nsing = hc[0];
-        nclus = hc[1];
-        nmem = hc[2];
-        level++;
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#16");
+        const int ns2 = hc[0], nc2 = hc[1], nm2 = hc[2];
+        dmax = std::max(dmax, F.level + 1);
         if (ctx->dump)
-            fprintf(stderr, "[mr3] level %d: %d singles %d clusters %d members\n", level, nsing,
-                    nclus, nmem);
+            fprintf(stderr, "[mr3] level %d batch: %d singles %d clusters %d members\n",
+                    F.level + 1, ns2, nc2, nm2);
+        if (ns2 > 0) {
+            rc = run_rqi(singles, ns2);
+            if (rc) return rc;
+        }
+        if ((rc = push_clusters(F.level + 1, nc2, nm2))) return rc;
     }
+    const int level = dmax;
+    ctx->stats.levels = dmax + 1;
     if (ctx->dump && ctx->bufs.count("rqi_sorted") && ctx->n > 1) {
         // twist-index distribution (r / n in 10 bins) and spread per 128-run of the sorted list
         cudaStreamSynchronize(s);
@@ -1429,14 +1493,6 @@ int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
     }
     cudaEventRecord(ctx->ev_pp, ctx->side);  // (completed: nothing to wait for before a plan)
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
-    const char *dbg = getenv("MR3_DEBUG");
-    ctx->debug = dbg ? atoi(dbg) : 0;
-    {
-        const char *fz = getenv("MR3_FUSE_SCALE");
-        ctx->fuse_scale = fz ? (atoi(fz) != 0) : 1;
-    }
-    // MR3_DEBUG bits: 1 = dumps and histograms, 2 = host sync points, 4 = device timeline
-    ctx->dump = (ctx->debug & 1) ? (ctx->debug > 8 ? ctx->debug : 40) : 0;
     *out = ctx;
     return 0;
 }
@@ -1445,13 +1501,13 @@ int mr3_destroy(mr3_ctx ctx) {
     if (!ctx) return 0;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->side);  // (its kernels read the buffers freed below)
     for (auto &b : ctx->bufs)
         if (b.second.p) cudaFree(b.second.p);
     for (auto &t : ctx->kt) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
     }
-    cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
     cudaEventDestroy(ctx->ev_root);
     cudaEventDestroy(ctx->ev_pp);

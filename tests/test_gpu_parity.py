@@ -402,3 +402,54 @@ def test_rare_paths_parity(params):
         assert_parity(res)
         if params.get("MAX_RQI") == 1 and not p.name.startswith("glued"):
             assert st["rqi_fallbacks"] > 0
+
+
+@pytest.mark.parametrize("make", [lambda: synth.legendre(3000), lambda: synth.random_uniform(1500, 3),
+                                  lambda: synth.random_uniform(700, 8),
+                                  lambda: synth.glued_wilkinson(30, 21)])
+@pytest.mark.parametrize("params", [{"GROUPS": 1}, {"GROUPS": 1, "NEWTON": 1}])
+def test_newton_path_parity(make, params):
+    """The bench workload's own bisection path -- one lane per eigenvalue, the
+    Newton/Laguerre-accelerated binary_x phase (R8e) and its multisection tail -- which the
+    automatic lane choice takes only above ~19k items, forced at small n (GROUPS = 1) and
+    checked against the oracle on every pair."""
+    p = make()
+    w, Z, st = _with_params(params, lambda: run(p))
+    assert st["newton_rows_x"] > 0, st  # the Newton passes really ran
+    res = check_solution(p, w, Z, np.arange(1, p.n + 1))
+    assert_parity(res)
+
+
+def test_fused_scale_off_bitwise():
+    """MR3_FUSE_SCALE = 0 (one k_zscale launch after the RQI phase) computes exactly what the
+    fused epilogue of k_rqi computes: same bits."""
+    for p in (synth.random_uniform(900, 2), synth.glued_wilkinson(12, 21),
+              synth.random_normal_f32(1200, 3, 1, 200)):
+        w1, Z1, _ = run(p)
+        w0, Z0, _ = _with_params({"FUSE_SCALE": 0}, lambda: run(p))
+        np.testing.assert_array_equal(w1, w0)
+        np.testing.assert_array_equal(Z1, Z0)
+
+
+@pytest.mark.parametrize("make", [lambda: synth.glued_wilkinson(12, 21),
+                                  lambda: synth.glued_wilkinson(40, 21)])
+def test_pool_batches_bitwise(make):
+    """Clusters processed in depth-first batches (child-pool budget MR3_POOL_MB forced to one
+    cluster per batch) give the same eigenpairs, bit for bit, as one batch per level."""
+    p = make()
+    w1, Z1, s1 = run(p)
+    w0, Z0, s0 = _with_params({"POOL_MB": 1e-9}, lambda: run(p))
+    assert s1["n_clusters"] == s0["n_clusters"] and s1["d_max"] == s0["d_max"] >= 1
+    np.testing.assert_array_equal(w1, w0)
+    np.testing.assert_array_equal(Z1, Z0)
+    res = check_solution(p, w0, Z0, np.arange(1, p.n + 1))
+    assert_parity(res)
+
+
+def test_index_range_z_columns():
+    """An index range allocates and returns exactly iu - il + 1 columns."""
+    p = synth.random_uniform(800, 6)
+    w, Z, _ = run(p, rng="I", il=101, iu=164)
+    assert Z.shape == (800, 64) and w.shape == (64,)
+    assert_parity(check_solution(p, w, Z, np.arange(101, 165)))
+
