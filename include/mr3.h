@@ -103,7 +103,9 @@ enum mr3_param {
                           processed in depth-first batches */
     MR3_DEBUG = 20,    /* diagnostics to stderr: bit 1 dumps/histograms, 2 host sync points,
                           4 device timeline, 8 check every launch; 0 */
-    MR3_NPARAM = 21
+    MR3_RQI_FB = 21,   /* 1: RQI iterations 1-2 with the two halves of every factorization in
+                          two threads (k_rqi_fb), later iterations in k_rqi; 0: all in k_rqi; 1 */
+    MR3_NPARAM = 22
 };
 
 /* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a

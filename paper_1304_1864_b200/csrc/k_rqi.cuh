@@ -50,6 +50,15 @@ constexpr int RQ_HALO = 8;   // rows staged below a tile (the sweeps need row t0
 constexpr int RQ_TPB = 128;  // threads per CTA
 
 
+// state of an eigenpair handed from k_rqi_fb (iterations 1-2) to k_rqi (later iterations)
+template <class R>
+struct RqiResume {
+    R lam, a, b, lam_out;  // current shift, guard bracket, converged eigenvalue (if done)
+    int32_t iters;         // passes done
+    int32_t erefF, erefB;  // scale references of the product-form z (k_zprod.cuh)
+    int32_t flags;         // 1: converged, 2: z of the converged shift written
+};
+
 template <class R>
 struct RqiArgs {
     const NodeInfo *nodes;
@@ -76,6 +85,10 @@ struct RqiArgs {
     int32_t *dbg_iters;  // optional (MR3_DEBUG): iterations per item
     double *dbg_trace;   // optional (MR3_DEBUG): 8 per item: x0 used, gap, r, res/tol per iteration
     unsigned long long *dbg_clk;  // optional (MR3_DEBUG): 4 per CTA: start, end (ns), rmin, rmax
+    char *left;                   // k_rqi_fb: per list position, 1 = continue in k_rqi
+    RqiResume<R> *resume;         // k_rqi_fb: per item id, state of the eigenpairs left
+    const RqiResume<R> *resume_in;  // k_rqi: nullptr = fresh start, else continue from it
+    int iter0;                    // k_rqi with resume_in: passes already done (uniform)
 };
 
 __device__ __forceinline__ unsigned long long gtimer_ns() {
@@ -354,6 +367,17 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     if (zcol != nullptr && n == 1) {  // 1x1 block: z = e_1
         zcol[0] = (OutT)1.0;
         zfinal = true;
+    }
+    if (active && A.resume_in != nullptr) {  // continue after k_rqi_fb's passes
+        const RqiResume<R> rs = A.resume_in[id];
+        lam = rs.lam;
+        a = rs.a;
+        b = rs.b;
+        lam_out = rs.lam_out;
+        erefF = rs.erefF;
+        erefB = rs.erefB;
+        done = (rs.flags & 1) != 0;
+        zfinal = (rs.flags & 2) != 0;
     }
 
     // one twisted factorization at lam for the threads with `need`
@@ -1000,7 +1024,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     };
 
 #pragma unroll 1
-    for (iters = 1; iters <= A.maxit; iters++) {
+    for (iters = A.iter0 + 1; iters <= A.maxit; iters++) {
         // an eigenpair that converged in the first (non-storing) pass joins the next
         // pass of its CTA at the same shift to write z (instead of an extra pass later)
         const bool store_only =

@@ -25,6 +25,7 @@
 #include "k_child.cuh"
 #include "k_misc.cuh"
 #include "k_rqi.cuh"
+#include "k_rqi_fb.cuh"
 #include "kernels.cuh"
 
 using namespace mr3;
@@ -101,9 +102,9 @@ static void hsync_note(mr3_ctx ctx, const char *where) {
 }
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG FB
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0},
 };
 
 #define CK(call)                                                                  \
@@ -1052,8 +1053,10 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         // pass of all 128 threads (R9d) -- the serial n-row chains would leave the GPU idle
         const bool split_all = P[MR3_SPLIT] >= 2 && ncount <= ctx->nsm * 16;
         bool rqi_split_all = false;  // (set for the k_rqi launch, read by launch_chunks)
-        auto make_tasks = [&](const int32_t *lst, int *nt, int per) -> int {
-            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, ncount, W.it.node, dseg, dtasks, dnt, per);
+        const RqiResume<R> *rqi_resume_in = nullptr;  // (k_rqi continuing after k_rqi_fb)
+        int rqi_iter0 = 0;
+        auto make_tasks = [&](const int32_t *lst, int *nt, int per, int count) -> int {
+            k_rqi_tasks<<<1, 1024, 0, s>>>(lst, count, W.it.node, dseg, dtasks, dnt, per);
             cudaError_t e2 = cudaGetLastError();
             if (e2 != cudaSuccess) {
                 ctx->err = std::string("k_rqi_tasks: ") + cudaGetErrorString(e2);
@@ -1110,6 +1113,10 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.dbg_iters = nullptr;
                 A.dbg_trace = nullptr;
                 A.dbg_clk = nullptr;
+                A.left = nullptr;
+                A.resume = nullptr;
+                A.resume_in = locate ? nullptr : rqi_resume_in;
+                A.iter0 = locate ? 0 : rqi_iter0;
                 if (ctx->dump && !locate) {
                     A.dbg_clk = (unsigned long long *)getbuf(ctx, "dbg_clk", (size_t)nb * 32, &rc3);
                     cudaMemsetAsync(A.dbg_clk, 0, (size_t)nb * 32, s);
@@ -1189,7 +1196,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         // K5a: twist indices in binary_x, then group the singletons by (node, r) so
         // that the CTAs of the fixed-twist iterations sweep nearly equal row ranges
         int ntasks = 0;
-        if ((rc2 = make_tasks(list, &ntasks, rtpb))) return rc2;
+        if ((rc2 = make_tasks(list, &ntasks, rtpb, ncount))) return rc2;
         if ((rc2 = launch_chunks(true, list, ntasks))) return rc2;
         k_twist_keys<<<(ncount + 255) / 256, 256, 0, s>>>(list, ncount, W.it.node, W.it.twist,
                                                           tkeys, tvals);
@@ -1204,9 +1211,76 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                                             ncount, 0, 64, s);
             CKL("radix sort (twist)");
         }
-        if ((rc2 = make_tasks(slist, &ntasks, split_all ? 1 : rtpb))) return rc2;
-        rqi_split_all = split_all;
-        return launch_chunks(false, slist, ntasks);
+        if (split_all || P[MR3_RQI_FB] == 0) {  // every iteration in k_rqi
+            if ((rc2 = make_tasks(slist, &ntasks, split_all ? 1 : rtpb, ncount))) return rc2;
+            rqi_split_all = split_all;
+            return launch_chunks(false, slist, ntasks);
+        }
+        // K5 main phase: iterations 1-2 with the F and B halves in two threads (k_rqi_fb);
+        // the eigenpairs it leaves continue in k_rqi from their saved state
+        char *left = (char *)getbuf(ctx, "rqi_left", (size_t)ncount, &rc2);
+        int32_t *llist = (int32_t *)getbuf(ctx, "rqi_llist", (size_t)ncount * 4, &rc2);
+        int *lcnt = (int *)getbuf(ctx, "rqi_lcnt", 16, &rc2);
+        RqiResume<R> *resume =
+            (RqiResume<R> *)getbuf(ctx, "rqi_resume", (size_t)cnt * sizeof(RqiResume<R>), &rc2);
+        if (rc2) return rc2;
+        if ((rc2 = make_tasks(slist, &ntasks, FB_NP, ncount))) return rc2;
+        {
+            RqiArgs<R> A;
+            memset(&A, 0, sizeof(A));
+            A.nodes = W.nodes;
+            A.it = W.it;
+            A.list = slist;
+            A.tasks = dtasks;
+            A.zc = dzc;
+            A.pivmin = ctx->pivmin;
+            A.krs = P[MR3_KRS];
+            A.eps_x = eps_x;
+            A.gaptol = gaptol;
+            A.root_widen = ctx->root_widen;
+            A.twist_w = P[MR3_TWISTW];
+            A.fuse_scale = ctx->fuse_scale;
+            A.maxit = (int)P[MR3_MAX_RQI];
+            A.jobz_v = jobz == 'V';
+            A.w = w;
+            A.Z = Z;
+            A.ldz = ldz;
+            A.zcol0 = c0;
+            A.unscale = 1.0 / ctx->scale;
+            A.st = W.st;
+            A.left = left;
+            A.resume = resume;
+            if (ctx->dump) A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc2);
+            constexpr size_t smem = fb_smem_bytes<R, OutT>();
+            static bool attr_fb = false;  // per instantiation, once per process
+            if (!attr_fb) {
+                cudaFuncSetAttribute(k_rqi_fb<R, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                attr_fb = true;
+            }
+            KTime *t = kt_begin(ctx, "k_rqi");
+            k_rqi_fb<R, OutT><<<ntasks, FB_TPB, smem, s>>>(A);
+            kt_end(ctx, t);
+            CKL("k_rqi_fb");
+        }
+        size_t tmpl = 0;
+        cub::DeviceSelect::Flagged(nullptr, tmpl, slist, left, llist, lcnt, ncount, s);
+        void *tmp = getbuf(ctx, "cubtmp_left", tmpl, &rc2);
+        if (rc2) return rc2;
+        cub::DeviceSelect::Flagged(tmp, tmpl, slist, left, llist, lcnt, ncount, s);
+        CKL("select (rqi left)");
+        int hl = 0;
+        CK(cudaMemcpyAsync(&hl, lcnt, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#13b");
+        if (ctx->dump) fprintf(stderr, "[mr3] k_rqi_fb left %d of %d eigenpairs\n", hl, ncount);
+        if (hl == 0) return 0;
+        if ((rc2 = make_tasks(llist, &ntasks, rtpb, hl))) return rc2;
+        rqi_resume_in = resume;
+        rqi_iter0 = std::min(2, (int)P[MR3_MAX_RQI]);
+        rc2 = launch_chunks(false, llist, ntasks);
+        rqi_resume_in = nullptr;
+        rqi_iter0 = 0;
+        return rc2;
     };
 
     auto dump = [&](const char *tag, const int32_t *list, int cntl, int lvl) {

@@ -453,3 +453,21 @@ def test_index_range_z_columns():
     assert Z.shape == (800, 64) and w.shape == (64,)
     assert_parity(check_solution(p, w, Z, np.arange(101, 165)))
 
+
+@pytest.mark.parametrize("make", [lambda: synth.random_uniform(1200, 1), lambda: synth.legendre(3000),
+                                  lambda: synth.glued_wilkinson(20, 21),
+                                  lambda: synth.random_normal_f32(3000, 4, 1, 700),
+                                  lambda: synth.split_matrix(500, 5, split_at=(100, 101, 333))])
+@pytest.mark.parametrize("params", [{}, {"MAX_RQI": 1}, {"KRS": 1e-4}, {"GROUPS": 1}])
+def test_rqi_fb_matches_single_thread_rqi(make, params):
+    """k_rqi_fb (the two halves of every twisted factorization in two threads, iterations 1-2,
+    then k_rqi from the saved state) computes exactly what k_rqi alone computes (MR3_RQI_FB = 0):
+    same bits, including eigenpairs continued after the hand-off (KRS = 1e-4 forces third
+    iterations, MAX_RQI = 1 the bisection fallback)."""
+    p = make()
+    w1, Z1, s1 = _with_params(params, lambda: run(p))
+    w0, Z0, s0 = _with_params(dict(params, RQI_FB=0), lambda: run(p))
+    np.testing.assert_array_equal(w1, w0)
+    np.testing.assert_array_equal(Z1, Z0)
+    assert s1["rqi_fallbacks"] == s0["rqi_fallbacks"]
+
