@@ -42,6 +42,8 @@ typedef struct mr3_ctx_s *mr3_ctx;
 #define MR3_OK 0
 #define MR3_ERR_NONFINITE 1 /* NaN or Inf in d or e */
 #define MR3_ERR_CUDA 2      /* a CUDA runtime error (mr3_last_error_string) */
+#define MR3_ERR_NCCL 3      /* a collective failed (NCCL error, exchange callback error, or
+                               world > 1 with neither a communicator nor a callback) */
 #define MR3_ERR_NOMEM 4     /* device allocation failed */
 #define MR3_ERR_NOCONV 5    /* reserved: the fallbacks are total */
 #define MR3_ERR_ZCAP 6      /* two-phase form: Z has fewer columns than needed */
@@ -108,9 +110,20 @@ enum mr3_param {
     MR3_NPARAM = 22
 };
 
-/* one context per (device, stream).  cuda_stream: cudaStream_t or NULL for a
- * stream owned by the context. */
-int mr3_create(mr3_ctx *ctx, int device, void *cuda_stream);
+/*
+ * One context per (device, stream, rank).
+ *   cuda_stream: the cudaStream_t all work is ordered on (cudaStreamLegacy = (void *)1 for the
+ *                legacy default stream); NULL = a non-blocking stream owned by the context,
+ *                which is NOT ordered after the caller's other work -- the caller must
+ *                synchronise its inputs first.
+ *   nccl_comm:   an ncclComm_t spanning `world` ranks (one GPU each; this process is `rank`)
+ *                or NULL.  With world > 1 the one-call solvers below exchange the bracket
+ *                records and the eigenvalues with ncclAllGather on it (NCCL is loaded
+ *                lazily, libnccl.so.2, the first time a communicator is used), unless an
+ *                exchange callback is installed (mr3_set_exchange).  world = 1: single GPU.
+ * Errors: -1 ctx NULL, -5 rank/world invalid, MR3_ERR_CUDA.
+ */
+int mr3_create(mr3_ctx *ctx, int device, void *cuda_stream, void *nccl_comm, int rank, int world);
 int mr3_destroy(mr3_ctx ctx);
 /* mode 0: fp64 I/O (double-double internal), mode 1: fp32 I/O (fp64 internal).
  * Parameters are stored per mode; a negative value restores the default. */
@@ -118,21 +131,50 @@ int mr3_set_param(mr3_ctx ctx, int mode, int which, double value);
 double mr3_get_param(mr3_ctx ctx, int mode, int which);
 
 /*
+ * In-place all-gather used by the one-call solvers when world > 1 (instead of NCCL): buf is a
+ * DEVICE buffer of world slices of bytes_per_rank bytes; this rank's slice (offset
+ * rank * bytes_per_rank) is valid on entry, all slices on return.  Work before the call is
+ * ordered on `stream` (cudaStream_t); the callback must leave buf complete in stream order
+ * (e.g. synchronise, copy through the host, or enqueue its own collective).  Returns 0 or
+ * nonzero (-> MR3_ERR_NCCL).  fn = NULL removes the callback.
+ */
+typedef int (*mr3_allgather_fn)(void *user, void *buf, size_t bytes_per_rank, int rank, int world,
+                                void *stream);
+int mr3_set_exchange(mr3_ctx ctx, mr3_allgather_fn fn, void *user);
+
+/* NCCL helpers (libnccl.so.2 loaded lazily): a unique id (128 bytes, rank 0 creates it and
+ * the caller broadcasts it), a communicator of `world` ranks on `device`, and its release.
+ * Return 0 or MR3_ERR_NCCL. */
+int mr3_nccl_unique_id(void *id128);
+int mr3_nccl_comm_init(void **comm, const void *id128, int rank, int world, int device);
+int mr3_nccl_comm_destroy(void *comm);
+
+/*
  * fp64 I/O, double-double internal (the "double/quadruple" solver of L1318-L1326).
  *   jobz : 'V' eigenvalues and eigenvectors, 'N' eigenvalues only
  *   range: 'A' all; 'I' indices il..iu (1-based, inclusive); 'V' vl < lambda <= vu
- *   d[n], e[n-1]: device; w[n]: device output (first *m entries valid, ascending);
- *   Z: device output, column-major, ldz >= n, at least *m columns (may be NULL
- *   when jobz = 'N').  *m: number of eigenvalues found.
+ *   d[n], e[n-1]: device inputs (the same on every rank).
+ *   *m: number of eigenvalues found (globally).
+ *   w[n]: device output, the first *m entries ascending -- all of them on every rank.
+ *   Z: device output, column-major, ldz >= n, zcap columns allocated (may be NULL when
+ *   jobz = 'N'): this rank's columns [*zcol_begin, *zcol_end) of the global m, at local
+ *   positions 0 .. *zcol_end - *zcol_begin - 1.  Single GPU (world = 1): all m columns.
+ *   With world > 1 the index set is partitioned over the ranks of the context (SURVEY.md
+ *   8(e): replicated root, static-slice bisection, all-gather of the bracket records,
+ *   identical classification, cluster-whole column ranges, all-gather of w); zcap below the
+ *   rank's column count returns MR3_ERR_ZCAP with the range filled in (size Z from it, or
+ *   use the two-phase form mr3_plan / mr3_execute).
  */
 int mr3_dstemr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d, const double *e,
                   double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
-                  int64_t ldz, mr3_stats *stats);
+                  int64_t ldz, int64_t zcap, int64_t *zcol_begin, int64_t *zcol_end,
+                  mr3_stats *stats);
 
 /* fp32 I/O, fp64 internal (the "single/double" solver of L1291-L1304); same contract. */
 int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, const float *e,
                  float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
-                 int64_t ldz, mr3_stats *stats);
+                 int64_t ldz, int64_t zcap, int64_t *zcol_begin, int64_t *zcol_end,
+                 mr3_stats *stats);
 
 /*
  * End-to-end forms with HOST buffers (same contract as mr3_dstemr_dd /
@@ -146,10 +188,12 @@ int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, 
  */
 int mr3_dstemr_dd_host(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d,
                        const double *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
-                       double *w, double *Z, int64_t ldz, mr3_stats *stats);
+                       double *w, double *Z, int64_t ldz, int64_t zcap, int64_t *zcol_begin,
+                       int64_t *zcol_end, mr3_stats *stats);
 int mr3_sstemr_d_host(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d,
                       const float *e, float vl, float vu, int64_t il, int64_t iu, int64_t *m,
-                      float *w, float *Z, int64_t ldz, mr3_stats *stats);
+                      float *w, float *Z, int64_t ldz, int64_t zcap, int64_t *zcol_begin,
+                      int64_t *zcol_end, mr3_stats *stats);
 
 /*
  * Two-phase form for an index-set partition over `world` ranks (one GPU each).

@@ -11,7 +11,9 @@ Public API (names follow the C-ABI):
     mr3_sstemr_d(d, e, ...)                                            fp32 I/O, fp64 internal
     dstemr(...) / sstemr(...)            aliases of the two above
     solve_host(d_np, e_np, ...)          end to end through the host-buffer C-ABI entry points
-    solve_distributed(d, e, group=...)   index-set partition over ranks (mr3_plan/mr3_execute)
+    solve_distributed(d, e, group=...)   index-set partition over ranks: one library call per
+                                         rank, all-gathers inside it (in-library NCCL
+                                         communicator, or an exchange callback over gloo)
     fp64_peak()                          K7 same-run FP64 peak + dd-step latency
     set_param(name, value, mode)         GAPTOL, XI, KRS, MAX_RQI, MAX_DEPTH, SEED, ELG_MAX, RTOL, GROUPS
 """
@@ -33,7 +35,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
           "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10, "GRID": 11, "CTA": 12, "XPTS": 13, "YCERT": 14, "NEWTON": 15, "TWISTW": 16,
           "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20, "RQI_FB": 21}
-ERRORS = {1: "NONFINITE", 2: "CUDA", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
+ERRORS = {1: "NONFINITE", 2: "CUDA", 3: "NCCL", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 
 class MR3Error(RuntimeError):
@@ -76,6 +78,9 @@ class Stats(ctypes.Structure):
 
 _lib = None
 _lock = threading.Lock()
+# int (*)(void *user, void *buf, size_t bytes_per_rank, int rank, int world, void *stream)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_int, ctypes.c_int, ctypes.c_void_p)
 
 
 def lib():
@@ -88,16 +93,21 @@ def lib():
             L = ctypes.CDLL(LIB_PATH)
             i64, i32, dbl, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
             pi64 = ctypes.POINTER(ctypes.c_int64)
-            L.mr3_create.argtypes = [ctypes.POINTER(vp), i32, vp]
+            L.mr3_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
+            L.mr3_set_exchange.argtypes = [vp, EXCHANGE_FN, vp]
+            L.mr3_nccl_unique_id.argtypes = [vp]
+            L.mr3_nccl_comm_init.argtypes = [ctypes.POINTER(vp), vp, i32, i32, i32]
+            L.mr3_nccl_comm_destroy.argtypes = [vp]
             L.mr3_destroy.argtypes = [vp]
             L.mr3_set_param.argtypes = [vp, i32, i32, dbl]
             L.mr3_get_param.argtypes = [vp, i32, i32]
             L.mr3_get_param.restype = dbl
             L.mr3_dstemr_dd.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp, dbl, dbl,
-                                        i64, i64, pi64, vp, vp, i64, ctypes.POINTER(Stats)]
+                                        i64, i64, pi64, vp, vp, i64, i64, pi64, pi64,
+                                        ctypes.POINTER(Stats)]
             L.mr3_sstemr_d.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp,
                                        ctypes.c_float, ctypes.c_float, i64, i64, pi64, vp, vp,
-                                       i64, ctypes.POINTER(Stats)]
+                                       i64, i64, pi64, pi64, ctypes.POINTER(Stats)]
             L.mr3_dstemr_dd_host.argtypes = L.mr3_dstemr_dd.argtypes
             L.mr3_sstemr_d_host.argtypes = L.mr3_sstemr_d.argtypes
             L.mr3_plan.argtypes = [vp, i32, ctypes.c_char, i64, vp, vp, dbl, dbl, i64, i64, i32,
@@ -139,7 +149,7 @@ def _ctx(device=None, stream=None):
     c = _ctx_cache.get(key)
     if c is None:
         h = ctypes.c_void_p()
-        rc = lib().mr3_create(ctypes.byref(h), dev, ctypes.c_void_p(sh))
+        rc = lib().mr3_create(ctypes.byref(h), dev, ctypes.c_void_p(sh), None, 0, 1)
         if rc:
             raise MR3Error(rc, "mr3_create")
         c = h
@@ -211,12 +221,15 @@ def _solve(mode, d, e, jobz, range_, il, iu, vl, vu, w=None, Z=None):
     else:
         Zs = Z
     m = ctypes.c_int64(0)
+    zb, ze = ctypes.c_int64(0), ctypes.c_int64(0)
     st = Stats()
     fn = lib().mr3_dstemr_dd if mode == 0 else lib().mr3_sstemr_d
+    zcap = Zs.shape[0] if Zs is not None else 0
     rc = fn(c, jobz.encode(), range_.encode(), n, ctypes.c_void_p(d.data_ptr()),
             ctypes.c_void_p(e.data_ptr() if n > 1 else d.data_ptr()), vl, vu, il, iu,
             ctypes.byref(m), ctypes.c_void_p(w.data_ptr()),
-            ctypes.c_void_p(Zs.data_ptr() if Zs is not None else 0), max(n, 1), ctypes.byref(st))
+            ctypes.c_void_p(Zs.data_ptr() if Zs is not None else 0), max(n, 1), zcap,
+            ctypes.byref(zb), ctypes.byref(ze), ctypes.byref(st))
     _err(c, rc, "mr3_dstemr_dd" if mode == 0 else "mr3_sstemr_d")
     mm = m.value
     Zout = Zs[:mm].T if (jobz == "V" and Zs is not None) else None
@@ -262,13 +275,15 @@ def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, w=None, Z=
         Z = torch.empty((max(mcap, 1), max(n, 1)), dtype=dt)
     c = _ctx()
     m = ctypes.c_int64(0)
+    zb, ze = ctypes.c_int64(0), ctypes.c_int64(0)
     st = Stats()
     fn = lib().mr3_dstemr_dd_host if mode == 0 else lib().mr3_sstemr_d_host
+    zcap = Z.shape[0] if (jobz == "V" and Z is not None) else 0
     rc = fn(c, jobz.encode(), range.encode(), n, ctypes.c_void_p(hd.data_ptr()),
             ctypes.c_void_p(he.data_ptr() if n > 1 else hd.data_ptr()), vl, vu, il, iu,
             ctypes.byref(m), ctypes.c_void_p(w.data_ptr()),
             ctypes.c_void_p(Z.data_ptr() if (jobz == "V" and Z is not None) else 0), max(n, 1),
-            ctypes.byref(st))
+            zcap, ctypes.byref(zb), ctypes.byref(ze), ctypes.byref(st))
     _err(c, rc, "mr3_dstemr_dd_host" if mode == 0 else "mr3_sstemr_d_host")
     mm = m.value
     return w[:mm], (Z[:mm].T if jobz == "V" else None), st.asdict()

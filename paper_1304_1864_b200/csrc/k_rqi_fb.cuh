@@ -37,12 +37,18 @@ struct FBX {  // end state of one half of a twisted factorization (exchanged thr
     int negc, E;
 };
 
+// dynamic shared memory: 4 staged tiles (rows + PP rows; after a pass they hold the exchanged
+// end states, at the end the epilogue's column table), the two z tiles of a storing pass and
+// the per-column store data.  33 KB in dd: 6 CTAs (768 threads) per SM, one wave for
+// 50 000 eigenpairs on 148 SMs.
 template <class R, class OutT>
 constexpr size_t fb_smem_bytes() {
     return 4 * (size_t)(Stage<R>::TILE + PP_TILE) * sizeof(double) +
            2 * 16 * (size_t)(FB_NP + 1) * sizeof(OutT) + 2 * FB_NP * sizeof(int64_t) +
-           2 * FB_NP * sizeof(FBX<R>) + 4 * sizeof(int);
+           4 * sizeof(int);
 }
+static_assert(2 * FB_NP * sizeof(FBX<dd>) <= 4 * (Stage<dd>::TILE + PP_TILE) * sizeof(double),
+              "the exchange area aliases the staging tiles");
 
 template <class R, class OutT>
 __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
@@ -53,8 +59,8 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
     OutT(*ztB)[FB_NP + 1] = ztF + 16;
     int2 *s_rb = reinterpret_cast<int2 *>(ztB + 16);          // per column: F rows < x, B rows > y
     OutT **s_zp = reinterpret_cast<OutT **>(s_rb + FB_NP);    // per column: base pointer
-    FBX<R> *xch = reinterpret_cast<FBX<R> *>(s_zp + FB_NP);   // [2][FB_NP]
-    int *s_lim = reinterpret_cast<int *>(xch + 2 * FB_NP);    // rmin, rmax
+    FBX<R> *xch = reinterpret_cast<FBX<R> *>(sstage);         // [2][FB_NP], between passes
+    int *s_lim = reinterpret_cast<int *>(s_zp + FB_NP);       // rmin, rmax
 
     const int tid = threadIdx.x;
     const int role = tid / FB_NP;  // 0: F (top-down), 1: B (bottom-up); warp-uniform

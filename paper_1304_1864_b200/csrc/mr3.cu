@@ -6,6 +6,8 @@
 // then the cluster members are refined (K2) and classified (K3) in the child
 // coordinates.  The host only sizes launches (a few counters per level).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is loaded lazily (nccl_api below)
 
 #include <algorithm>
 #include <cmath>
@@ -89,7 +91,72 @@ struct mr3_ctx_s {
     int debug = 0;
     double root_widen = 0.0;  // relative guard widening per row of a root node (R8d), 0 = certified
     mr3_stats stats;
+    // ranks of the one-call solvers (mr3_create): communicator or exchange callback
+    void *nccl_comm = nullptr;
+    int crank = 0, cworld = 1;
+    mr3_allgather_fn xfn = nullptr;
+    void *xuser = nullptr;
+    std::vector<int64_t> colb;  // column partition of the last execute (world + 1 entries)
 };
+
+// ------------------------------------------------------------------ NCCL (lazy)
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi g_nccl;
+// the process's libnccl.so.2 if one is loaded already (e.g. PyTorch's), else the system one
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    g_nccl.GetUniqueId = (decltype(&ncclGetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(&ncclCommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.CommDestroy = (decltype(&ncclCommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.AllGather = (decltype(&ncclAllGather))dlsym(h, "ncclAllGather");
+    g_nccl.GetErrorString = (decltype(&ncclGetErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy &&
+                g_nccl.AllGather && g_nccl.GetErrorString;
+    return g_nccl.ok;
+}
+}  // namespace
+
+// in-place all-gather of world slices of `bytes` bytes (this rank's slice valid on entry)
+static int exchange_allgather(mr3_ctx ctx, void *buf, size_t bytes) {
+    if (ctx->cworld <= 1 || bytes == 0) return 0;
+    if (ctx->xfn) {
+        const int r = ctx->xfn(ctx->xuser, buf, bytes, ctx->crank, ctx->cworld, (void *)ctx->stream);
+        if (r != 0) {
+            ctx->err = "exchange callback returned " + std::to_string(r);
+            return MR3_ERR_NCCL;
+        }
+        return 0;
+    }
+    if (!ctx->nccl_comm) {
+        ctx->err = "world > 1 without an NCCL communicator or an exchange callback";
+        return MR3_ERR_NCCL;
+    }
+    if (!nccl_load()) {
+        ctx->err = "libnccl.so.2 not found";
+        return MR3_ERR_NCCL;
+    }
+    char *b = (char *)buf;
+    const ncclResult_t r = g_nccl.AllGather(b + (size_t)ctx->crank * bytes, b, bytes, ncclUint8,
+                                            (ncclComm_t)ctx->nccl_comm, ctx->stream);
+    if (r != ncclSuccess) {
+        ctx->err = std::string("ncclAllGather: ") + g_nccl.GetErrorString(r);
+        return MR3_ERR_NCCL;
+    }
+    return 0;
+}
 
 // ------------------------------------------------------------------ helpers
 #include <chrono>
@@ -927,6 +994,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         mr3_partition_columns((int64_t)segs.size(), sb.data(), cost.data(), ctx->world, cb.data());
         c0 = cb[ctx->rank];
         c1 = cb[ctx->rank + 1];
+        ctx->colb = cb;
         // keep this rank's singletons and clusters
         std::vector<int32_t> ns, nb, ne, nm;
         for (auto &sg : segs) {
@@ -952,9 +1020,25 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         }
         CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#12");
     }
+    if (ctx->world <= 1) ctx->colb = {0, m};
     *zcol_begin = c0;
     *zcol_end = c1;
-    if (jobz == 'V' && zcap < c1 - c0) return MR3_ERR_ZCAP;
+    bool zfail = jobz == 'V' && zcap < c1 - c0;
+    if (ctx->cworld > 1 && ctx->world > 1) {
+        // one-call multi-rank solve: the ranks agree on MR3_ERR_ZCAP before any of them starts
+        // the RQI phase (a rank that returned alone would leave the others waiting in the
+        // eigenvalue all-gather)
+        int32_t *zf = (int32_t *)getbuf(ctx, "zcap_flags", (size_t)ctx->cworld * 4, &rc);
+        if (rc) return rc;
+        std::vector<int32_t> hf(ctx->cworld, 0);
+        hf[ctx->crank] = zfail ? 1 : 0;
+        CK(cudaMemcpyAsync(zf + ctx->crank, &hf[ctx->crank], 4, cudaMemcpyHostToDevice, s));
+        if ((rc = exchange_allgather(ctx, zf, 4))) return rc;
+        CK(cudaMemcpyAsync(hf.data(), zf, (size_t)ctx->cworld * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int r = 0; r < ctx->cworld; r++) zfail = zfail || hf[r] != 0;
+    }
+    if (zfail) return MR3_ERR_ZCAP;
     if (jobz == 'V' && ctx->split && c1 > c0) {
         CK(cudaMemset2DAsync(Z, ldz * sizeof(OutT), 0, ctx->n * sizeof(OutT), c1 - c0, s));
     }
@@ -1054,6 +1138,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         const bool split_all = P[MR3_SPLIT] >= 2 && ncount <= ctx->nsm * 16;
         bool rqi_split_all = false;  // (set for the k_rqi launch, read by launch_chunks)
         const RqiResume<R> *rqi_resume_in = nullptr;  // (k_rqi continuing after k_rqi_fb)
+        const char *rqi_tname = "k_rqi";
         int rqi_iter0 = 0;
         auto make_tasks = [&](const int32_t *lst, int *nt, int per, int count) -> int {
             k_rqi_tasks<<<1, 1024, 0, s>>>(lst, count, W.it.node, dseg, dtasks, dnt, per);
@@ -1125,7 +1210,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                     A.dbg_iters = (int32_t *)getbuf(ctx, "dbg_iters", (size_t)cnt * 4, &rc3);
                     A.dbg_trace = (double *)getbuf(ctx, "dbg_trace", (size_t)cnt * 64, &rc3);
                 }
-                KTime *t = kt_begin(ctx, locate ? "k_rqi_locate" : "k_rqi");
+                KTime *t = kt_begin(ctx, locate ? "k_rqi_locate" : rqi_tname);
                 if (locate)
                     k_rqi_locate<R><<<nb, rtpb, 0, s>>>(A);
                 else
@@ -1256,6 +1341,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             if (!attr_fb) {
                 cudaFuncSetAttribute(k_rqi_fb<R, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
+                cudaFuncSetAttribute(k_rqi_fb<R, OutT>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
                 attr_fb = true;
             }
             KTime *t = kt_begin(ctx, "k_rqi");
@@ -1277,7 +1365,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         if ((rc2 = make_tasks(llist, &ntasks, rtpb, hl))) return rc2;
         rqi_resume_in = resume;
         rqi_iter0 = std::min(2, (int)P[MR3_MAX_RQI]);
+        rqi_tname = "k_rqi_tail";
         rc2 = launch_chunks(false, llist, ntasks);
+        rqi_tname = "k_rqi";
         rqi_resume_in = nullptr;
         rqi_iter0 = 0;
         return rc2;
@@ -1526,7 +1616,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     for (auto &p : ctx->ktimes) {
         const std::string &nm = p.first;
         int slot = nm == "k_root" ? 0 : nm == "k_bisect" ? 1 : nm == "k_classify" ? 2
-                                     : nm == "k_child"  ? 3 : nm == "k_rqi" ? 4 : 6;
+                                     : nm == "k_child"  ? 3 : (nm == "k_rqi" || nm == "k_rqi_tail") ? 4 : 6;
         ctx->stats.t_ms[slot] += p.second.first;
         ctx->stats.t_ms[5] += p.second.first;
     }
@@ -1539,10 +1629,15 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
 
 extern "C" {
 
-int mr3_create(mr3_ctx *out, int device, void *cuda_stream) {
+int mr3_create(mr3_ctx *out, int device, void *cuda_stream, void *nccl_comm, int rank,
+               int world) {
     if (!out) return -1;
+    if (world < 1 || rank < 0 || rank >= world) return -5;
     mr3_ctx ctx = new mr3_ctx_s();
     ctx->device = device;
+    ctx->nccl_comm = nccl_comm;
+    ctx->crank = rank;
+    ctx->cworld = world;
     for (int m = 0; m < 2; m++)
         for (int i = 0; i < MR3_NPARAM; i++) ctx->cfg[m].v[i] = kDefaults[m][i];
     if (cudaSetDevice(device) != cudaSuccess) {
@@ -1627,9 +1722,11 @@ int mr3_execute(mr3_ctx ctx, char jobz, void *w, void *Z, int64_t ldz, int64_t z
                                        zcol_end, stats);
 }
 
+// the one-call solve: plan, all-gather of the bracket records, execute, all-gather of w
 static int solve_common(mr3_ctx ctx, int mode, char jobz, char range, int64_t n, const void *d,
                         const void *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
-                        void *w, void *Z, int64_t ldz, mr3_stats *stats) {
+                        void *w, void *Z, int64_t ldz, int64_t zcap, int64_t *zcol_begin,
+                        int64_t *zcol_end, mr3_stats *stats) {
     if (!ctx) return -1;
     if (jobz != 'V' && jobz != 'N') return -2;
     if (range != 'A' && range != 'I' && range != 'V') return -3;
@@ -1637,35 +1734,105 @@ static int solve_common(mr3_ctx ctx, int mode, char jobz, char range, int64_t n,
     if (!m) return -11;
     if (n > 0 && !w) return -12;
     if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -14;
+    if (!zcol_begin || !zcol_end) return -16;
+    *zcol_begin = 0;
+    *zcol_end = 0;
     double *brk = nullptr;
     int64_t cap = 0, cntm = 0;
-    int rc = mr3_plan(ctx, mode, range, n, d, e, vl, vu, il, iu, 0, 1, m, &brk, &cap, &cntm);
+    int rc = mr3_plan(ctx, mode, range, n, d, e, vl, vu, il, iu, ctx->crank, ctx->cworld, m, &brk,
+                      &cap, &cntm);
     if (rc) {
         if (stats) *stats = ctx->stats;
         return rc;
     }
-    int64_t zb = 0, ze = 0;
-    rc = mr3_execute(ctx, jobz, w, Z, ldz, n, &zb, &ze, stats);
+    if (ctx->cworld > 1 && brk != nullptr) {
+        rc = exchange_allgather(ctx, brk, (size_t)cap * MR3_BRK_REC * sizeof(double));
+        if (rc) return rc;
+    }
+    rc = mr3_execute(ctx, jobz, w, Z, ldz, zcap, zcol_begin, zcol_end, stats);
     *m = ctx->m < 0 ? 0 : ctx->m;
-    return rc;
+    if (rc || ctx->cworld <= 1 || *m == 0) return rc;
+    // w: every rank holds its own columns' eigenvalues; padded all-gather of the slices
+    const std::vector<int64_t> cb = ctx->colb;
+    if ((int)cb.size() != ctx->cworld + 1) {
+        ctx->err = "column partition missing";
+        return MR3_ERR_STATE;
+    }
+    int64_t wcap = 1;
+    for (int r = 0; r < ctx->cworld; r++) wcap = std::max(wcap, cb[r + 1] - cb[r]);
+    const size_t es = mode ? 4 : 8;
+    char *wg = (char *)getbuf(ctx, "w_gather", (size_t)ctx->cworld * wcap * es, &rc);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    const int me = ctx->crank;
+    if (cb[me + 1] > cb[me])
+        CK(cudaMemcpyAsync(wg + (size_t)me * wcap * es, (char *)w + cb[me] * es,
+                           (size_t)(cb[me + 1] - cb[me]) * es, cudaMemcpyDeviceToDevice, s));
+    rc = exchange_allgather(ctx, wg, (size_t)wcap * es);
+    if (rc) return rc;
+    for (int r = 0; r < ctx->cworld; r++)
+        if (r != me && cb[r + 1] > cb[r])
+            CK(cudaMemcpyAsync((char *)w + cb[r] * es, wg + (size_t)r * wcap * es,
+                               (size_t)(cb[r + 1] - cb[r]) * es, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
 }
 
 int mr3_dstemr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d, const double *e,
                   double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
-                  int64_t ldz, mr3_stats *stats) {
-    return solve_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+                  int64_t ldz, int64_t zcap, int64_t *zcol_begin, int64_t *zcol_end,
+                  mr3_stats *stats) {
+    return solve_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, zcap,
+                        zcol_begin, zcol_end, stats);
 }
 
 int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, const float *e,
                  float vl, float vu, int64_t il, int64_t iu, int64_t *m, float *w, float *Z,
-                 int64_t ldz, mr3_stats *stats) {
-    return solve_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+                 int64_t ldz, int64_t zcap, int64_t *zcol_begin, int64_t *zcol_end,
+                 mr3_stats *stats) {
+    return solve_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, zcap,
+                        zcol_begin, zcol_end, stats);
+}
+
+int mr3_set_exchange(mr3_ctx ctx, mr3_allgather_fn fn, void *user) {
+    if (!ctx) return -1;
+    ctx->xfn = fn;
+    ctx->xuser = user;
+    return 0;
+}
+
+int mr3_nccl_unique_id(void *id128) {
+    if (!id128) return -1;
+    if (!nccl_load()) return MR3_ERR_NCCL;
+    ncclUniqueId id;
+    if (g_nccl.GetUniqueId(&id) != ncclSuccess) return MR3_ERR_NCCL;
+    memcpy(id128, &id, sizeof(id));
+    return 0;
+}
+
+int mr3_nccl_comm_init(void **comm, const void *id128, int rank, int world, int device) {
+    if (!comm || !id128) return -1;
+    if (world < 1 || rank < 0 || rank >= world) return -3;
+    if (!nccl_load()) return MR3_ERR_NCCL;
+    if (cudaSetDevice(device) != cudaSuccess) return MR3_ERR_CUDA;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    if (g_nccl.CommInitRank(&c, world, id, rank) != ncclSuccess) return MR3_ERR_NCCL;
+    *comm = (void *)c;
+    return 0;
+}
+
+int mr3_nccl_comm_destroy(void *comm) {
+    if (!comm) return 0;
+    if (!nccl_load()) return MR3_ERR_NCCL;
+    return g_nccl.CommDestroy((ncclComm_t)comm) == ncclSuccess ? 0 : MR3_ERR_NCCL;
 }
 
 static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64_t n,
                              const void *d, const void *e, double vl, double vu, int64_t il,
-                             int64_t iu, int64_t *m, void *w, void *Z, int64_t ldz,
-                             mr3_stats *stats) {
+                             int64_t iu, int64_t *m, void *w, void *Z, int64_t ldz, int64_t zcap,
+                             int64_t *zcol_begin, int64_t *zcol_end, mr3_stats *stats) {
     if (!ctx) return -1;
     if (jobz != 'V' && jobz != 'N') return -2;
     if (range != 'A' && range != 'I' && range != 'V') return -3;
@@ -1674,16 +1841,18 @@ static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64
     if (n > 0 && (!d || (n > 1 && !e))) return -5;
     if (n > 0 && !w) return -12;
     if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -14;
+    if (!zcol_begin || !zcol_end) return -16;
     *m = 0;
     if (n == 0) return solve_common(ctx, mode, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz,
-                                    stats);
+                                    zcap, zcol_begin, zcol_end, stats);
     const size_t es = mode ? 4 : 8;
     int rc = 0;
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    // columns the solve can produce: all for 'A' / 'V', iu - il + 1 for 'I'
+    // device columns: at most what the host Z holds (zcap) and what the solve can produce
     int64_t mcap = n;
     if (range == 'I') mcap = std::max<int64_t>(0, std::min<int64_t>(iu, n) - std::max<int64_t>(il, 1) + 1);
+    mcap = std::min(mcap, std::max<int64_t>(zcap, 0));
     char *dd_ = (char *)getbuf(ctx, "host_d", (size_t)n * es, &rc);
     char *de_ = (char *)getbuf(ctx, "host_e", (size_t)std::max<int64_t>(n - 1, 1) * es, &rc);
     char *dw = (char *)getbuf(ctx, "host_w", (size_t)n * es, &rc);
@@ -1692,13 +1861,14 @@ static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64
     if (rc) return rc;
     CK(cudaMemcpyAsync(dd_, d, (size_t)n * es, cudaMemcpyHostToDevice, s));
     if (n > 1) CK(cudaMemcpyAsync(de_, e, (size_t)(n - 1) * es, cudaMemcpyHostToDevice, s));
-    rc = solve_common(ctx, mode, jobz, range, n, dd_, de_, vl, vu, il, iu, m, dw, dZ, n, stats);
+    rc = solve_common(ctx, mode, jobz, range, n, dd_, de_, vl, vu, il, iu, m, dw, dZ, n, mcap,
+                      zcol_begin, zcol_end, stats);
     if (rc) return rc;
-    const int64_t mm = *m;
+    const int64_t mm = *m, nc = *zcol_end - *zcol_begin;
     if (mm > 0) {
         CK(cudaMemcpyAsync(w, dw, (size_t)mm * es, cudaMemcpyDeviceToHost, s));
-        if (jobz == 'V')
-            CK(cudaMemcpy2DAsync(Z, (size_t)ldz * es, dZ, (size_t)n * es, (size_t)n * es, (size_t)mm,
+        if (jobz == 'V' && nc > 0)
+            CK(cudaMemcpy2DAsync(Z, (size_t)ldz * es, dZ, (size_t)n * es, (size_t)n * es, (size_t)nc,
                                  cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#17");
@@ -1707,14 +1877,18 @@ static int solve_host_common(mr3_ctx ctx, int mode, char jobz, char range, int64
 
 int mr3_dstemr_dd_host(mr3_ctx ctx, char jobz, char range, int64_t n, const double *d,
                        const double *e, double vl, double vu, int64_t il, int64_t iu, int64_t *m,
-                       double *w, double *Z, int64_t ldz, mr3_stats *stats) {
-    return solve_host_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+                       double *w, double *Z, int64_t ldz, int64_t zcap, int64_t *zcol_begin,
+                       int64_t *zcol_end, mr3_stats *stats) {
+    return solve_host_common(ctx, 0, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, zcap,
+                             zcol_begin, zcol_end, stats);
 }
 
 int mr3_sstemr_d_host(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d,
                       const float *e, float vl, float vu, int64_t il, int64_t iu, int64_t *m,
-                      float *w, float *Z, int64_t ldz, mr3_stats *stats) {
-    return solve_host_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, stats);
+                      float *w, float *Z, int64_t ldz, int64_t zcap, int64_t *zcol_begin,
+                      int64_t *zcol_end, mr3_stats *stats) {
+    return solve_host_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, zcap,
+                             zcol_begin, zcol_end, stats);
 }
 
 int mr3_partition_columns(int64_t nseg, const int64_t *seg_begin, const double *cost, int world,
@@ -1806,6 +1980,8 @@ const char *mr3_strerror(int code) {
             return "NaN or Inf in d or e";
         case MR3_ERR_CUDA:
             return "CUDA error";
+        case MR3_ERR_NCCL:
+            return "collective (NCCL / exchange) error";
         case MR3_ERR_NOMEM:
             return "device allocation failed";
         case MR3_ERR_NOCONV:

@@ -165,22 +165,23 @@ def test_deterministic_repeat():
     np.testing.assert_array_equal(Z1, Z2)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_two_phase_world_emulation_bitwise(world):
-    """Ranks of the plan/execute form emulated one after another on one GPU: the
-    union of their columns equals the world=1 solve bit for bit (S:343)."""
+def _emulate_world(p, world, params=None):
+    """Ranks of the plan/execute form emulated one after another on one GPU (each with its
+    own context and stream); returns the world-1 solution and the union of the ranks'
+    columns, both on the device."""
     import ctypes
-    p = synth.glued_wilkinson(8, 21)
     d = torch.from_numpy(p.d).cuda()
     e = torch.from_numpy(p.e).cuda()
     w1, Z1, _ = mr3.mr3_dstemr_dd(d, e)
-    w1, Z1 = w1.cpu().numpy(), Z1.cpu().numpy()
     L = mr3.lib()
     ctxs, bufs, caps = [], [], []
     streams = [torch.cuda.Stream() for _ in range(world)]
     for r in range(world):
         h = ctypes.c_void_p()
-        assert L.mr3_create(ctypes.byref(h), 0, ctypes.c_void_p(streams[r].cuda_stream)) == 0
+        assert L.mr3_create(ctypes.byref(h), 0, ctypes.c_void_p(streams[r].cuda_stream), None, 0,
+                            1) == 0
+        for k, v in (params or {}).items():
+            L.mr3_set_param(h, 0, mr3.PARAMS[k], float(v))
         ctxs.append(h)
         m = ctypes.c_int64()
         brk = ctypes.c_void_p()
@@ -198,25 +199,57 @@ def test_two_phase_world_emulation_bitwise(world):
     for r in range(world):
         bufs[r][:world * rec].copy_(full)
     torch.cuda.synchronize()
-    wall = np.zeros(p.n)
-    Zall = np.zeros((p.n, p.n))
+    wall = torch.zeros(p.n, dtype=torch.float64, device="cuda")
+    Zall = torch.zeros((p.n, p.n), dtype=torch.float64, device="cuda")
+    ranges = []
     for r in range(world):
         w = torch.zeros(p.n, dtype=torch.float64, device="cuda")
-        Zs = torch.zeros((p.n, p.n), dtype=torch.float64, device="cuda")
         zb, ze = ctypes.c_int64(), ctypes.c_int64()
         st = mr3.Stats()
-        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
-                           ctypes.c_void_p(Zs.data_ptr()), p.n, p.n, ctypes.byref(zb),
-                           ctypes.byref(ze), ctypes.byref(st))
-        assert rc == 0
+        # size Z from MR3_ERR_ZCAP (the partition is known after classification)
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()), None, p.n, 0,
+                           ctypes.byref(zb), ctypes.byref(ze), ctypes.byref(st))
+        if rc == 6:
+            Zs = torch.zeros((ze.value - zb.value, p.n), dtype=torch.float64, device="cuda")
+            rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
+                               ctypes.c_void_p(Zs.data_ptr()), p.n, Zs.shape[0], ctypes.byref(zb),
+                               ctypes.byref(ze), ctypes.byref(st))
+        assert rc == 0, rc
         torch.cuda.synchronize()
         a, b = zb.value, ze.value
-        wall[a:b] = w.cpu().numpy()[a:b]
-        Zall[:, a:b] = Zs[:b - a].T.cpu().numpy()
+        ranges.append((a, b))
+        wall[a:b] = w[a:b]
+        if b > a:
+            Zall[:, a:b] = Zs[:b - a].T
     for h in ctxs:
         L.mr3_destroy(h)
-    np.testing.assert_array_equal(wall, w1)
-    np.testing.assert_array_equal(Zall, Z1)
+    assert ranges[0][0] == 0 and ranges[-1][1] == p.n
+    assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+    return w1, Z1, wall, Zall, ranges
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_two_phase_world_emulation_bitwise(world):
+    """Ranks of the plan/execute form emulated one after another on one GPU: the
+    union of their columns equals the world=1 solve bit for bit (S:343)."""
+    w1, Z1, wall, Zall, _ = _emulate_world(synth.glued_wilkinson(8, 21), world)
+    assert torch.equal(wall, w1) and torch.equal(Zall, Z1)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("make", [lambda: synth.legendre(20000), lambda: synth.glued_wilkinson(1000, 21)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_world_emulation_bitwise_large(make, world):
+    """The same at sizes where the default large-n path runs across ranks: the shared grid
+    (>= 512 items), the Newton/Laguerre binary_x phase (one lane per eigenvalue above ~19k
+    items) and its fixed-lane multisection tail, the refinement, k_rqi_fb and the k_rqi
+    hand-off; and (glued Wilkinson) clusters that must stay whole on one rank."""
+    p = make()
+    w1, Z1, wall, Zall, ranges = _emulate_world(p, world)
+    assert torch.equal(wall, w1)
+    assert torch.equal(Zall, Z1)
+    del Z1, Zall
+    torch.cuda.empty_cache()
 
 
 def test_fp64_peak_microbenchmark():
