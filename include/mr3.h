@@ -106,7 +106,9 @@ enum mr3_param {
     MR3_DEBUG = 20,    /* diagnostics to stderr: bit 1 dumps/histograms, 2 host sync points,
                           4 device timeline, 8 check every launch; 0 */
     MR3_RQI_FB = 21,   /* 1: RQI iterations 1-2 with the two halves of every factorization in
-                          two threads (k_rqi_fb), later iterations in k_rqi; 0: all in k_rqi; 1 */
+                          two threads (k_rqi_fb), later iterations in k_rqi; 2: the same with the
+                          row update in two-dot-product form (shorter dependent chain);
+                          0: all in k_rqi; 1 */
     MR3_NPARAM = 22
 };
 

@@ -50,7 +50,13 @@ constexpr size_t fb_smem_bytes() {
 static_assert(2 * FB_NP * sizeof(FBX<dd>) <= 4 * (Stage<dd>::TILE + PP_TILE) * sizeof(double),
               "the exchange area aliases the staging tiles");
 
-template <class R, class OutT>
+// DOT2: the row update in "two dot products" form -- p' = (lld - lam) p - (lam d) q and
+// q' = d q + p (F; B likewise with d and lld exchanged) -- both from the state (p, q), so
+// the dependent chain per row is one pair dot product instead of two pair FMAs in sequence;
+// lld - lam and lam d are off the chain.  The same recurrence in exact arithmetic; every step
+// is exact for data and shift perturbed by O(eps_y) relative (reading R8b).  ~40% more FP64
+// instructions per row, about half the dependent latency.
+template <class R, class OutT, bool DOT2>
 __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
     extern __shared__ __align__(16) double fb_dyn[];
     double *sstage = fb_dyn;
@@ -172,7 +178,8 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             const double lpx = hi(rw.ld) * hi(qx) * rcp(hi(D));  // l+ = ld / d+
             const double l2 = lpx * lpx;
             const double N2 = clampbig(fma(l2, nrm, l2));
-            const R p2 = fma_dd(mlam, D, mul(rw.lld, px));
+            const R p2 = DOT2 ? dot2_dd(add(rw.lld, mlam), px, mul(mlam, rw.d), qx)
+                              : fma_dd(mlam, D, mul(rw.lld, px));
             if (!GUARD || (int)kk < (int)r) {
                 if (wz) {
                     double pm, ipm;
@@ -196,7 +203,8 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             const double ux = hi(rw.l) * hi(rw.d) * hi(qx) * rcp(hi(E));  // u- = l d / D-
             const double u2 = ux * ux;
             const double N2 = clampbig(fma(u2, nrm, u2));
-            const R P2 = fma_dd(mlam, E, mul(rw.d, px));
+            const R P2 = DOT2 ? dot2_dd(add(rw.d, mlam), px, mul(mlam, rw.lld), qx)
+                              : fma_dd(mlam, E, mul(rw.d, px));
             if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
                 if (wz) {
                     double pm, ipm;

@@ -1339,15 +1339,18 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             constexpr size_t smem = fb_smem_bytes<R, OutT>();
             static bool attr_fb = false;  // per instantiation, once per process
             if (!attr_fb) {
-                cudaFuncSetAttribute(k_rqi_fb<R, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                cudaFuncSetAttribute(k_rqi_fb<R, OutT>,
-                                     cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     (int)cudaSharedmemCarveoutMaxShared);
+                for (auto fk : {k_rqi_fb<R, OutT, false>, k_rqi_fb<R, OutT, true>}) {
+                    cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    cudaFuncSetAttribute(fk, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared);
+                }
                 attr_fb = true;
             }
             KTime *t = kt_begin(ctx, "k_rqi");
-            k_rqi_fb<R, OutT><<<ntasks, FB_TPB, smem, s>>>(A);
+            if (P[MR3_RQI_FB] >= 2)
+                k_rqi_fb<R, OutT, true><<<ntasks, FB_TPB, smem, s>>>(A);
+            else
+                k_rqi_fb<R, OutT, false><<<ntasks, FB_TPB, smem, s>>>(A);
             kt_end(ctx, t);
             CKL("k_rqi_fb");
         }

@@ -295,9 +295,12 @@ def test_config3_full_size():
     jh, jl, _, _ = oracle.jacobi(db, eb)
     ref = np.sort(np.repeat(jh + jl, 200))
     assert np.max(np.abs(w - ref)) <= 2.0 ** -26 * 1.0001
-    idx = np.array([1, 2, 200, 201, 2100, 2101, 4000, 4199, 4200])
-    lh, ll = oracle.eigvals(p.d, p.e, idx)
-    assert np.max(np.abs(w[idx - 1] - lh)) <= 4e-16 * oracle.norm1(p.d, p.e)
+    # every pair against the oracle: eigenvalues, R1 floor, per-column angles of the
+    # isolated eigenvectors and subspace angles of the degenerate / glue-split groups
+    # (Gap-theorem and Davis-Kahan bounds)
+    res = check_solution(p, w, Z, np.arange(1, p.n + 1), full_orth=False, verbose=True)
+    assert res["n_groups"] >= 1
+    assert_parity(res)
 
 
 @pytest.mark.slow
@@ -307,7 +310,12 @@ def test_config4_full_size():
     assert w.shape == (2000,)
     o, dd = exact_orthogonality(torch.from_numpy(Z).cuda())
     assert o <= 5e-6 and dd <= 5e-6
-    idx = _sample_indices(p.n, 2000, k=16)
+    # every column: R1 (Eq. (1.1)) and R2 in binary128
+    r1, r2, _ = oracle.residuals(p.d.astype(np.float64), p.e.astype(np.float64),
+                                 w.astype(np.float64), Z.astype(np.float64))
+    print("config 4: R1 max %.3g R2 max %.3g" % (r1.max(), r2.max()))
+    assert r1.max() <= 5e-7
+    idx = _sample_indices(p.n, 2000, k=64)
     res = check_solution(p, w[idx - 1], Z[:, idx - 1], idx, io="f32", full_orth=False,
                          verbose=True)
     assert_parity(res, io="f32")
@@ -324,10 +332,22 @@ def test_config5_full_size_sampled():
     assert st["d_max"] == 0 and st["largest_cluster"] == 1  # rho = 1/n (Table 2)
     wc = w.cpu().numpy()
     assert np.all(np.diff(wc) > 0)
-    idx = _sample_indices(p.n, p.n, k=12)
+    # 512 indices against the oracle: 64 from each dense end of the spectrum (the
+    # Gauss-Legendre nodes cluster at +-1) and 384 spread over the interior
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([np.arange(1, 65), np.arange(p.n - 63, p.n + 1),
+                                    rng.choice(np.arange(65, p.n - 63), 384, replace=False)]))
+    assert idx.size == 512
     Zs = Z[:, torch.from_numpy(idx - 1).cuda()]
     res = check_solution(p, wc[idx - 1], Zs.cpu().numpy(), idx, full_orth=True, verbose=True)
     assert_parity(res)
+    # R2 of every column (binary128 residuals, chunked through host memory)
+    r2max, r1max = 0.0, 0.0
+    for c0 in range(0, p.n, 2500):
+        r1, r2, _ = oracle.residuals(p.d, p.e, wc[c0:c0 + 2500], Z[:, c0:c0 + 2500].cpu().numpy())
+        r2max, r1max = max(r2max, float(r2.max())), max(r1max, float(r1.max()))
+    print("config 5: all columns R2 max %.3g R1 max %.3g" % (r2max, r1max))
+    assert r2max <= 1e-15
     # orthogonality of the sample against every column, exactly (c7)
     omax = 0.0
     for c0 in range(0, p.n, 5000):

@@ -266,3 +266,58 @@ def test_sin_angle_verifier():
     assert abs(s2[0] - np.sin(th)) < 1e-24
     sub = oracle.subspace_sin(zhat, zo, np.zeros_like(zo))
     assert abs(sub - np.sin(th)) < 1e-20
+
+
+def test_norm1_and_gershgorin_rows_differ():
+    """||T||_1 (Eq. (1.1)) and the Gershgorin bounds on matrices whose row sums
+    differ, with the maximum in the first, a middle and the last row: against the dense
+    matrix summed in mpmath (a plain definition, no tridiagonal shortcut)."""
+    cases = [(np.array([9.0, 1.0, -2.0, 0.5]), np.array([-3.0, 0.25, 1.0])),      # first row
+             (np.array([0.5, -1.0, 7.0, 0.25, 1.0]), np.array([0.5, -2.0, 3.0, 0.125])),  # middle
+             (np.array([1.0, 2.0, -0.5, -6.0]), np.array([0.5, 0.75, -4.0]))]     # last row
+    rng = np.random.default_rng(3)
+    cases.append((rng.standard_normal(37) * np.exp2(rng.integers(-8, 9, 37)),
+                   rng.standard_normal(36) * np.exp2(rng.integers(-8, 9, 36))))
+    for d, e in cases:
+        n = d.size
+        T = [[mp.mpf(0)] * n for _ in range(n)]
+        for i in range(n):
+            T[i][i] = mp.mpf(float(d[i]))
+        for i in range(n - 1):
+            T[i][i + 1] = T[i + 1][i] = mp.mpf(float(e[i]))
+        cols = [mp.fsum(abs(T[i][j]) for i in range(n)) for j in range(n)]
+        assert abs(oracle.norm1(d, e) - float(max(cols))) <= 1e-30 * float(max(cols))
+        radii = [mp.fsum(abs(T[i][j]) for j in range(n) if j != i) for i in range(n)]
+        gl = min(T[i][i] - radii[i] for i in range(n))
+        gu = max(T[i][i] + radii[i] for i in range(n))
+        ogl, ogu = oracle.gershgorin(d, e)
+        assert abs(ogl - float(gl)) <= 1e-28 * float(max(cols))
+        assert abs(ogu - float(gu)) <= 1e-28 * float(max(cols))
+
+
+@pytest.mark.parametrize("g", [2, 3, 5])
+def test_subspace_sin_constructed_rotation(g):
+    """Group subspace angles (oracle_subspace_residual) for g >= 2: the
+    computed span Zhat is built with known principal angles theta_j to span(Z_G) and then
+    mixed by a g x g rotation, so no column of Zhat lines up with a column of Z_G.  The
+    largest principal angle's sine must come out as sin(max theta) and as the largest
+    singular value of (I - Z_G Z_G^T) Zhat from an mpmath SVD: an index slip or a transposed
+    operand in the g x g Gram matrix fails it."""
+    rng = np.random.default_rng(100 + g)
+    n = 40
+    Q, _ = np.linalg.qr(rng.standard_normal((n, 2 * g)))
+    U, V = Q[:, :g], Q[:, g:]                 # span(Z_G) and an orthogonal complement part
+    A, _ = np.linalg.qr(rng.standard_normal((g, g)))  # basis of span(Z_G) given to the oracle
+    B, _ = np.linalg.qr(rng.standard_normal((g, g)))  # rotation mixing the columns of Zhat
+    theta = np.array([10.0 ** (-3 - 2 * j) for j in range(g)])
+    rng.shuffle(theta)
+    Zo = U @ A
+    Zhat = (U * np.cos(theta) + V * np.sin(theta)) @ B
+    s = oracle.subspace_sin(Zhat, Zo, np.zeros_like(Zo))
+    assert abs(s - np.sin(theta.max())) <= 1e-14 * np.sin(theta.max()) + 1e-16
+    # mpmath: singular values of the projection residual
+    Zm = mp.matrix(Zhat.tolist())
+    Om = mp.matrix(Zo.tolist())
+    Pm = Zm - Om * (Om.T * Zm)
+    sv = mp.svd_r(Pm, compute_uv=False)
+    assert abs(s - float(max(sv))) <= 1e-14 * float(max(sv)) + 1e-18
