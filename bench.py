@@ -51,7 +51,25 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--other-configs", default="1,2,3,4",
+                    help="BASELINE configs also timed (with roofline and the full oracle run "
+                         "as CPU baseline), reported under 'other_configs'; '' = none")
+    ap.add_argument("--emulate-world", default="2,4,8",
+                    help="world sizes whose ranks (mr3_plan + mr3_execute) are emulated one "
+                         "after another on this GPU; per-rank device times under "
+                         "'emulated_world' (an emulation, not a multi-GPU measurement)")
+    ap.add_argument("--no-zstore", action="store_true")
     return ap.parse_args()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -127,13 +145,14 @@ class Clocks:
                 "power_w_max": float(max(s[3] for s in self.samples))}
 
 
-def cpu_baseline_run(p, n_idx, seed=0):
+def cpu_baseline_run(p, n_idx, seed=0, idx=None):
     """The oracle (binary128 bisection + inverse iteration) on a bounded sample of
-    eigenpairs of the same matrix, on all host cores."""
+    eigenpairs of the same matrix (or the given 1-based indices), on all host cores."""
     import oracle
     rng = np.random.default_rng(seed)
-    idx = np.unique(np.concatenate([[1, p.n], rng.choice(np.arange(2, p.n), n_idx - 2,
-                                                          replace=False)]))
+    if idx is None:
+        idx = np.unique(np.concatenate([[1, p.n], rng.choice(np.arange(2, p.n), n_idx - 2,
+                                                              replace=False)]))
     d, e = p.d.astype(np.float64), p.e.astype(np.float64)
     t0 = time.perf_counter()
     lh, ll = oracle.eigvals(d, e, idx)
@@ -163,11 +182,190 @@ def run_reference(args, p, rank, world):
             "scaling": "strong", "vs_baseline": None, "dtype": "binary128 (oracle)",
             "data": "synthetic", "config": {"workload": p.name, "n": p.n, "sample_per_step": per_step},
             "cpu_baseline": {"value": v, "unit": "eigenpairs/s", "cores": cores, "kind": "oracle",
+                             "cpu": cpu_model(),
                              "sample": f"{per_step} eigenpairs of the n={p.n} workload per step "
                                        "(bisection on T + inverse iteration, binary128)"},
             "e2e": {"value": v, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def make_roof(ktot, stats, steps, mode, traffic_tab, peak_ips):
+    """roofline(kname): algorithmic FP64 instructions per launch of kname (DESIGN.md section 5
+    counts x the units the solve processed) / its CUDA-event time per launch."""
+
+    def roof(kname):
+        ms, nl = ktot.get(kname, (0.0, 0))
+        if kname == "k_bisect":
+            rows = stats["bisect_rows"] if stats else 0.0
+            rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
+            rows_n = stats.get("newton_rows_x", 0.0) if stats else 0.0
+            inst = (rows * FP64_INST_PER_BISECT_ROW[mode] +
+                    (rows_x - rows_n) * FP64_INST_PER_BISECT_ROW["x"] +
+                    rows_n * FP64_INST_PER_BISECT_ROW["newton"])
+            per = {"binary_y_row": FP64_INST_PER_BISECT_ROW[mode],
+                   "binary_x_row": FP64_INST_PER_BISECT_ROW["x"],
+                   "binary_x_newton_row": FP64_INST_PER_BISECT_ROW["newton"]}
+            units = {"binary_y_rows": rows, "binary_x_rows": rows_x - rows_n,
+                     "binary_x_newton_rows": rows_n}
+        else:
+            rows = stats["rqi_rows"] if stats else 0.0
+            inst = rows * FP64_INST_PER_RQI_ROW[mode]
+            per = {"rqi_row": FP64_INST_PER_RQI_ROW[mode]}
+            units = {"rqi_rows": rows}
+        t_launch = ms / max(nl, 1) * 1e-3  # average launch duration
+        inst_launch = inst / max(nl / steps, 1)
+        ach = inst_launch / t_launch if t_launch else 0.0
+        return {"bound": "alu", "kernel": kname, "achieved": ach / 1e12,
+                "peak": DERIVED_FP64_PEAK / 1e12, "unit": "T FP64-inst/s",
+                "frac": ach / DERIVED_FP64_PEAK, "traffic": traffic_tab.get(kname),
+                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz (MEASURED_PEAKS.json "
+                               "has no FP64 entry); measured_peak_same_run = K7 DFMA microbenchmark",
+                "measured_peak_same_run": peak_ips / 1e12,
+                "frac_of_measured": ach / peak_ips if peak_ips else None,
+                "inst_per_unit": per, "units_per_step": units,
+                "launches_per_step": nl / steps, "ms_per_launch": t_launch * 1e3}
+    return roof
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), \
+            "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except Exception:
+        return 6546.2, "fallback: B200_PROFILING.md measured copy bandwidth"
+
+
+def timed_solves(mr3, fn, d, e, p, il, iu, steps, warmup, flush, stream):
+    """Device-timed solves of one config (inputs resident, L2 flushed between steps)."""
+    import torch
+    for _ in range(warmup):
+        out = fn(d, e, "V", p.range, il, iu)
+        del out
+    torch.cuda.synchronize()
+    times, ktot, launches, stats = [], {}, 0, None
+    for s in range(steps):
+        flush.fill_(s)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        w, Z, stats = fn(d, e, "V", p.range, il, iu)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+        for k, (ms, nl) in mr3.kernel_times().items():
+            t0, n0 = ktot.get(k, (0.0, 0))
+            ktot[k] = (t0 + ms, n0 + nl)
+        launches += mr3.launch_count()
+        del w, Z
+    return times, ktot, launches, stats
+
+
+def other_config_line(mr3, cfg, args, flush, stream, peak_ips, cpu):
+    """Timing, roofline and CPU baseline of another BASELINE config (a secondary line)."""
+    import torch
+    p = synth.config(cfg)
+    il, iu = p.index_range()
+    m_req = iu - il + 1
+    fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    steps = max(3, min(args.steps, 5))
+    times, ktot, launches, stats = timed_solves(mr3, fn, d, e, p, il, iu, steps, 2, flush, stream)
+    t = float(np.mean(times))
+    mode = "f64" if p.io == "f32" else "dd"
+    roof = make_roof(ktot, stats, steps, mode, {}, peak_ips)
+    cand = [k for k in ("k_bisect", "k_rqi") if k in ktot]
+    dom = max(cand, key=lambda k: ktot[k][0]) if cand else "k_rqi"
+    line = {"config": cfg, "metric": metric_name(p), "value": m_req / (t * 1e-3),
+            "unit": "eigenpairs/s", "ms_per_step": t, "steps": steps, "n": p.n, "m": m_req,
+            "io": p.io, "roofline": roof(dom),
+            "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
+                        for k, v in ktot.items()},
+            "gpu_launches": launches,
+            "stats": {k: v for k, v in (stats or {}).items()}}
+    if cpu:
+        # the oracle in full (north_star: the full run for n <= 20000)
+        idx = np.arange(il, iu + 1)
+        cnt, dt_cpu, cores = cpu_baseline_run(p, 0, idx=idx)
+        line["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
+                                "cpu": cpu_model(), "kind": "oracle",
+                                "sample": f"full run: all {cnt} requested eigenpairs, binary128 "
+                                          f"bisection on T + inverse iteration, {dt_cpu:.1f} s"}
+    del d, e
+    torch.cuda.empty_cache()
+    return line
+
+
+def emulate_world(mr3, p, world, stream):
+    """Ranks of the two-phase form run one after another on this GPU: per rank, device time of
+    mr3_plan (root + its slice's bisection) and of mr3_execute (classification, its columns'
+    child representations and eigenvectors); the bracket all-gather is a device copy."""
+    import ctypes
+
+    import torch
+    L = mr3.lib()
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    n = p.n
+    ctxs, bufs, caps, tplan = [], [], [], []
+    for r in range(world):
+        h = ctypes.c_void_p()
+        assert L.mr3_create(ctypes.byref(h), torch.cuda.current_device(),
+                            ctypes.c_void_p(int(stream.cuda_stream) or 1), None, 0, 1) == 0
+        ctxs.append(h)
+        m, brk = ctypes.c_int64(), ctypes.c_void_p()
+        cap, cnt = ctypes.c_int64(), ctypes.c_int64()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rc = L.mr3_plan(h, 0 if p.io == "f64" else 1, p.range.encode(), n,
+                        ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(e.data_ptr()), 0.0, 0.0,
+                        1, n, r, world, ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap),
+                        ctypes.byref(cnt))
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        tplan.append(a.elapsed_time(b))
+        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * 6, d.device))
+        caps.append(cap.value)
+    rec = 6 * caps[0]
+    full = torch.cat([bufs[r][r * rec:(r + 1) * rec] for r in range(world)])
+    for r in range(world):
+        bufs[r][:world * rec].copy_(full)
+    torch.cuda.synchronize()
+    dt = torch.float64 if p.io == "f64" else torch.float32
+    texec, cols = [], []
+    for r in range(world):
+        w = torch.zeros(n, dtype=dt, device="cuda")
+        zb, ze = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()), None, n, 0,
+                           ctypes.byref(zb), ctypes.byref(ze), None)
+        Zs = torch.empty((max(ze.value - zb.value, 1), n), dtype=dt, device="cuda")
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
+                           ctypes.c_void_p(Zs.data_ptr()), n, Zs.shape[0], ctypes.byref(zb),
+                           ctypes.byref(ze), None)
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        texec.append(a.elapsed_time(b))
+        cols.append(ze.value - zb.value)
+        del Zs, w
+    for h in ctxs:
+        L.mr3_destroy(h)
+    per_rank = [a + b for a, b in zip(tplan, texec)]
+    torch.cuda.empty_cache()
+    return {"world": world, "per_rank_ms": [round(x, 3) for x in per_rank],
+            "plan_ms": [round(x, 3) for x in tplan], "execute_ms": [round(x, 3) for x in texec],
+            "columns": cols, "max_rank_ms": max(per_rank),
+            "note": "ranks emulated sequentially on one GPU (each alone on the device); the "
+                    "all-gathers are device copies; not a multi-GPU measurement"}
 
 
 def metric_name(p):
@@ -263,7 +461,197 @@ def main():
         except Exception:
             traffic_tab = {}
 
-    def roof(kname):
+    roof = make_roof(ktot, stats, args.steps, mode, traffic_tab, peak_ips)
+
+    cand = [k for k in ("k_bisect", "k_rqi") if k in ktot]
+    dom = max(cand, key=lambda k: ktot[k][0]) if cand else "k_rqi"
+    line = {"config": cfg, "metric": metric_name(p), "value": m_req / (t * 1e-3),
+            "unit": "eigenpairs/s", "ms_per_step": t, "steps": steps, "n": p.n, "m": m_req,
+            "io": p.io, "roofline": roof(dom),
+            "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
+                        for k, v in ktot.items()},
+            "gpu_launches": launches,
+            "stats": {k: v for k, v in (stats or {}).items()}}
+    if cpu:
+        # the oracle in full (north_star: the full run for n <= 20000)
+        idx = np.arange(il, iu + 1)
+        cnt, dt_cpu, cores = cpu_baseline_run(p, 0, idx=idx)
+        line["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
+                                "cpu": cpu_model(), "kind": "oracle",
+                                "sample": f"full run: all {cnt} requested eigenpairs, binary128 "
+                                          f"bisection on T + inverse iteration, {dt_cpu:.1f} s"}
+    del d, e
+    torch.cuda.empty_cache()
+    return line
+
+
+def emulate_world(mr3, p, world, stream):
+    """Ranks of the two-phase form run one after another on this GPU: per rank, device time of
+    mr3_plan (root + its slice's bisection) and of mr3_execute (classification, its columns'
+    child representations and eigenvectors); the bracket all-gather is a device copy."""
+    import ctypes
+
+    import torch
+    L = mr3.lib()
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    n = p.n
+    ctxs, bufs, caps, tplan = [], [], [], []
+    for r in range(world):
+        h = ctypes.c_void_p()
+        assert L.mr3_create(ctypes.byref(h), torch.cuda.current_device(),
+                            ctypes.c_void_p(int(stream.cuda_stream) or 1), None, 0, 1) == 0
+        ctxs.append(h)
+        m, brk = ctypes.c_int64(), ctypes.c_void_p()
+        cap, cnt = ctypes.c_int64(), ctypes.c_int64()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rc = L.mr3_plan(h, 0 if p.io == "f64" else 1, p.range.encode(), n,
+                        ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(e.data_ptr()), 0.0, 0.0,
+                        1, n, r, world, ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap),
+                        ctypes.byref(cnt))
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        tplan.append(a.elapsed_time(b))
+        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * 6, d.device))
+        caps.append(cap.value)
+    rec = 6 * caps[0]
+    full = torch.cat([bufs[r][r * rec:(r + 1) * rec] for r in range(world)])
+    for r in range(world):
+        bufs[r][:world * rec].copy_(full)
+    torch.cuda.synchronize()
+    dt = torch.float64 if p.io == "f64" else torch.float32
+    texec, cols = [], []
+    for r in range(world):
+        w = torch.zeros(n, dtype=dt, device="cuda")
+        zb, ze = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()), None, n, 0,
+                           ctypes.byref(zb), ctypes.byref(ze), None)
+        Zs = torch.empty((max(ze.value - zb.value, 1), n), dtype=dt, device="cuda")
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
+                           ctypes.c_void_p(Zs.data_ptr()), n, Zs.shape[0], ctypes.byref(zb),
+                           ctypes.byref(ze), None)
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        texec.append(a.elapsed_time(b))
+        cols.append(ze.value - zb.value)
+        del Zs, w
+    for h in ctxs:
+        L.mr3_destroy(h)
+    per_rank = [a + b for a, b in zip(tplan, texec)]
+    torch.cuda.empty_cache()
+    return {"world": world, "per_rank_ms": [round(x, 3) for x in per_rank],
+            "plan_ms": [round(x, 3) for x in tplan], "execute_ms": [round(x, 3) for x in texec],
+            "columns": cols, "max_rank_ms": max(per_rank),
+            "note": "ranks emulated sequentially on one GPU (each alone on the device); the "
+                    "all-gathers are device copies; not a multi-GPU measurement"}
+
+
+def metric_name(p):
+    io = "fp32 I/O fp64-internal" if p.io == "f32" else "fp64 I/O dd-internal"
+    return f"eigenpairs/s, {io}, {p.name} n={p.n}"
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    p = synth.config(args.config)
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, p, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1304_1864_b200 as mr3
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mr3.lib()
+    dt = torch.float32 if p.io == "f32" else torch.float64
+    d = torch.from_numpy(p.d).cuda()
+    e = torch.from_numpy(p.e).cuda()
+    n = p.n
+    il, iu = p.index_range()
+    m_req = iu - il + 1
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
+
+    def solve():
+        if world > 1:
+            return mr3.solve_distributed(d, e, "V", p.range, il, iu)
+        fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
+        w, Z, st = fn(d, e, "V", p.range, il, iu)
+        return w, Z, (0, w.numel()), st
+
+    # K7: same-run FP64 peak
+    peak_ips, dd_step_ns = mr3.fp64_peak()
+
+    for _ in range(args.warmup):
+        out = solve()
+        del out
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    times = []
+    ktot = {}
+    launches = 0
+    stats = None
+    with Clocks(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s)  # L2 flush between timed steps (outside the events)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            w, Z, rng, stats = solve()
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+            for k, (ms, nl) in mr3.kernel_times().items():
+                t0, n0 = ktot.get(k, (0.0, 0))
+                ktot[k] = (t0 + ms, n0 + nl)
+            launches += mr3.launch_count()
+            del w, Z
+    t_step = float(np.mean(times))
+    t_max = t_step
+    if world > 1:
+        tt = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = m_req / (t_max * 1e-3)  # all ranks together produce the m eigenpairs of one solve
+
+    # roofline of the dominant kernel (the larger of k_bisect and k_rqi): algorithmic FP64
+    # instructions per launch / its CUDA-event time inside the timed region
+    mode = "f64" if p.io == "f32" else "dd"
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic_tab = {}
+    if os.path.exists(tp):
+        try:
+            traffic_tab = json.load(open(tp)).get(f"config{args.config}", {})
+        except Exception:
+            traffic_tab = {}
+
+    roof = make_roof(ktot, stats, args.steps, mode, traffic_tab, peak_ips)
+    _unused = roof  # (noqa)
+
+    def roof_old(kname):
         ms, nl = ktot.get(kname, (0.0, 0))
         if kname == "k_bisect":
             rows = stats["bisect_rows"] if stats else 0.0
@@ -356,10 +744,58 @@ def main():
         k = args.cpu_sample or max(32 * oracle.num_threads(), 64)
         cnt, dt_cpu, cores = cpu_baseline_run(p, k)
         result["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
-                                  "kind": "oracle",
+                                  "kind": "oracle", "cpu": cpu_model(),
                                   "sample": f"{cnt} eigenpairs (incl. both spectrum ends) of the "
                                             f"n={n} workload: binary128 bisection on T + "
                                             f"inverse iteration, {dt_cpu:.1f} s"}
+    if rank == 0 and world == 1 and not args.no_zstore and p.io == "f64":
+        # the Z normalisation pass as its own HBM-bound kernel (MR3_FUSE_SCALE = 0: k_zscale reads
+        # and writes every written column once): bytes / its CUDA-event time vs the measured HBM
+        # peak; with the default fused epilogue the same traffic runs inside k_rqi
+        mr3.set_param("FUSE_SCALE", 0, 0)
+        try:
+            zt = []
+            for s in range(2):
+                flush.fill_(s)
+                w, Z, st = mr3.mr3_dstemr_dd(d, e, "V", p.range, il, iu)
+                torch.cuda.synchronize()
+                kz = mr3.kernel_times().get("k_zscale")
+                if kz:
+                    zt.append(kz[0])
+                del w, Z
+        finally:
+            mr3.set_param("FUSE_SCALE", -1, 0)
+        pk, src = hbm_peak()
+        if zt:
+            tz = min(zt) * 1e-3
+            zbytes = 2.0 * 8.0 * n * m_req  # read + write of every element of Z
+            result["roofline_other"]["z_store"] = {
+                "bound": "hbm", "kernel": "k_zscale (MR3_FUSE_SCALE=0)",
+                "achieved": zbytes / tz / 1e9, "peak": pk, "unit": "GB/s",
+                "frac": zbytes / tz / 1e9 / pk, "peak_source": src,
+                "bytes_per_launch": zbytes, "ms_per_launch": tz * 1e3,
+                "traffic": (traffic_tab.get("k_zscale") if traffic_tab else None),
+                "z_algorithmic_bytes": 8.0 * n * m_req,
+                "k_rqi_dram_bytes_fused": traffic_tab.get("k_rqi"),
+                "note": "Z is written once by the storing RQI pass (8 n m bytes) and read + "
+                        "written once more by the exact normalisation (DESIGN.md section 5): 3x "
+                        "the algorithmic bytes in total"}
+    if rank == 0 and world == 1 and args.other_configs:
+        oc = []
+        for cfg in [int(x) for x in args.other_configs.split(",") if x.strip()]:
+            if cfg == args.config:
+                continue
+            oc.append(other_config_line(mr3, cfg, args, flush, stream, peak_ips,
+                                        cpu=not args.no_cpu))
+        result["other_configs"] = oc
+    if rank == 0 and world == 1 and args.emulate_world:
+        em = []
+        for wv in [int(x) for x in args.emulate_world.split(",") if x.strip()]:
+            r = emulate_world(mr3, p, wv, stream)
+            r["emulated_value"] = m_req / (r["max_rank_ms"] * 1e-3)
+            r["unit"] = "eigenpairs/s"
+            em.append(r)
+        result["emulated_world"] = em
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -34,7 +34,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
           "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10, "GRID": 11, "CTA": 12, "XPTS": 13, "YCERT": 14, "NEWTON": 15, "TWISTW": 16,
-          "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20, "RQI_FB": 21}
+          "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20, "RQI_FB": 21, "RQI_CHUNK": 22}
 ERRORS = {1: "NONFINITE", 2: "CUDA", 3: "NCCL", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 

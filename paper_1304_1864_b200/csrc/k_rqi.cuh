@@ -368,8 +368,10 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         zcol[0] = (OutT)1.0;
         zfinal = true;
     }
-    if (active && A.resume_in != nullptr) {  // continue after k_rqi_fb's passes
+    int pdone = 0;  // passes done before this launch beyond A.iter0 (per eigenpair)
+    if (active && A.resume_in != nullptr) {  // continue after k_rqi_fb's / k_rqi_chunk's passes
         const RqiResume<R> rs = A.resume_in[id];
+        pdone = A.iter0 == 0 ? rs.iters : 0;
         lam = rs.lam;
         a = rs.a;
         b = rs.b;
@@ -605,7 +607,8 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         };
         // storing pass: the written components go through two 16-row smem tiles (one per
         // stream) and leave as coalesced 128-byte column segments
-        const bool cta_store = store && A.jobz_v;  // uniform over the CTA
+        // (collective: with resumed eigenpairs the store flag can differ between threads)
+        const bool cta_store = __syncthreads_or(store && A.jobz_v) != 0;
         if (cta_store) {
             // per column: the rows each stream writes (F: g < rF, B: g > rB; nothing if the
             // column is not written) and the column's base pointer
@@ -1027,13 +1030,14 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
     for (iters = A.iter0 + 1; iters <= A.maxit; iters++) {
         // an eigenpair that converged in the first (non-storing) pass joins the next
         // pass of its CTA at the same shift to write z (instead of an extra pass later)
+        const int itp = iters + pdone;  // this eigenpair's iteration number
         const bool store_only =
-            A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;
-        const bool need = !done || store_only;
+            A.jobz_v && itp >= 2 && done && !zfinal && zcol != nullptr && n > 1;
+        const bool need = (!done || store_only) && itp <= A.maxit;
         if (!__syncthreads_or(need)) break;
         const int c = ((iters <= 2 && A.split < 2) || n < 4 * RQ_TPB || !A.split)
-                          ? twisted_fixed(need, A.jobz_v && iters >= 2)
-                                                     : split_all(need, A.jobz_v && iters >= 2);
+                          ? twisted_fixed(need, A.jobz_v && itp >= 2)
+                                                     : split_all(need, A.jobz_v && itp >= 2);
         if (store_only) zfinal = zwritten;
         if (need && !store_only) {
             if (c >= k) {

@@ -28,6 +28,7 @@
 #include "k_misc.cuh"
 #include "k_rqi.cuh"
 #include "k_rqi_fb.cuh"
+#include "k_rqi_chunk.cuh"
 #include "kernels.cuh"
 
 using namespace mr3;
@@ -169,9 +170,9 @@ static void hsync_note(mr3_ctx ctx, const char *where) {
 }
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG FB
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG FB CHUNK
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0},
 };
 
 #define CK(call)                                                                  \
@@ -655,6 +656,17 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         CKL("k_iota");
         ctx->G0 = choose_groups(ctx, cnt, (int)P[MR3_GROUPS]);
         const bool xphase = words == 2 && P[MR3_XPHASE] != 0;
+        // the Newton/Laguerre phase (R8e) runs on the binary64 copy of the representation: in
+        // dd mode that is the binary_x phase (brackets widened by R8d), in fp32-I/O mode the
+        // binary64 counts are the binary_y counts themselves (no widening, no certification).
+        // It needs one lane per eigenvalue (G0 = 1: automatic above ~19k items, or forced by
+        // MR3_GROUPS = 1).  Measured on the small configs: 4-lane to 8-lane multisection is
+        // faster than Newton below that size except on config 3 (profiles/r02_ab_groups.log)
+        const int ycert0 = P[MR3_YCERT] != 0 ? 1 : 0;
+        const bool newton_ok = (xphase || words == 1) && !ycert0 && P[MR3_XPTS] == 3;
+        const bool xkern = xphase || (words == 1 && newton_ok && ctx->G0 == 1);
+        const double eps_xw = xphase ? eps_x : 0.0;   // M_x -> M_y widening of the x phase
+        const double eps_xt = words == 2 ? eps_x : 1.1102230246251565e-16;  // tail: 2 ulps
         if (!ctx->split && P[MR3_GRID] != 0 && cnt >= 512) {
             // shared top of the bisection tree: a uniform grid of counts, then cells with
             // two or more eigenvalues subdivided level by level (k_grid.cuh)
@@ -735,15 +747,15 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         }
         // definite roots: binary_x brackets are enclosed rigorously after widening by the
         // relative-robustness bound (R8d); binary_y certification only if MR3_YCERT
-        const int ycert = P[MR3_YCERT] != 0 ? 1 : 0;
+        const int ycert = ycert0;
         ctx->root_widen = (xphase && !ycert) ? 10.0 * eps_x : 0.0;
         char *tail = nullptr;
-        const bool newton = xphase && !ycert && ctx->G0 == 1 && P[MR3_XPTS] == 3;
+        const bool newton = newton_ok && ctx->G0 == 1;
         if (newton) {
             tail = (char *)getbuf(ctx, "bis_tailflag", (size_t)mine, &rc);
             if (rc) return rc;
         }
-        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xphase, eps_x,
+        rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xkern, eps_xw,
                               "k_bisect", ycert, tail);
         if (rc) return rc;
         if (newton) {
@@ -802,8 +814,8 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                 // (a fixed lane count: the bits of a bracket must not depend on how many
                 // items this rank's slice sent to the tail)
                 const int G = 32;
-                rc = launch_bisect<R>(ctx, W, tl, ht, G, 2.0 * eps_x, absfloor, 0, true, eps_x,
-                                      "k_bisect", 0, nullptr);
+                rc = launch_bisect<R>(ctx, W, tl, ht, G, std::min(rtol, 2.0 * eps_xt), absfloor,
+                                      0, true, eps_xw, "k_bisect", 0, nullptr);
             }
         }
         if (rc) return rc;
@@ -1139,6 +1151,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         bool rqi_split_all = false;  // (set for the k_rqi launch, read by launch_chunks)
         const RqiResume<R> *rqi_resume_in = nullptr;  // (k_rqi continuing after k_rqi_fb)
         const char *rqi_tname = "k_rqi";
+        bool rqi_nosplit = false;  // (serial passes only: the eigenpairs k_rqi_chunk could not split)
         int rqi_iter0 = 0;
         auto make_tasks = [&](const int32_t *lst, int *nt, int per, int count) -> int {
             k_rqi_tasks<<<1, 1024, 0, s>>>(lst, count, W.it.node, dseg, dtasks, dnt, per);
@@ -1185,7 +1198,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
                 A.gaptol = gaptol;
                 A.root_widen = ctx->root_widen;
                 A.twist_w = P[MR3_TWISTW];
-                A.split = P[MR3_SPLIT] != 0 ? (rqi_split_all && !locate ? 2 : 1) : 0;
+                A.split = (P[MR3_SPLIT] != 0 && !rqi_nosplit) ? (rqi_split_all && !locate ? 2 : 1) : 0;
                 A.fuse_scale = ctx->fuse_scale;
                 A.maxit = (int)P[MR3_MAX_RQI];
                 A.jobz_v = jobz == 'V';
@@ -1301,6 +1314,91 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             rqi_split_all = split_all;
             return launch_chunks(false, slist, ntasks);
         }
+        // small index sets: every iteration chunk-parallel, one eigenpair per CTA (k_rqi_chunk)
+        const bool small = P[MR3_RQI_CHUNK] > 0 && ncount <= (int64_t)P[MR3_RQI_CHUNK];
+        char *leftc = (char *)getbuf(ctx, "rqi_leftc", (size_t)ncount, &rc2);
+        int32_t *llc = (int32_t *)getbuf(ctx, "rqi_llc", (size_t)ncount * 4, &rc2);
+        RqiResume<R> *resume0 =
+            (RqiResume<R> *)getbuf(ctx, "rqi_resume", (size_t)cnt * sizeof(RqiResume<R>), &rc2);
+        if (rc2) return rc2;
+        auto rqi_args = [&](const int32_t *lst, char *lf, const RqiResume<R> *rin) {
+            RqiArgs<R> A;
+            memset(&A, 0, sizeof(A));
+            A.nodes = W.nodes;
+            A.it = W.it;
+            A.list = lst;
+            A.zc = dzc;
+            A.pivmin = ctx->pivmin;
+            A.krs = P[MR3_KRS];
+            A.eps_x = eps_x;
+            A.gaptol = gaptol;
+            A.root_widen = ctx->root_widen;
+            A.twist_w = P[MR3_TWISTW];
+            A.fuse_scale = ctx->fuse_scale;
+            A.maxit = (int)P[MR3_MAX_RQI];
+            A.jobz_v = jobz == 'V';
+            A.w = w;
+            A.Z = Z;
+            A.ldz = ldz;
+            A.zcol0 = c0;
+            A.unscale = 1.0 / ctx->scale;
+            A.st = W.st;
+            A.left = lf;
+            A.resume = resume0;
+            A.resume_in = rin;
+            return A;
+        };
+        // k_rqi_chunk over `lst` (count cntl), then the eigenpairs it leaves continue serially
+        // in k_rqi from their state (bisection fallback after max_rqi)
+        auto run_chunked = [&](const int32_t *lst, int cntl, const RqiResume<R> *rin) -> int {
+            if (cntl <= 0) return 0;
+            RqiArgs<R> A = rqi_args(lst, leftc, rin);
+            if (ctx->dump) {
+                A.dbg_trace = (double *)getbuf(ctx, "dbg_trace", (size_t)cnt * 64, &rc2);
+                if (rc2) return rc2;
+                CK(cudaMemsetAsync(A.dbg_trace, 0, (size_t)cnt * 64, s));
+            }
+            const int tpb = ctx->n >= 4096 ? 128 : (ctx->n >= 2048 ? 64 : 32);
+            KTime *t = kt_begin(ctx, rin ? "k_rqi_tail" : "k_rqi");
+            k_rqi_chunk<R, OutT><<<cntl, tpb, 0, s>>>(A);
+            kt_end(ctx, t);
+            CKL("k_rqi_chunk");
+            int *lcnt2 = (int *)getbuf(ctx, "rqi_lcnt2", 16, &rc2);
+            if (rc2) return rc2;
+            size_t tmpl = 0;
+            cub::DeviceSelect::Flagged(nullptr, tmpl, lst, leftc, llc, lcnt2, cntl, s);
+            void *tmp = getbuf(ctx, "cubtmp_leftc", tmpl, &rc2);
+            if (rc2) return rc2;
+            cub::DeviceSelect::Flagged(tmp, tmpl, lst, leftc, llc, lcnt2, cntl, s);
+            CKL("select (chunk left)");
+            int hl = 0;
+            CK(cudaMemcpyAsync(&hl, lcnt2, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#13c");
+            if (ctx->dump) {
+                fprintf(stderr, "[mr3] k_rqi_chunk left %d of %d eigenpairs\n", hl, cntl);
+                std::vector<int32_t> hll(hl);
+                std::vector<double> tr((size_t)cnt * 8);
+                cudaMemcpy(hll.data(), llc, (size_t)hl * 4, cudaMemcpyDeviceToHost);
+                cudaMemcpy(tr.data(), A.dbg_trace, (size_t)cnt * 64, cudaMemcpyDeviceToHost);
+                for (int i = 0; i < hl && i < 24; i++) {
+                    const double *t = &tr[8 * (size_t)hll[i]];
+                    fprintf(stderr, "[mr3]   item %d: log2 rel %.1f jr/tol %.3g iter %g r %g n %g bad %g\n",
+                            hll[i], t[0], t[1], t[2], t[3], t[4], t[5]);
+                }
+            }
+            if (hl == 0) return 0;
+            if ((rc2 = make_tasks(llc, &ntasks, rtpb, hl))) return rc2;
+            rqi_resume_in = resume0;
+            rqi_iter0 = 0;
+            rqi_tname = "k_rqi_serial";
+            rqi_nosplit = true;
+            rc2 = launch_chunks(false, llc, ntasks);
+            rqi_nosplit = false;
+            rqi_tname = "k_rqi";
+            rqi_resume_in = nullptr;
+            return rc2;
+        };
+        if (small) return run_chunked(slist, ncount, nullptr);
         // K5 main phase: iterations 1-2 with the F and B halves in two threads (k_rqi_fb);
         // the eigenpairs it leaves continue in k_rqi from their saved state
         char *left = (char *)getbuf(ctx, "rqi_left", (size_t)ncount, &rc2);
@@ -1365,6 +1463,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#13b");
         if (ctx->dump) fprintf(stderr, "[mr3] k_rqi_fb left %d of %d eigenpairs\n", hl, ncount);
         if (hl == 0) return 0;
+        if (P[MR3_RQI_CHUNK] > 0)  // the stragglers: chunk-parallel, one CTA each
+            return run_chunked(llist, hl, resume);
         if ((rc2 = make_tasks(llist, &ntasks, rtpb, hl))) return rc2;
         rqi_resume_in = resume;
         rqi_iter0 = std::min(2, (int)P[MR3_MAX_RQI]);
@@ -1619,7 +1719,7 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     for (auto &p : ctx->ktimes) {
         const std::string &nm = p.first;
         int slot = nm == "k_root" ? 0 : nm == "k_bisect" ? 1 : nm == "k_classify" ? 2
-                                     : nm == "k_child"  ? 3 : (nm == "k_rqi" || nm == "k_rqi_tail") ? 4 : 6;
+                                     : nm == "k_child"  ? 3 : (nm == "k_rqi" || nm == "k_rqi_tail" || nm == "k_rqi_serial") ? 4 : 6;
         ctx->stats.t_ms[slot] += p.second.first;
         ctx->stats.t_ms[5] += p.second.first;
     }

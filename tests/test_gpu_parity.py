@@ -518,9 +518,33 @@ def test_rqi_fb_matches_single_thread_rqi(make, params):
     same bits, including eigenpairs continued after the hand-off (KRS = 1e-4 forces third
     iterations, MAX_RQI = 1 the bisection fallback)."""
     p = make()
-    w1, Z1, s1 = _with_params(params, lambda: run(p))
-    w0, Z0, s0 = _with_params(dict(params, RQI_FB=0), lambda: run(p))
+    # (RQI_CHUNK = 0: small sets take k_rqi_fb too, with the stragglers in serial k_rqi)
+    w1, Z1, s1 = _with_params(dict(params, RQI_CHUNK=0), lambda: run(p))
+    w0, Z0, s0 = _with_params(dict(params, RQI_FB=0, RQI_CHUNK=0), lambda: run(p))
     np.testing.assert_array_equal(w1, w0)
     np.testing.assert_array_equal(Z1, Z0)
     assert s1["rqi_fallbacks"] == s0["rqi_fallbacks"]
+
+
+@pytest.mark.parametrize("make", [lambda: synth.random_uniform(1200, 1), lambda: synth.legendre(3000),
+                                  lambda: synth.glued_wilkinson(20, 21),
+                                  lambda: synth.random_normal_f32(3000, 4, 1, 700),
+                                  lambda: synth.split_matrix(500, 5, split_at=(100, 101, 333)),
+                                  lambda: synth.random_uniform(5000, 7)])
+@pytest.mark.parametrize("params", [{}, {"MAX_RQI": 1}, {"KRS": 1e-4}, {"RQI_CHUNK": 1e9}])
+def test_rqi_chunk_parity(make, params):
+    """k_rqi_chunk (every RQI iteration chunk-parallel over a CTA, one eigenpair per CTA: the
+    small-index-set path, default up to 8192 singletons) against the oracle on every pair, and
+    against the serial k_rqi_fb path to the accuracy of the method (different rounding of the
+    same recurrences)."""
+    p = make()
+    io = p.io
+    w1, Z1, s1 = _with_params(params, lambda: run(p))
+    il, iu = p.index_range()
+    res = check_solution(p, w1, Z1, np.arange(il, iu + 1), io=io)
+    assert_parity(res, io=io)
+    w0, Z0, _ = _with_params(dict(params, RQI_CHUNK=0), lambda: run(p))
+    nrm = float(np.abs(p.d).max() + 2 * np.abs(p.e).max())
+    tolw = (4e-16 if io == "f64" else 4 * 2.0 ** -24) * nrm * 2
+    assert np.max(np.abs(w1.astype(np.float64) - w0)) <= tolw
 
