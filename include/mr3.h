@@ -109,9 +109,9 @@ enum mr3_param {
                           two threads (k_rqi_fb), later iterations in k_rqi; 2: the same with the
                           row update in two-dot-product form (shorter dependent chain);
                           0: all in k_rqi; 1 */
-    MR3_RQI_CHUNK = 22, /* index sets of at most this many singletons run every RQI iteration
-                           chunk-parallel, one eigenpair per CTA (k_rqi_chunk; also the
-                           stragglers of k_rqi_fb); 0 = off; 8192 */
+    MR3_RQI_CHUNK = 22, /* solves of at most this many wanted eigenpairs (globally) run every
+                           RQI iteration chunk-parallel, one eigenpair per CTA (k_rqi_chunk;
+                           it also takes the stragglers of k_rqi_fb); 0 = off; 8192 */
     MR3_NPARAM = 23
 };
 

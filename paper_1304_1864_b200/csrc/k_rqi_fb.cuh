@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
     using G0 = std::integral_constant<bool, false>;
     using G1 = std::integral_constant<bool, true>;
     // one fixed-twist factorization at lam for the eigenpairs with `need` (collective)
-    auto pass = [&](bool need, bool store) -> int {
+    // (STORE is a compile-time flag: the non-storing pass carries no z-store code per row)
+    auto pass = [&](bool need, auto store_c) -> int {
+        constexpr bool STORE = decltype(store_c)::value;
         if (need) zwritten = false;
         const R mlam = neg(lam);
         R px = mlam, qx = mk<R>(1.0);  // F: (pF, qF); B: (pB, qB)
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
         const int ntile = (int)((n + RQ_TR - 1) / RQ_TR);
         const int nA = cta_rmax / RQ_TR + 1;
         const int nD = ntile - cta_rmin / RQ_TR;
-        const bool wz = store && need && zcol != nullptr;
+        const bool wz = STORE && need && zcol != nullptr;
         const int eref = role == 0 ? erefF : erefB;
         auto rescale = [](R &x, R &y, int &E) {
             const unsigned ex = (unsigned)__double2hiint(hi(x)) & 0x7ff00000u;
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
                 qx = E;
             }
         };
-        const bool cta_store = store && A.jobz_v;  // uniform over the CTA
+        const bool cta_store = STORE && A.jobz_v;  // uniform over the CTA
         if (cta_store && role == 0) {
             s_rb[pi] = wz ? make_int2((int)r, (int)r) : make_int2(-1, INT_MAX);
             s_zp[pi] = wz ? reinterpret_cast<OutT *>(A.Z) + (col0 - A.zcol0) * A.ldz + nd.row0
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;
         const bool need = !done || store_only;
         if (!__syncthreads_or(need)) break;
-        const int c = pass(need, A.jobz_v && iters >= 2);
+        const int c = (A.jobz_v && iters >= 2) ? pass(need, std::integral_constant<bool, true>{})
+                                                : pass(need, std::integral_constant<bool, false>{});
         if (need) passes = iters;
         if (store_only) zfinal = zwritten;
         if (need && !store_only) {

@@ -1315,7 +1315,9 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
             return launch_chunks(false, slist, ntasks);
         }
         // small index sets: every iteration chunk-parallel, one eigenpair per CTA (k_rqi_chunk)
-        const bool small = P[MR3_RQI_CHUNK] > 0 && ncount <= (int64_t)P[MR3_RQI_CHUNK];
+        // (decided by the global number of wanted eigenpairs, not this rank's or this level's
+        // singletons: the path, hence every bit, must not depend on the world size)
+        const bool small = P[MR3_RQI_CHUNK] > 0 && ctx->m <= (int64_t)P[MR3_RQI_CHUNK];
         char *leftc = (char *)getbuf(ctx, "rqi_leftc", (size_t)ncount, &rc2);
         int32_t *llc = (int32_t *)getbuf(ctx, "rqi_llc", (size_t)ncount * 4, &rc2);
         RqiResume<R> *resume0 =
