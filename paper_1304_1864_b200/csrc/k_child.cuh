@@ -4,30 +4,6 @@
 
 namespace mr3 {
 
-// dstqds with shift tau, ratio form with the pivot
-// guard of reading R6 (the sequential write, used when the chunked write below detects a jump):
-//   s_1 = -tau ; d+_i = d_i + s_i ; l+_i = ld_i / d+_i ; s_{i+1} = l+_i l_i s_i - tau
-// L+D+L+^T = LDL^T - tau I.
-template <class R>
-__device__ void dstqds_write(const double *__restrict__ rep, int64_t n, R tau, double pivmin,
-                             double *__restrict__ child, double *__restrict__ childx) {
-    R s = neg(tau);
-#pragma unroll 1
-    for (int64_t i = 0; i < n; i++) {
-        Row4<R> r = load_row4<R>(rep, i);
-        R dp = guard(add(r.d, s), pivmin);
-        R lp = mk<R>(0.0);
-        if (i < n - 1) {
-            lp = div(r.ld, dp);
-            s = sub(mul(mul(lp, r.l), s), tau);
-        }
-        R ldp = mul(dp, lp);
-        R lldp = mul(ldp, lp);
-        store_row4<R>(child, i, dp, lldp, lp, ldp);
-        reinterpret_cast<double2 *>(childx)[i] = make_double2(hi(dp), hi(lldp));
-    }
-}
-
 // Rows of the parent staged through shared memory (all 32 lanes read the same row: broadcast),
 // double-buffered with cp.async: tiles of CH_TR rows.
 constexpr int CH_TR = 32;
@@ -115,7 +91,10 @@ __device__ __forceinline__ void child_rescale(R &p, R &q) {  // by a power of tw
 // as a projective point -- a pivot guard fired inside it (the guard is not linear), or the
 // chained products lost accuracy (strongly graded / glued parents: measured on glued
 // Wilkinson, 2^-40 let a child through whose eigenvectors came out at residual 5e-13) --
-// sends the whole child to the sequential write by lane 0.
+// sends the whole child to the sequential write: lane 0 runs the growth pass's projective
+// recurrence over rows the warp stages through shared memory.
+// (dstqds: s_1 = -tau; d+_i = d_i + s_i;
+// l+_i = ld_i / d+_i; s_{i+1} = l+_i l_i s_i - tau; L+D+L+^T = LDL^T - tau I.)
 template <class R>
 __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, Items it,
                                               const int32_t *__restrict__ next_active,
@@ -151,7 +130,10 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     R tau = side ? add(lamR, mk<R>(delta)) : sub(lamL, mk<R>(delta));
     const R mtau = neg(tau);
 
-    // ---- growth pass (staged rows, one candidate per lane)
+    double *child = child_pool + (int64_t)c * pool_stride_rows * 4 * Prec<R>::words;
+    double *childx = childx_pool + (int64_t)c * pool_stride_rows * 2;
+    // ---- growth pass (staged rows, one candidate per lane); lane 0's candidate -- the nearest
+    // shift, the usual winner -- writes its child rows on the way (speculative write)
     double growth = 0.0;
     bool bad = false;
     {
@@ -176,6 +158,16 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
                 const double dp = fabs(hi(D) * rcp(hi(q)));  // |d+| (growth only)
                 bad |= !(dp <= 1e300);
                 growth = fmax(growth, dp);
+                if (lane == 0) {
+                    const int64_t k = (int64_t)t * CH_TR + j;
+                    const R dpr = div(D, q);  // d+_k
+                    R lp = mk<R>(0.0);
+                    if (k < n - 1) lp = div(rw.ld, dpr);
+                    const R ldp = mul(dpr, lp);
+                    const R lldp = mul(ldp, lp);
+                    store_row4<R>(child, k, dpr, lldp, lp, ldp);
+                    reinterpret_cast<double2 *>(childx)[k] = make_double2(hi(dpr), hi(lldp));
+                }
                 p = fma_dd(mtau, D, mul(rw.lld, p));
                 q = D;
                 if ((j & 7) == 7) child_rescale<R>(p, q);
@@ -209,8 +201,7 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     }
     const R t = shfl_R<R>(0xffffffffu, tau, win, 32);
     const R mt = neg(t);
-    double *child = child_pool + (int64_t)c * pool_stride_rows * 4 * Prec<R>::words;
-    double *childx = childx_pool + (int64_t)c * pool_stride_rows * 2;
+    if (win != 0) {  // (uniform) the speculative child is not the chosen one: write it
 
     // ---- write pass, chunk-parallel (see above)
     const int64_t L = (n + 31) / 32;
@@ -293,10 +284,48 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
         const double tolj = Prec<R>::words == 2 ? 0x1p-100 : 0x1p-50;
         jump = !(cross <= tolj * mag);
     }
-    if (__any_sync(0xffffffffu, jump)) {  // sequential write (ratio form, reading R6 guard)
+    if (__any_sync(0xffffffffu, jump)) {
+        // sequential write: the projective recurrence of the growth pass (the same guard),
+        // rows staged through shared memory by the warp, lane 0 runs the chain
         __syncwarp();
-        if (lane == 0) dstqds_write<R>(P.rep, n, t, pivmin, child, childx);
+        R p = mt, q = mk<R>(1.0);
+        const int ntile = (int)((n + CH_TR - 1) / CH_TR);
+        child_stage<R>(sbuf[0], P.rep, n, 0);
+#pragma unroll 1
+        for (int ti = 0; ti < ntile; ti++) {
+            if (ti + 1 < ntile) {
+                child_stage<R>(sbuf[(ti + 1) & 1], P.rep, n, (int64_t)(ti + 1) * CH_TR);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const double *buf = sbuf[ti & 1];
+                const int64_t k0t = (int64_t)ti * CH_TR;
+                const int jn = (int)min((int64_t)CH_TR, n - k0t);
+#pragma unroll 4
+                for (int j = 0; j < jn; j++) {
+                    const int64_t k = k0t + j;
+                    const Row4<R> rw = child_row<R>(buf, j);
+                    const R D = child_D<R>(rw, p, q, pivmin);
+                    const R dp = div(D, q);  // d+_k
+                    R lp = mk<R>(0.0);
+                    if (k < n - 1) lp = div(rw.ld, dp);
+                    const R ldp = mul(dp, lp);
+                    const R lldp = mul(ldp, lp);
+                    store_row4<R>(child, k, dp, lldp, lp, ldp);
+                    reinterpret_cast<double2 *>(childx)[k] = make_double2(hi(dp), hi(lldp));
+                    p = fma_dd(mt, D, mul(rw.lld, p));
+                    q = D;
+                    if ((j & 7) == 7) child_rescale<R>(p, q);
+                }
+                child_rescale<R>(p, q);
+            }
+            __syncwarp();
+        }
     }
+    }  // win != 0
     __syncwarp();
     if (lane == win) {
         NodeInfo ch = P;

@@ -75,9 +75,10 @@ def _run_world(name, world, exchange, params=None):
     return sorted(out, key=lambda t: t[0])
 
 
-@pytest.mark.parametrize("name,params", [("legendre3000", {"GROUPS": 1}), ("glued30", {}),
-                                         ("uniform2000", {}), ("f32", {})])
-@pytest.mark.parametrize("exchange", ["host", "torch"])
+@pytest.mark.parametrize("name,params,exchange", [("legendre3000", {"GROUPS": 1}, "host"),
+                                                  ("glued30", {}, "host"),
+                                                  ("uniform2000", {}, "torch"),
+                                                  ("f32", {}, "host")])
 def test_two_process_solve_bitwise(name, params, exchange):
     import paper_1304_1864_b200 as mr3
     p = _make(name)

@@ -8,7 +8,7 @@ O=gpurun_out
 mkdir -p $O
 if [ "$SEL" != "none" ]; then
   if [ "$SEL" = "all" ]; then
-    timeout 1500 python -m pytest tests -m gpu -q -x > $O/${TAG}_pytest.log 2>&1
+    timeout 2400 python -m pytest tests -m gpu -q -x --durations=30 > $O/${TAG}_pytest.log 2>&1
   else
     timeout 1500 python -m pytest tests -m gpu -q -x -k "$SEL" > $O/${TAG}_pytest.log 2>&1
   fi
