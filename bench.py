@@ -34,10 +34,12 @@ import synth  # noqa: E402
 #   Sturm row, binary_x projective (2 DFMA + 1 DMUL + rescale/8)      3.25
 #   Sturm row, fp64-internal mode (projective, binary64)              3.25
 #   Newton/Laguerre pass row, binary_x (value + two x-derivatives)    11
-#   RQI row (rqi_rows: 2 fixed-twist passes of n rows each; projective F row 45, B row 45,
-#   +10 on the last pass for the product-form z components and their squares)  50
+#   RQI row (rqi_rows: 2 fixed-twist passes of n rows each; projective F or B row: pair fma
+#   15 + pair dot product 19 + prefix norm 6 (+ rescale/8) = 40.5; +6 on the storing pass for
+#   the product-form z component and its compensated square; SASS of k_rqi_fb: 40.5 / 46.5)
+#   dd 43.5, fp64-internal 12.25 (9.25 / 15.25)
 FP64_INST_PER_BISECT_ROW = {"dd": 37.0, "f64": 3.25, "x": 3.25, "newton": 11.0}
-FP64_INST_PER_RQI_ROW = {"dd": 50.0, "f64": 12.0}
+FP64_INST_PER_RQI_ROW = {"dd": 43.5, "f64": 12.25}
 DERIVED_FP64_PEAK = 148 * 64 * 1.965e9  # SMs x FP64 lanes x max SM clock (inst/s)
 
 

@@ -53,6 +53,15 @@ MR3_HD double rcp(double b) {
     return fma_rn(fma_rn(e, e, e), r, r);
 }
 
+// reciprocal to ~2^-44 relative (one quadratic Newton step): for the prefix norms W, V of
+// the twisted factorizations (reading R9), which only feed ||z||^2 of the RQ correction and
+// the stopping test -- a relative error of n 2^-43 there moves the corrected shift by that
+// fraction of the correction, far below the dd accuracy the next pass needs
+MR3_HD double rcp_w(double b) {
+    const double r = rcp_seed(b);
+    return fma_rn(r, fma_rn(-b, r, 1.0), r);
+}
+
 // a / b to ~1 ulp with one residual correction (fp64-internal mode)
 MR3_HD double div(double a, double b) {
     double r = rcp(b);

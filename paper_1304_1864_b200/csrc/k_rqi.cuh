@@ -97,7 +97,12 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
     return t;
 }
 
-__device__ __forceinline__ double clampbig(double x) { return fmin(x, 1e250); }
+// caps a prefix norm W >= 0 (or NaN) near 1e250: an unsigned min on the high word orders
+// non-negative doubles (and sends every NaN to the cap) in one integer instruction
+__device__ __forceinline__ double clampbig(double x) {
+    const unsigned h = (unsigned)__double2hiint(x);
+    return __hiloint2double((int)min(h, 0x73d658e3u), __double2loint(x));
+}
 
 // sign(x) != sign(y) as 0/1 (the inertia of a projective step)
 template <class R>
@@ -563,10 +568,10 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             constexpr bool GUARD = decltype(guard)::value;
             Row4<R> rw = srow<R>(bA, tA, kk);
             const R D = fma_dd(rw.d, qF, pF);
-            const double lpx = hi(rw.ld) * hi(qF) * rcp(hi(D));  // l+ = ld / d+
+            const double lpx = hi(rw.ld) * hi(qF) * rcp_w(hi(D));  // l+ = ld / d+
             const double l2 = lpx * lpx;
             const double W2 = clampbig(fma(l2, W, l2));
-            const R p2 = fma_dd(mlam, D, mul(rw.lld, pF));
+            const R p2 = dot2_dd(mlam, D, rw.lld, pF);
             if (!GUARD || (int)kk < (int)r) {
                 if (wz) {
                     double pm, ipm;
@@ -586,10 +591,10 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             constexpr bool GUARD = decltype(guard)::value;
             Row4<R> rw = srow<R>(bD, tD, kk - 1);
             const R E = fma_dd(rw.lld, qB, pB);
-            const double ux = hi(rw.l) * hi(rw.d) * hi(qB) * rcp(hi(E));  // u- = l d / D-
+            const double ux = hi(rw.ld) * hi(qB) * rcp_w(hi(E));  // u- = l d / D-
             const double u2 = ux * ux;
             const double V2 = clampbig(fma(u2, V, u2));
-            const R P2 = fma_dd(mlam, E, mul(rw.d, pB));
+            const R P2 = dot2_dd(mlam, E, rw.d, pB);
             if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
                 if (wz) {
                     double pm, ipm;
@@ -785,8 +790,8 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                         const Row4<R> rw = load_row4<R>(nd.rep, isF ? kk : kk - 1);
                         const R m1 = isF ? rw.d : rw.lld, m2 = isF ? rw.lld : rw.d;
                         const R U = fma_dd(m1, uq, up), V = fma_dd(m1, vq, vp);
-                        up = fma_dd(mlam, U, mul(m2, up));
-                        vp = fma_dd(mlam, V, mul(m2, vp));
+                        up = dot2_dd(mlam, U, m2, up);
+                        vp = dot2_dd(mlam, V, m2, vp);
                         uq = U;
                         vq = V;
                     }
@@ -854,7 +859,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
                     const R m1 = isF ? rw.d : rw.lld, m2 = isF ? rw.lld : rw.d;
                     const R D = fma_dd(m1, q, p);
                     ng += sgn_ne_R<R>(D, q);
-                    p = fma_dd(mlam, D, mul(m2, p));
+                    p = dot2_dd(mlam, D, m2, p);
                     q = D;
                 }
             }

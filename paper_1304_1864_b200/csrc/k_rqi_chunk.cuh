@@ -52,7 +52,7 @@ __device__ __forceinline__ RowFB<R> load_fb(const double *__restrict__ rep, int6
     RowFB<R> o;
     o.m1 = isF ? rw.d : rw.lld;
     o.m2 = isF ? rw.lld : rw.d;
-    o.x = isF ? hi(rw.ld) : hi(rw.l) * hi(rw.d);
+    o.x = hi(rw.ld);  // l+ = ld qF / qF' (F), u- = ld QB / QB' (B)
     o.nrm = fabs(hi(rw.d)) + fabs(hi(rw.lld)) + 2.0 * fabs(hi(rw.ld));
     return o;
 }
@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(RC_TPB) k_rqi_chunk(RqiArgs<R> A) {
                 for (int j = 0; j < RC_U; j++)
                     if (j < jn) {
                         const R U = fma_dd(m1v[j], uq, up), V = fma_dd(m1v[j], vq, vp);
-                        up = fma_dd(mlam, U, mul(m2v[j], up));
-                        vp = fma_dd(mlam, V, mul(m2v[j], vp));
+                        up = dot2_dd(mlam, U, m2v[j], up);
+                        vp = dot2_dd(mlam, V, m2v[j], vp);
                         uq = U;
                         vq = V;
                     }
@@ -300,12 +300,12 @@ __global__ void __launch_bounds__(RC_TPB) k_rqi_chunk(RqiArgs<R> A) {
                         const R m1 = rw[j].m1, m2 = rw[j].m2;
                         const R D = fma_dd(m1, q, p);
                         // l+ = ld / d+ (F), u- = l d / D- (B), in binary64 off the chain
-                        const double lx = rw[j].x * hi(q) * rcp(hi(D));
+                        const double lx = rw[j].x * hi(q) * rcp_w(hi(D));
                         const double a2 = lx * lx;
                         Am = clampbig(a2 * Am);
                         Bm = clampbig(a2 * (Bm + 1.0));
                         ng += sgn_ne_R<R>(D, q);
-                        p = fma_dd(mlam, D, mul(m2, p));
+                        p = dot2_dd(mlam, D, m2, p);
                         q = D;
                     }
                 const unsigned ex = (unsigned)__double2hiint(hi(p)) & 0x7ff00000u;

@@ -173,22 +173,24 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             e = __double2loint(a1.x);
         };
         // F row kk (< r): y_kk = qF / PP_kk is component kk of the product-form z
-        auto frow = [&](auto guard, const double *bA, int64_t tA, int64_t kk) {
+        // (zt: this thread's slot of the z tile row kk; a storing pass computes and stages the
+        // component unconditionally -- columns not written are masked by s_rb at the flush)
+        auto frow = [&](auto guard, const double *bA, int64_t tA, int64_t kk, OutT *zt) {
             constexpr bool GUARD = decltype(guard)::value;
             const Row4<R> rw = srow<R>(bA, tA, kk);
             const R D = fma_dd(rw.d, qx, px);
-            const double lpx = hi(rw.ld) * hi(qx) * rcp(hi(D));  // l+ = ld / d+
+            const double lpx = hi(rw.ld) * hi(qx) * rcp_w(hi(D));  // l+ = ld / d+
             const double l2 = lpx * lpx;
             const double N2 = clampbig(fma(l2, nrm, l2));
             const R p2 = DOT2 ? dot2_dd(add(rw.lld, mlam), px, mul(mlam, rw.d), qx)
-                              : fma_dd(mlam, D, mul(rw.lld, px));
+                              : dot2_dd(mlam, D, rw.lld, px);
             if (!GUARD || (int)kk < (int)r) {
-                if (wz) {
+                if (STORE) {
                     double pm, ipm;
                     int e;
                     sppr(bA, tA, kk, pm, ipm, e);
                     const OutT zo = (OutT)pow2mul_d(hi(qx) * ipm, Ex - e - eref);
-                    ztF[(kk - tA) & 15][pi] = zo;
+                    *zt = zo;
                     kahan_sq((double)zo, ks, kc);
                 }
                 negc += sgn_ne_R<R>(D, qx);
@@ -198,22 +200,22 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             }
         };
         // B row kk (> r): x_kk = QB PP_kk
-        auto brow = [&](auto guard, const double *bD, int64_t tD, int64_t kk) {
+        auto brow = [&](auto guard, const double *bD, int64_t tD, int64_t kk, OutT *zt) {
             constexpr bool GUARD = decltype(guard)::value;
             const Row4<R> rw = srow<R>(bD, tD, kk - 1);
             const R E = fma_dd(rw.lld, qx, px);
-            const double ux = hi(rw.l) * hi(rw.d) * hi(qx) * rcp(hi(E));  // u- = l d / D-
+            const double ux = hi(rw.ld) * hi(qx) * rcp_w(hi(E));  // u- = l d / D-
             const double u2 = ux * ux;
             const double N2 = clampbig(fma(u2, nrm, u2));
             const R P2 = DOT2 ? dot2_dd(add(rw.d, mlam), px, mul(mlam, rw.lld), qx)
-                              : fma_dd(mlam, E, mul(rw.d, px));
+                              : dot2_dd(mlam, E, rw.d, px);
             if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
-                if (wz) {
+                if (STORE) {
                     double pm, ipm;
                     int e;
                     sppr(bD, tD, kk, pm, ipm, e);
                     const OutT zo = (OutT)pow2mul_d(hi(qx) * pm, Ex + e - eref);
-                    ztB[(kk - tD) & 15][pi] = zo;
+                    *zt = zo;
                     kahan_sq((double)zo, ks, kc);
                 }
                 negc += sgn_ne_R<R>(E, qx);
@@ -257,13 +259,16 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
 #pragma unroll 1
                                 for (int q = 2 * h; q < 2 * h + 2; q++) {
                                     const int64_t b0 = tA + q * RQ_C;
+                                    OutT *zt = &ztF[(q & 1) * RQ_C][pi];
                                     if (b0 + RQ_C <= cta_rmin) {  // below every twist: no guard
 #pragma unroll
-                                        for (int j = 0; j < RQ_C; j++) frow(G0{}, bA, tA, b0 + j);
+                                        for (int j = 0; j < RQ_C; j++)
+                                            frow(G0{}, bA, tA, b0 + j, zt + j * (FB_NP + 1));
                                         rescale(px, qx, Ex);
                                     } else if (b0 < r) {
 #pragma unroll
-                                        for (int j = 0; j < RQ_C; j++) frow(G1{}, bA, tA, b0 + j);
+                                        for (int j = 0; j < RQ_C; j++)
+                                            frow(G1{}, bA, tA, b0 + j, zt + j * (FB_NP + 1));
                                         rescale(px, qx, Ex);
                                     }
                                 }
@@ -272,15 +277,18 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
 #pragma unroll 1
                             for (int q = 2 * h; q < 2 * h + 2; q++) {
                                 const int64_t b0 = tD + (RQ_TR / RQ_C - 1 - q) * RQ_C;
+                                OutT *zt = &ztB[((RQ_TR / RQ_C - 1 - q) & 1) * RQ_C][pi];
                                 if (b0 > cta_rmax && b0 + RQ_C <= n) {  // above every twist
 #pragma unroll
                                     for (int j = 0; j < RQ_C; j++)
-                                        brow(G0{}, bD, tD, b0 + RQ_C - 1 - j);
+                                        brow(G0{}, bD, tD, b0 + RQ_C - 1 - j,
+                                             zt + (RQ_C - 1 - j) * (FB_NP + 1));
                                     rescale(px, qx, Ex);
                                 } else if (b0 + RQ_C > r && b0 < n) {
 #pragma unroll
                                     for (int j = 0; j < RQ_C; j++)
-                                        brow(G1{}, bD, tD, b0 + RQ_C - 1 - j);
+                                        brow(G1{}, bD, tD, b0 + RQ_C - 1 - j,
+                                             zt + (RQ_C - 1 - j) * (FB_NP + 1));
                                     rescale(px, qx, Ex);
                                 }
                             }
