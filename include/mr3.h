@@ -70,6 +70,8 @@ typedef struct {
     double bisect_rows_x;        /* Sturm-count rows executed in binary_x (fp64 phase) */
     double newton_rows_x;        /* of which Newton passes (count + derivative, R8e) */
     double t_ms[8];
+    int32_t backtracks;          /* clusters whose child came from the grandparent (R22) */
+    int32_t backtrack_tries;     /* clusters re-processed from the grandparent */
 } mr3_stats;
 
 /* tunable parameters (mr3_set_param / mr3_get_param); defaults per PAPER.md §4 */
@@ -112,7 +114,18 @@ enum mr3_param {
     MR3_RQI_CHUNK = 22, /* solves of at most this many wanted eigenpairs (globally) run every
                            RQI iteration chunk-parallel, one eigenpair per CTA (k_rqi_chunk;
                            it also takes the stragglers of k_rqi_fb); 0 = off; 8192 */
-    MR3_NPARAM = 23
+    MR3_RELAX = 23,    /* NEXT-1b: bisection of an eigenvalue whose own
+                          Sturm counts isolate it by gaps >= 4 gaptol |lambda| stops once its
+                          bracket is narrower than c gap sqrt(eps_x sqrt(n) / C) (C = MR3_REFINE),
+                          c = this value, instead of going to rtol (R20); 0 = off; 0.5 */
+    MR3_ABSGAP = 24,   /* absolute-gap splitting: neighbours
+                          whose bracket gap is >= this value * ||T||_1 are separated even when
+                          their relative gap is below gaptol (R21); 0 = off */
+    MR3_BACKTRACK = 25, /* 1: a child at depth >= 2 that fails the acceptance tests is redone
+                           from its grandparent and kept if it passes or grows less (PAPER.md
+                           L1190-L1197, R22); 0: off; 2: test hook (every child at
+                           depth >= 2 counts as failed first); 1 */
+    MR3_NPARAM = 26
 };
 
 /*

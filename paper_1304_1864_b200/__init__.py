@@ -34,7 +34,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 PARAMS = {"GAPTOL": 0, "XI": 1, "KRS": 2, "MAX_RQI": 3, "MAX_DEPTH": 4, "SEED": 5, "ELG_MAX": 6,
           "RTOL": 7, "GROUPS": 8, "XPHASE": 9, "REFINE": 10, "GRID": 11, "CTA": 12, "XPTS": 13, "YCERT": 14, "NEWTON": 15, "TWISTW": 16,
-          "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20, "RQI_FB": 21, "RQI_CHUNK": 22}
+          "SPLIT": 17, "FUSE_SCALE": 18, "POOL_MB": 19, "DEBUG": 20, "RQI_FB": 21, "RQI_CHUNK": 22,
+          "RELAX": 23, "ABSGAP": 24, "BACKTRACK": 25}
 ERRORS = {1: "NONFINITE", 2: "CUDA", 3: "NCCL", 4: "NOMEM", 5: "NOCONV", 6: "ZCAP", 7: "STATE"}
 
 
@@ -67,7 +68,8 @@ class Stats(ctypes.Structure):
                 ("rho", ctypes.c_double), ("bisect_rows", ctypes.c_double),
                 ("rqi_rows", ctypes.c_double), ("bisect_rows_x", ctypes.c_double),
                 ("newton_rows_x", ctypes.c_double),
-                ("t_ms", ctypes.c_double * 8)]
+                ("t_ms", ctypes.c_double * 8),
+                ("backtracks", ctypes.c_int32), ("backtrack_tries", ctypes.c_int32)]
 
     def asdict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "t_ms"}

@@ -68,7 +68,8 @@ struct SegOut {
 
 template <class R>
 __global__ void __launch_bounds__(1024) k_classify(Items it, const int32_t *__restrict__ list,
-                                                   int cnt, double gaptol, SegOut out) {
+                                                   int cnt, double gaptol, SegOut out,
+                                                   double absgap = 0.0) {
     __shared__ int sh[33];
     __shared__ int carry[4];
     if (threadIdx.x < 4) carry[threadIdx.x] = 0;
@@ -92,7 +93,10 @@ __global__ void __launch_bounds__(1024) k_classify(Items it, const int32_t *__re
                 double den = fmax(fmax(fabs(hi(l0)), fabs(hi(h0))), fmax(fabs(hi(l1)), fabs(hi(h1))));
                 it.lgap[id] = gap;
                 it.rgap[id - 1] = gap;
-                start = (den == 0.0 || gap >= gaptol * den) ? 1 : 0;
+                // relative gap (Eq. (2.2)), or -- NEXT-3, absgap > 0 -- an absolute gap of at
+                // least absgap ("amended by a criterion based on the
+                // absolute separation"; R21)
+                start = (den == 0.0 || gap >= gaptol * den || (absgap > 0.0 && gap >= absgap)) ? 1 : 0;
             }
         }
         int tot;

@@ -558,12 +558,36 @@ __device__ __forceinline__ void count_y_cta(double *smem, const NodeInfo &nd, bo
     cb = B.c;
 }
 
+// NEXT-1b ("the above criterion can be relaxed for eigenvalues with a
+// large gap to the rest of the spectrum"): isolation of lambda_k read off the item's OWN
+// Sturm counts, so it depends on nothing but the item's path (world- and CTA-independent).
+// A point x with count(x) = k - 1 lies in (lambda_{k-1}, lambda_k], one with count(x) = k in
+// (lambda_k, lambda_{k+1}]; with alo the smallest point seen of the first kind and bhi the
+// largest of the second, the gaps of lambda_k are at least a - alo and bhi - b.  Once they are
+// both >= sep * max(|a|, |b|) (so the item will classify as a singleton with room to spare)
+// and the bracket is narrower than relax * gap, the bracket stops: its midpoint is a start
+// from which the RQI needs the same two passes (R20), whatever rtol asks for.
+struct Iso {
+    double alo = INFINITY, bhi = -INFINITY;  // isolation points seen so far
+    double relax = 0.0;                      // 0: off (rtol alone decides)
+    double sep = 0.0;                        // required gap / magnitude (4 gaptol)
+    double slack = 0.0;                      // width allowed on top (the x -> y widening)
+    int kmax = 0;                            // eigenvalues of the node (k = kmax: no right one)
+};
+__device__ __forceinline__ bool iso_stop(const Iso &I, int k, double a, double b) {
+    if (!(I.relax > 0.0)) return false;
+    const double gl = k <= 1 ? INFINITY : a - I.alo;
+    const double gr = k >= I.kmax ? INFINITY : I.bhi - b;
+    const double g = fmin(gl, gr);
+    return g >= I.sep * fmax(fabs(a), fabs(b)) && b - a <= I.relax * g + I.slack;
+}
+
 // CTA-synchronous multisection rounds of the groups (see multisect in k_bisect.cuh)
 template <class T, int G, class Count>
 __device__ __forceinline__ void msect_cta(T &a, T &b, bool active, int k, int lig, int lane,
                                           unsigned gmask, double rtol, double absfloor,
                                           double tolmul, unsigned long long &rows, int64_t n,
-                                          Count count) {
+                                          Count count, Iso *iso = nullptr) {
     bool mdone = !active;
 #pragma unroll 1
     for (int round = 0; round < 4000; round++) {
@@ -572,7 +596,7 @@ __device__ __forceinline__ void msect_cta(T &a, T &b, bool active, int k, int li
         if (!mdone) {
             T w = sub(b, a);
             double tol = tolmul * fmax(2.0 * rtol * fmax(fabs(hi(a)), fabs(hi(b))), absfloor);
-            if (hi(w) <= tol) {
+            if (hi(w) <= tol || (iso != nullptr && iso_stop(*iso, k, hi(a), hi(b)))) {
                 mdone = true;
             } else {
                 x = add(a, mul(w, (double)(lig + 1) / (double)(G + 1)));
@@ -588,9 +612,19 @@ __device__ __forceinline__ void msect_cta(T &a, T &b, bool active, int k, int li
             else
                 c = above ? k : k - 1;  // x == b counts as right of lambda_k, x == a as left
             bool P = c >= k;
+            const unsigned sh = lane & ~(G - 1) & 31;
+            const unsigned gm = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
             unsigned bal = __ballot_sync(gmask, P);
-            bal = (bal >> (lane & ~(G - 1) & 31)) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
+            bal = (bal >> sh) & gm;
             int first = bal ? __ffs(bal) : G + 1;
+            if (iso != nullptr) {  // isolation points among the evaluated ones (group-uniform)
+                const unsigned e1 = (__ballot_sync(gmask, need && c == k - 1) >> sh) & gm;
+                const unsigned e2 = (__ballot_sync(gmask, need && c == k) >> sh) & gm;
+                const double x1 = __shfl_sync(gmask, hi(x), e1 ? __ffs(e1) - 1 : 0, G);
+                const double x2 = __shfl_sync(gmask, hi(x), e2 ? 31 - __clz(e2) : 0, G);
+                if (e1) iso->alo = fmin(iso->alo, x1);
+                if (e2) iso->bhi = fmax(iso->bhi, x2);
+            }
             T xb = shfl_R<T>(gmask, x, first <= G ? first - 1 : 0, G);
             T xa = shfl_R<T>(gmask, x, first >= 2 ? first - 2 : 0, G);
             T nb = first <= G ? xb : b;
@@ -677,7 +711,8 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
                                                   double absfloor, double pivmin, double pivmin_x,
                                                   double eps_x, int certify, int xpts,
                                                   int ycert, char *tailflag, int xpts_maxpass,
-                                                  double widen, DevStats *st) {
+                                                  double widen, double relax_f, double sep,
+                                                  int iso_init, DevStats *st) {
     __shared__ __align__(16) double sbuf[2 * BS_TILE];
     if ((int)blockIdx.x >= *ntasks) return;  // grid is an upper bound (whole CTA leaves)
     const RqiTask task = tasks[blockIdx.x];
@@ -696,6 +731,22 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
         b = reinterpret_cast<R *>(it.hi)[id];
     }
     unsigned long long rows = 0, rows_x = 0;
+    // NEXT-1b: relaxed stop for isolated eigenvalues (relax_f = 0: off); relax = relax_f n^(1/4)
+    // makes the stop width relax * gap = c gap sqrt(eps_x sqrt(n) / C) (host: mr3.cu)
+    Iso iso;
+    iso.relax = relax_f > 0.0 ? relax_f * sqrt(sqrt((double)n)) : 0.0;
+    iso.sep = sep;
+    iso.kmax = (int)n;
+    if (iso_init && active) {  // isolation points from the grid cells (k_cell_final)
+        const double l0 = it.lgap[id], r0 = it.rgap[id];
+        if (!isnan(l0)) iso.alo = l0;
+        if (!isnan(r0)) iso.bhi = r0;
+        __syncwarp(gmask);
+        if (lig == 0) {  // (restored: the gaps are classification's from here on)
+            it.lgap[id] = 1e300;
+            it.rgap[id] = 1e300;
+        }
+    }
 
     // binary_y certification: count_y(a) < k <= count_y(b); failing ends are widened
     // (by delta, then 8x per try) until certified (k_bisect.cuh certify_bracket)
@@ -778,7 +829,7 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
             msect_cta<double, G>(ax, bx, active, k, lig, lane, gmask, rtol, absfloor, 0.5, rows_x,
                                  n, [&](bool need, double x) {
                                      return count_x_cta(sbuf, nd, need, x, pivmin_x);
-                                 });
+                                 }, &iso);
         if (!(G == 1 && xpts == 3) && !ycert && !certify && active && lig == 0) {
             // multisection result: its midpoint is the RQI start, |error| <= half-width
             // (dx < 0 marks a direct bound, dx >= 0 a Newton step; k_refine_flags)
@@ -809,13 +860,19 @@ __global__ void __launch_bounds__(BS_TPB) k_bisect_s(const NodeInfo *__restrict_
             return;
         }
         certify_y(delta);
+        // the binary_x isolation points, moved toward lambda_k by the M_x -> M_y shift; a
+        // bracket the x phase stopped by isolation stays stopped after the widening by delta
+        // (certify_y may widen further: then the y phase bisects back)
+        iso.alo += delta;
+        iso.bhi -= delta;
+        iso.slack = 4.0 * delta;
     }
     msect_cta<R, G>(a, b, active, k, lig, lane, gmask, rtol, absfloor, 1.0, rows, n,
                     [&](bool need, R x) {
                         int c, dummy;
                         count_y_cta<R, false>(sbuf, nd, need, x, x, pivmin, c, dummy);
                         return c;
-                    });
+                    }, &iso);
     if (active && lig == 0) {
         reinterpret_cast<R *>(it.lo)[id] = a;
         reinterpret_cast<R *>(it.hi)[id] = b;

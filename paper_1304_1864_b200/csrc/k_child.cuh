@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
                                               double *child_pool, double *childx_pool,
                                               int64_t pool_stride_rows,
                                               double spdiam, double elg1, double elg2,
-                                              double pivmin, DevStats *st, double *dbg) {
+                                              double pivmin, DevStats *st, double *dbg,
+                                              double *cfail, int mode, int force_depth) {
     constexpr int ROWD = 4 * Prec<R>::words;
     __shared__ __align__(16) double sbuf[2][CH_TR * ROWD];
     __shared__ R sS[2 * 33];  // chunk start states (p, q)
@@ -112,12 +113,26 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     const int lane = threadIdx.x;
     const int b = cbeg[c], e = cend[c];
     const int id0 = next_active[b], id1 = next_active[e - 1];
-    const int pnode = it.node[id0];
+    // mode 0: the child of the cluster's node.  mode 1 (backtracking, PAPER.md L1190-L1197,
+    // reading R22): a cluster whose child failed the acceptance tests in mode 0 (cfail[c] >= 0:
+    // the failed child's growth) takes its child from the grandparent instead -- a different
+    // shift at a higher level of the tree -- and keeps it if it passes or grows less.
+    int pnode = it.node[id0];
+    R shift_in = mk<R>(0.0);  // member brackets: + shift_in = base-node coordinates
+    if (mode == 1) {
+        // cfail: -1 none (or no grandparent), -2 forced by the test hook, else the growth
+        if (!(cfail[c] >= 0.0 || cfail[c] == -2.0)) return;  // (uniform)
+        const NodeInfo C = nodes[pnode];
+        pnode = nodes[C.parent].parent;
+        const NodeInfo Gn = nodes[pnode];
+        shift_in = sub(mk2<R>(C.sig_hi, C.sig_lo), mk2<R>(Gn.sig_hi, Gn.sig_lo));
+        if (lane == 0) atomicAdd(&st->backtrack_tries, 1);
+    }
     const NodeInfo P = nodes[pnode];
     const int64_t n = P.n;
     const R *lo = reinterpret_cast<const R *>(it.lo);
     const R *hi_ = reinterpret_cast<const R *>(it.hi);
-    R lamL = lo[id0], lamR = hi_[id1];
+    R lamL = add(lo[id0], shift_in), lamR = add(hi_[id1], shift_in);
     double wL = hi(sub(hi_[id0], lo[id0])), wR = hi(sub(hi_[id1], lo[id1]));
     double gL = it.lgap[id0], gR = it.rgap[id1];
     const int side = lane & 1, lev = lane >> 1;
@@ -158,7 +173,7 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
                 const double dp = fabs(hi(D) * rcp(hi(q)));  // |d+| (growth only)
                 bad |= !(dp <= 1e300);
                 growth = fmax(growth, dp);
-                if (lane == 0) {
+                if (lane == 0 && mode == 0) {
                     const int64_t k = (int64_t)t * CH_TR + j;
                     const R dpr = div(D, q);  // d+_k
                     R lp = mk<R>(0.0);
@@ -199,9 +214,14 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
         win = l;
         fail = true;
     }
+    const double gwin = __shfl_sync(0xffffffffu, growth, win);
+    const bool was_forced = mode == 1 && cfail[c] == -2.0;
+    if (mode == 1 && !was_forced && fail && !(gwin < cfail[c])) return;  // (uniform) keep mode 0's
+    // test hook (MR3_BACKTRACK = 2): children at depth >= force_depth count as failed in mode 0
+    const bool forced = mode == 0 && force_depth > 0 && P.depth + 1 >= force_depth;
     const R t = shfl_R<R>(0xffffffffu, tau, win, 32);
     const R mt = neg(t);
-    if (win != 0) {  // (uniform) the speculative child is not the chosen one: write it
+    if (win != 0 || mode == 1) {  // (uniform) the speculative child is not the chosen one: write it
 
     // ---- write pass, chunk-parallel (see above)
     const int64_t L = (n + 31) / 32;
@@ -335,8 +355,17 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
         ch.sig_hi = hi(sig);
         ch.sig_lo = lo_part(sig);
         ch.depth = P.depth + 1;
+        ch.parent = pnode;
+        if (mode == 1) {
+            ch.depth = nodes[node_base + c].depth;  // (the failed child's level)
+            atomicAdd(&st->backtracks, 1);
+            if (!fail && !was_forced) atomicSub(&st->robustness_failures, 1);  // (mode 0's)
+            if (fail && was_forced) atomicAdd(&st->robustness_failures, 1);
+        }
         nodes[node_base + c] = ch;
-        if (fail) atomicAdd(&st->robustness_failures, 1);
+        if (fail && mode == 0) atomicAdd(&st->robustness_failures, 1);
+        if (cfail != nullptr && mode == 0)
+            cfail[c] = P.depth < 1 ? -1.0 : fail ? gwin : forced ? -2.0 : -1.0;
         if (dbg) {
             dbg[4 * c + 0] = win;
             dbg[4 * c + 1] = growth;
@@ -348,10 +377,11 @@ __global__ void __launch_bounds__(32) k_child(NodeInfo *nodes, int node_base, It
     // translate the member brackets into the child's coordinates (Alg. 1 l.16)
     R *wlo = reinterpret_cast<R *>(it.lo);
     R *whi = reinterpret_cast<R *>(it.hi);
+    const R tt = sub(t, shift_in);
     for (int j = b + lane; j < e; j += 32) {
         int id = next_active[j];
-        wlo[id] = sub(wlo[id], t);
-        whi[id] = sub(whi[id], t);
+        wlo[id] = sub(wlo[id], tt);
+        whi[id] = sub(whi[id], tt);
         it.node[id] = node_base + c;
     }
 }

@@ -212,13 +212,19 @@ __global__ void k_cell_assign(CellSet cs, int mine, const int32_t *__restrict__ 
     cs.chi2[t] = nchi;
 }
 
-// final cells -> item brackets
+// final cells -> item brackets; a cell end whose count shows it isolates lambda_k (count k - 1
+// on the left, k on the right) is handed to the bisection as an isolation point of NEXT-1b
+// (k_bisect_s Iso; carried in lgap / rgap, which classification overwrites later)
 template <class R>
-__global__ void k_cell_final(Items it, int first, int mine, CellSet cs) {
+__global__ void k_cell_final(Items it, int first, int mine, CellSet cs,
+                             const int32_t *__restrict__ kk) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= mine) return;
     reinterpret_cast<R *>(it.lo)[first + t] = mk<R>(cs.lo[t]);
     reinterpret_cast<R *>(it.hi)[first + t] = mk<R>(cs.hi[t]);
+    const int k = kk[t];
+    it.lgap[first + t] = cs.clo[t] == k - 1 ? cs.lo[t] : NAN;
+    it.rgap[first + t] = cs.chi[t] == k ? cs.hi[t] : NAN;
 }
 
 }  // namespace mr3

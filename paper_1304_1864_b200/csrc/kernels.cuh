@@ -22,6 +22,8 @@ struct NodeInfo {
     double sig_hi, sig_lo;  // accumulated shift sigma (scaled units), Alg.1 l.19/29
     int32_t depth;
     int32_t block;
+    int32_t parent;     // node this one was shifted from (-1: a root), for backtracking (R22)
+    int32_t pad_;
     const double *pp;   // per row {PP, 1/PP, exponent} of prod_{j<k} (-ld_j) (k_zprod.cuh)
 };
 
@@ -58,6 +60,8 @@ struct DevStats {
     int n_clusters;
     int pad;
     unsigned long long refine_rows_x;  // binary_x rows of the RQI start refinement (K2')
+    int backtracks;       // clusters whose child was taken from the grandparent (R22)
+    int backtrack_tries;  // clusters re-processed from the grandparent
 };
 
 template <class R>
@@ -631,6 +635,8 @@ __global__ void k_root_nodes(const BlockDesc *blocks, int nblocks, const double 
     ni.sig_lo = 0.0;
     ni.depth = 0;
     ni.block = b;
+    ni.parent = -1;
+    ni.pad_ = 0;
     ni.pp = nullptr;
     nodes[b] = ni;
 }

@@ -170,9 +170,9 @@ static void hsync_note(mr3_ctx ctx, const char *where) {
 }
 
 static const double kDefaults[2][MR3_NPARAM] = {
-    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG FB CHUNK
-    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0},
-    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0},
+    // GAPTOL XI                     KRS MAXRQI MAXDEPTH SEED      ELG RTOL GROUPS XPHASE REFINE GRID CTA XPTS YCERT NEWTON TWISTW SPLIT FUSE POOL DEBUG FB CHUNK RELAX ABSGAP BT
+    {1e-10, 1.1102230246251565e-16, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 1.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0, 0.5, 0.0, 1.0},
+    {1e-5, 5.9604644775390625e-08, 1.0, 10, 10, 5067315.0, 8.0, -1.0, 0.0, 0.0, 4.0, 1.0, 0.0, 3.0, 0.0, 6.0, 100.0, 1.0, 1.0, 0.0, 0.0, 1.0, 8192.0, 0.5, 0.0, 1.0},
 };
 
 #define CK(call)                                                                  \
@@ -315,9 +315,18 @@ template <class R>
 static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, int G, double rtol,
                          double absfloor, int certify, bool xphase, double eps_x,
                          const char *tname = "k_bisect", int ycert = 1, char *tailflag = nullptr,
-                         double widen = 0.0) {
+                         double widen = 0.0, bool relax_ok = true, int iso_init = 0) {
     if (cnt <= 0) return 0;
     int rc = 0;
+    // NEXT-1b (R20): relaxed stop of isolated eigenvalues at width c gap sqrt(eps_x sqrt(n) / C)
+    // (the kernel multiplies by n^(1/4)); not for the RQI-start refinement and the Newton tail,
+    // whose targets are a few ulps
+    const double *Pm = ctx->cfg[ctx->mode].v;
+    const double eps_xm = ctx->mode ? 5.9604644775390625e-08 : 1.1102230246251565e-16;
+    const double Cref = Pm[MR3_REFINE] > 0 ? Pm[MR3_REFINE] : 4.0;
+    const double relax_f =
+        (relax_ok && certify != 2 && Pm[MR3_RELAX] > 0) ? Pm[MR3_RELAX] * std::sqrt(eps_xm / Cref) : 0.0;
+    const double sep = 4.0 * Pm[MR3_GAPTOL];
     const int tpb = choose_tpb(ctx, (int64_t)cnt * G, BS_TPB);
     int xpts = (int)ctx->cfg[ctx->mode].v[MR3_XPTS];
     if (xpts == 3 && (G != 1 || !xphase || certify || ycert)) xpts = 1;  // Newton: G = 1 root x-phase only
@@ -342,11 +351,11 @@ static int launch_bisect(mr3_ctx ctx, Work<R> &W, const int32_t *list, int cnt, 
         if (xphase)                                                                           \
             k_bisect_s<R, GG, true><<<grid, tpb, 0, ctx->stream>>>(                           \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, tailflag, maxpass, widen, W.st);                               \
+                certify, xpts, ycert, tailflag, maxpass, widen, relax_f, sep, iso_init, W.st);    \
         else                                                                                  \
             k_bisect_s<R, GG, false><<<grid, tpb, 0, ctx->stream>>>(                          \
                 W.nodes, W.it, list, dtasks, dnt, rtol, absfloor, ctx->pivmin, pivmin_x, eps_x, \
-                certify, xpts, ycert, tailflag, maxpass, widen, W.st);                               \
+                certify, xpts, ycert, tailflag, maxpass, widen, relax_f, sep, iso_init, W.st);    \
         break;
     switch (G) {
         BIS(1)
@@ -667,6 +676,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
         const bool xkern = xphase || (words == 1 && newton_ok && ctx->G0 == 1);
         const double eps_xw = xphase ? eps_x : 0.0;   // M_x -> M_y widening of the x phase
         const double eps_xt = words == 2 ? eps_x : 1.1102230246251565e-16;  // tail: 2 ulps
+        int grid_iso = 0;  // the grid left isolation points in lgap / rgap (NEXT-1b)
         if (!ctx->split && P[MR3_GRID] != 0 && cnt >= 512) {
             // shared top of the bisection tree: a uniform grid of counts, then cells with
             // two or more eigenvalues subdivided level by level (k_grid.cuh)
@@ -741,7 +751,8 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                 std::swap(cs.clo, cs.clo2);
                 std::swap(cs.chi, cs.chi2);
             }
-            k_cell_final<R><<<ib, 256, 0, s>>>(W.it, (int)first, (int)mine, cs);
+            k_cell_final<R><<<ib, 256, 0, s>>>(W.it, (int)first, (int)mine, cs, kslice);
+            grid_iso = 1;
             CKL("k_cell_final");
             kt_end(ctx, tg);
         }
@@ -756,7 +767,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
             if (rc) return rc;
         }
         rc = launch_bisect<R>(ctx, W, list, (int)mine, ctx->G0, rtol, absfloor, 0, xkern, eps_xw,
-                              "k_bisect", ycert, tail);
+                              "k_bisect", ycert, tail, 0.0, true, grid_iso);
         if (rc) return rc;
         if (newton) {
             // items whose Newton phase did not finish in NEWTON_MAXPASS passes: multisection
@@ -815,7 +826,7 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
                 // items this rank's slice sent to the tail)
                 const int G = 32;
                 rc = launch_bisect<R>(ctx, W, tl, ht, G, std::min(rtol, 2.0 * eps_xt), absfloor,
-                                      0, true, eps_xw, "k_bisect", 0, nullptr);
+                                      0, true, eps_xw, "k_bisect", 0, nullptr, 0.0, false);
             }
         }
         if (rc) return rc;
@@ -954,7 +965,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     so.counts = dcounts;
     so.st = W.st;
     KTime *tc = kt_begin(ctx, "k_classify");
-    k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, cnt, gaptol, so);
+    k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, cnt, gaptol, so,
+                                                   P[MR3_ABSGAP] * ctx->norm1 * ctx->scale);
     kt_end(ctx, tc);
     CKL("k_classify");
     int hc[4];
@@ -1608,11 +1620,26 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         double *cdbg = nullptr;
         if (ctx->dump) cdbg = (double *)getbuf(ctx, "child_dbg", (size_t)nc * 32, &rc);
         KTime *tch = kt_begin(ctx, "k_child");
+        // backtracking (R22): children at depth >= 2 that fail the acceptance tests are redone
+        // from their grandparent (MR3_BACKTRACK = 2: a test hook that fails every child at
+        // depth >= 2 in the first launch)
+        const int bt = (int)P[MR3_BACKTRACK];
+        double *cfail = nullptr;
+        if (bt && F.level >= 1) {
+            cfail = (double *)getbuf(ctx, "child_fail", (size_t)nc * 8, &rc);
+            if (rc) return rc;
+        }
         k_child<R><<<nc, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, listB, cbeg, cend, nc, pool,
                                      poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin, W.st,
-                                     cdbg);
-        kt_end(ctx, tch);
+                                     cdbg, cfail, 0, bt == 2 ? 2 : 0);
         CKL("k_child");
+        if (cfail) {
+            k_child<R><<<nc, 32, 0, s>>>(W.nodes, ctx->nodes_used, W.it, listB, cbeg, cend, nc,
+                                         pool, poolx, ctx->n, ctx->spdiam, elg1, elg2, ctx->pivmin,
+                                         W.st, cdbg, cfail, 1, 0);
+            CKL("k_child (backtrack)");
+        }
+        kt_end(ctx, tch);
         if (ctx->dump) {
             std::vector<double> hd(4 * nc);
             cudaStreamSynchronize(s);
@@ -1634,7 +1661,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         CK(cudaMemcpyAsync(listA, listB, nm * 4, cudaMemcpyDeviceToDevice, s));
         so.next_active = listB;
         KTime *tc2 = kt_begin(ctx, "k_classify");
-        k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, nm, gaptol, so);
+        k_classify<R><<<1, 1024, 0, s>>>(W.it, listA, nm, gaptol, so,
+                                                   P[MR3_ABSGAP] * ctx->norm1 * ctx->scale);
         kt_end(ctx, tc2);
         CKL("k_classify");
         CK(cudaMemcpyAsync(hc, dcounts, 16, cudaMemcpyDeviceToHost, s));
@@ -1712,6 +1740,8 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
     ctx->stats.largest_cluster = std::max(1, hst.largest_cluster);
     ctx->stats.rho = (double)ctx->stats.largest_cluster / (double)ctx->n;
     ctx->stats.robustness_failures = hst.robustness_failures;
+    ctx->stats.backtracks = hst.backtracks;
+    ctx->stats.backtrack_tries = hst.backtrack_tries;
     ctx->stats.rqi_fallbacks = hst.rqi_fallbacks;
     ctx->stats.rqi_iters_max = hst.rqi_iters_max;
     ctx->stats.bisect_rows = (double)hst.bisect_rows;

@@ -420,14 +420,14 @@ def test_root_certification_modes_agree(make):
     assert dz.max() <= 1e-13, dz.max()
 
 
-def _with_params(params, fn):
+def _with_params(params, fn, mode=0):
     try:
         for k, v in params.items():
-            mr3.set_param(k, v)
+            mr3.set_param(k, v, mode)
         return fn()
     finally:
         for k in params:
-            mr3.set_param(k, -1)
+            mr3.set_param(k, -1, mode)
 
 
 def test_default_needs_no_rqi_fallback():
@@ -453,6 +453,8 @@ def test_default_needs_no_rqi_fallback():
     {"XPTS": 2},               # two points per lane
     {"GRID": 0},               # no shared grid start
     {"REFINE": 0},             # midpoints as RQI starts
+    {"RELAX": 0},              # every bracket to rtol (no NEXT-1b relaxed stop)
+    {"ABSGAP": 1e-12},         # absolute-gap splitting (NEXT-3)
 ])
 def test_rare_paths_parity(params):
     """The paths the default workload rarely takes, forced by parameters, against the oracle."""
@@ -555,3 +557,64 @@ def test_rqi_chunk_parity(make, params):
     tolw = (4e-16 if io == "f64" else 4 * 2.0 ** -24) * nrm * 2
     assert np.max(np.abs(w1.astype(np.float64) - w0)) <= tolw
 
+
+
+@pytest.mark.parametrize("make", [lambda: synth.random_uniform(1200, 2), lambda: synth.one_two_one(900),
+                                  lambda: synth.glued_wilkinson(10, 21),
+                                  lambda: synth.random_normal_f32(3000, 1, 1, 400)])
+def test_relaxed_isolation_stop(make):
+    """NEXT-1b (R20): bisection of eigenvalues that their own
+    Sturm counts isolate stops at c gap sqrt(eps_x sqrt(n) / C) instead of rtol.  Fewer Sturm
+    rows, the same classification, parity with the oracle, and RQI from the wider brackets
+    without the bisection fallback."""
+    p = make()
+    w1, Z1, s1 = run(p)                                      # default: RELAX = 0.5
+    w0, Z0, s0 = _with_params({"RELAX": 0}, lambda: run(p),  # every bracket to rtol
+                              mode=1 if p.io == "f32" else 0)
+    ks = np.arange(p.il, p.iu + 1) if p.range == "I" else np.arange(1, p.n + 1)
+    for w, Z in ((w1, Z1), (w0, Z0)):
+        assert_parity(check_solution(p, w, Z, ks, io=p.io), io=p.io)
+    rows1 = s1["bisect_rows"] + s1["bisect_rows_x"]
+    rows0 = s0["bisect_rows"] + s0["bisect_rows_x"]
+    assert rows1 < rows0, (rows1, rows0)
+    assert s1["n_clusters"] == s0["n_clusters"] and s1["d_max"] == s0["d_max"]
+    assert s1["rqi_fallbacks"] == 0
+
+
+def test_absolute_gap_splitting():
+    """NEXT-3 (R21): glued Wilkinson's top W21 pairs
+    are split by the glue by ~5.6e-11 (relative gap ~4e-12 < gaptol = 1e-10, so they form
+    clusters); with MR3_ABSGAP = 1e-12 the absolute gap >= 1e-12 ||T||_1 separates them at
+    the root.  Fewer clusters, the same parity with the oracle."""
+    p = synth.glued_wilkinson(2, 21)
+    w0, Z0, s0 = run(p)
+    w1, Z1, s1 = _with_params({"ABSGAP": 1e-12}, lambda: run(p))
+    ks = np.arange(1, p.n + 1)
+    assert_parity(check_solution(p, w0, Z0, ks))
+    assert_parity(check_solution(p, w1, Z1, ks))
+    assert s1["n_clusters"] < s0["n_clusters"], (s1["n_clusters"], s0["n_clusters"])
+
+
+@pytest.mark.slow
+def test_backtracking_from_grandparent():
+    """NEXT-3 backtracking (R22): a child at depth >= 2 that
+    fails the acceptance tests is redone from its grandparent.  The test hook MR3_BACKTRACK = 2
+    fails every depth->=2 child first, so each such cluster of config 3 (glued Wilkinson, the
+    one matrix here with a depth-2 tree) takes the backtracking path; the solve keeps the
+    config-3 parity bar.  By default no child fails, so nothing backtracks."""
+    p = synth.config(3)
+    _, _, s0 = run(p)
+    assert s0["d_max"] >= 2 and s0["backtrack_tries"] == 0 and s0["robustness_failures"] == 0
+    w, Z, st = _with_params({"BACKTRACK": 2}, lambda: run(p))
+    assert st["backtrack_tries"] > 0 and st["backtracks"] == st["backtrack_tries"], st
+    assert st["robustness_failures"] == 0, st
+    o, dd = exact_orthogonality(torch.from_numpy(Z).cuda())
+    assert o <= 1e-14 and dd <= 1e-14, (o, dd)
+    r1, r2, _ = oracle.residuals(p.d, p.e, w, Z)
+    assert r2.max() <= 1e-15
+    lh, ll = oracle.eigvals(p.d, p.e)
+    assert np.max(np.abs(w - (lh + ll))) <= 4e-16 * oracle.norm1(p.d, p.e)
+    for lo_i, hi_i in ((1, 200), (4001, 4200)):
+        idx = np.arange(lo_i, hi_i + 1)
+        res = check_solution(p, w[idx - 1], Z[:, idx - 1], idx, full_orth=False)
+        assert_parity(res)
