@@ -143,3 +143,43 @@ CONFIGS = {
 
 def config(k: int) -> Problem:
     return CONFIGS[k]()
+
+
+@dataclass
+class DenseProblem:
+    """Dense symmetric input A = Q T Q^T of the paper's dense experiments (PAPER.md L1529-L1531:
+    "applying random orthogonal similarity transformations to the tridiagonal matrices of the
+    previous experiments"); t is the tridiagonal source, kept for reference only."""
+    name: str
+    A: np.ndarray          # n x n float64, exactly symmetric, column-major (Fortran order)
+    t: Problem
+
+    @property
+    def n(self) -> int:
+        return int(self.A.shape[0])
+
+
+def random_orthogonal(n: int, seed: int) -> np.ndarray:
+    """Haar-random orthogonal matrix: Q of the QR factorization of a Gaussian matrix with the
+    signs of diag(R) folded in (input generation only)."""
+    rng = np.random.default_rng(7000 + seed)
+    G = rng.standard_normal((n, n))
+    Q, R = np.linalg.qr(G)
+    return Q * np.sign(np.diag(R))[None, :]
+
+
+def dense_from(t: Problem, seed: int = 0) -> DenseProblem:
+    """A = Q T Q^T, symmetrised exactly ((A + A^T) / 2), float64, column-major."""
+    n = t.n
+    Q = random_orthogonal(n, seed)
+    T = np.diag(t.d.astype(np.float64))
+    if n > 1:
+        T += np.diag(t.e.astype(np.float64), 1) + np.diag(t.e.astype(np.float64), -1)
+    A = Q @ T @ Q.T
+    A = 0.5 * (A + A.T)
+    return DenseProblem(f"dense-{t.name}", np.asfortranarray(A), t)
+
+
+def dense_config(n: int = 4096, seed: int = 0) -> DenseProblem:
+    """NEXT-4 bench workload: A = Q T Q^T with T the config-2 recipe (random uniform) of size n."""
+    return dense_from(random_uniform(n, seed), seed)
