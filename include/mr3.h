@@ -195,6 +195,27 @@ int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, 
                  mr3_stats *stats);
 
 /*
+ * Dense symmetric eigenproblem, fp64 I/O (Fig. 3):
+ * reduction A = Q T Q^T by Householder reflectors (LAPACK dsytrd's lower storage), the
+ * tridiagonal eigenpairs of T by mr3_dstemr_dd (double-double internal), Z <- Q Z.
+ *   A: device, column-major n x n, lda >= n; both triangles must hold the symmetric matrix
+ *      (only the reduction's updates are read); OVERWRITTEN: on return the diagonal and
+ *      subdiagonal hold T's d and e, the reflectors v_j (v_j(j+1) = 1 implicit) lie below the
+ *      subdiagonal, the strict upper triangle holds reduction intermediates.
+ *   jobz, range, vl, vu, il, iu, *m, w: as mr3_dstemr_dd.
+ *   Z: device, column-major, ldz >= n, >= *m columns (may be NULL when jobz = 'N'): the
+ *      eigenvectors of A.
+ *   stats: as mr3_dstemr_dd's, plus t_ms[6] = reduction ms, t_ms[7] = back-transformation ms.
+ * Single-rank contexts only (world = 1, else MR3_ERR_STATE).  The back-transformation's GEMMs
+ * are cuBLAS (libcublas.so.12, loaded on first use; missing -> MR3_ERR_CUDA).
+ * Errors: -1 ctx NULL, -2 jobz, -3 range, -4 n, -5 A NULL, -6 lda, -11 m NULL, -12 w NULL,
+ * -13 Z NULL or ldz < n, the errors of mr3_dstemr_dd, MR3_ERR_CUDA, MR3_ERR_NOMEM.
+ */
+int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int64_t lda,
+                  double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
+                  int64_t ldz, mr3_stats *stats);
+
+/*
  * End-to-end forms with HOST buffers (same contract as mr3_dstemr_dd /
  * mr3_sstemr_d otherwise): d[n], e[n-1] are read from host memory, w[n] and Z
  * (column-major, ldz >= n, >= *m columns; may be NULL when jobz = 'N') are

@@ -14,6 +14,8 @@ Public API (names follow the C-ABI):
     solve_distributed(d, e, group=...)   index-set partition over ranks: one library call per
                                          rank, all-gathers inside it (in-library NCCL
                                          communicator, or an exchange callback over gloo)
+    mr3_dsyevr_dd(A, ...) / dsyevr       dense symmetric fp64: reduction, tridiagonal solve,
+                                         back-transformation (NEXT-4)
     fp64_peak()                          K7 same-run FP64 peak + dd-step latency
     set_param(name, value, mode)         GAPTOL, XI, KRS, MAX_RQI, MAX_DEPTH, SEED, ELG_MAX, RTOL, GROUPS
 """
@@ -110,6 +112,8 @@ def lib():
             L.mr3_sstemr_d.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, vp,
                                        ctypes.c_float, ctypes.c_float, i64, i64, pi64, vp, vp,
                                        i64, i64, pi64, pi64, ctypes.POINTER(Stats)]
+            L.mr3_dsyevr_dd.argtypes = [vp, ctypes.c_char, ctypes.c_char, i64, vp, i64, dbl, dbl,
+                                        i64, i64, pi64, vp, vp, i64, ctypes.POINTER(Stats)]
             L.mr3_dstemr_dd_host.argtypes = L.mr3_dstemr_dd.argtypes
             L.mr3_sstemr_d_host.argtypes = L.mr3_sstemr_d.argtypes
             L.mr3_plan.argtypes = [vp, i32, ctypes.c_char, i64, vp, vp, dbl, dbl, i64, i64, i32,
@@ -251,6 +255,41 @@ def mr3_sstemr_d(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0):
 
 dstemr = mr3_dstemr_dd
 sstemr = mr3_sstemr_d
+
+
+def mr3_dsyevr_dd(A, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, overwrite=False):
+    """Dense symmetric fp64 eigenproblem (NEXT-4): reduction to tridiagonal form, the
+    double-double tridiagonal solver, back-transformation -- all on the device.
+    A: CUDA float64 (n, n) symmetric tensor (its row-major storage is the column-major storage
+    of A^T = A).  overwrite=False works on a copy (the C-ABI overwrites A with the reduction).
+    Returns (w[m], Z[n, m] or None, stats dict with t_ms['reduce'], t_ms['backtransform'])."""
+    import torch
+    if A.dtype != torch.float64 or not A.is_cuda or A.dim() != 2 or A.shape[0] != A.shape[1]:
+        raise TypeError("mr3: A must be a square CUDA float64 tensor")
+    n = A.shape[0]
+    Aw = A if (overwrite and A.is_contiguous()) else A.contiguous().clone()
+    c = _ctx(A.device.index)
+    w = torch.empty(max(n, 1), dtype=torch.float64, device=A.device)
+    Zs = None
+    if jobz == "V":
+        mcap = n if range != "I" else max(0, min(iu, n) - max(il, 1) + 1)
+        Zs = torch.empty((max(mcap, 1), max(n, 1)), dtype=torch.float64, device=A.device)
+    m = ctypes.c_int64(0)
+    st = Stats()
+    rc = lib().mr3_dsyevr_dd(c, jobz.encode(), range.encode(), n, ctypes.c_void_p(Aw.data_ptr()),
+                             max(n, 1), vl, vu, il, iu, ctypes.byref(m),
+                             ctypes.c_void_p(w.data_ptr()),
+                             ctypes.c_void_p(Zs.data_ptr() if Zs is not None else 0), max(n, 1),
+                             ctypes.byref(st))
+    _err(c, rc, "mr3_dsyevr_dd")
+    mm = m.value
+    d = st.asdict()
+    d["t_ms"]["reduce"] = st.t_ms[6]
+    d["t_ms"]["backtransform"] = st.t_ms[7]
+    return w[:mm], (Zs[:mm].T if Zs is not None else None), d
+
+
+dsyevr = mr3_dsyevr_dd
 
 
 def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, w=None, Z=None):

@@ -1,0 +1,173 @@
+// k_dense.cuh -- NEXT-4: the dense symmetric pipeline around the tridiagonal solver
+// (Fig. 3: reduction to tridiagonal form, the mixed-precision
+// tridiagonal eigensolver, back-transformation).
+//
+// Reduction A = Q T Q^T by Householder reflectors H_j = I - tau_j v_j v_j^T (the lower form of
+// LAPACK's dsytd2: v_j(j+1) = 1, v_j(j+2:) stored in A(j+2:, j), e_j = A(j+1, j) = beta_j).
+// Step j needs column j of A after the rank-2 updates of steps < j; the update of step j is
+//   w_j = tau_j A22 v_j,  w_j += -(tau_j / 2) (w_j^T v_j) v_j,  A22 -= v_j w_j^T + w_j v_j^T
+// (A22 = A(j+1:, j+1:)).  B200 form: the trailing block is streamed ONCE per step by
+// k_sytd_fused, which applies step j-1's rank-2 update to it and, on the updated values,
+// forms y_j = A22 v_j (the symmetric matrix-vector product, read down the columns: one warp
+// per column, a fixed-order warp reduction, so the bits do not depend on scheduling).  The
+// O(n) work between two such sweeps -- finishing w_{j-1} from y_{j-1}, updating column j,
+// generating v_j -- is one CTA (k_sytd_col).  Memory: one read + one write of the trailing
+// block per step (16 (n - j)^2 bytes), L2-resident once it is below ~126 MB.
+// Back-transformation Z <- Q Z = H_0 (H_1 (... Z)) in blocks of DN_NB reflectors,
+// H_j0 ... H_j1-1 = I - V T V^T (T from G = V^T V, k_larft), as three library GEMMs each.
+#pragma once
+#include "kernels.cuh"
+
+namespace mr3 {
+
+constexpr int DN_NB = 64;      // reflectors per back-transformation block
+constexpr int DN_COLTPB = 256; // k_sytd_fused: 8 warps, one column each
+
+// fixed-order CTA sum (every thread gets the total)
+__device__ __forceinline__ double dn_block_sum(double v, double *sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; i++) t += sh[i];
+    return t;
+}
+
+// Step j's O(n) part (one CTA): finish w_{j-1} = tau y - (tau/2)(tau y^T v) v from y_{j-1},
+// apply step j-1's update to column j, record d_j, and generate the reflector of x = A(j+1:, j)
+// (dlarfg: beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta, v = x / (alpha - beta) with
+// v(j+1) = 1).  j = n - 1 only finishes the last update and records d_{n-1}.
+__global__ void __launch_bounds__(1024) k_sytd_col(double *A, int64_t lda, int n, int j,
+                                                   const double *__restrict__ vprev,
+                                                   const double *__restrict__ y, double *w,
+                                                   double *vcur, double *tau, double *d,
+                                                   double *e) {
+    __shared__ double sh[32];
+    __shared__ double s_w[2];  // w_{j-1}(j), v_{j-1}(j)
+    double *colj = A + (int64_t)j * lda;
+    const int tid = threadIdx.x;
+    const double tp = j >= 1 ? tau[j - 1] : 0.0;
+    if (tp != 0.0) {
+        // w = tp y (rows >= j); alpha = -(tp / 2) w^T v
+        double part = 0.0;
+        for (int r = j + tid; r < n; r += blockDim.x) part += tp * y[r] * vprev[r];
+        const double al = -0.5 * tp * dn_block_sum(part, sh);
+        for (int r = j + tid; r < n; r += blockDim.x) w[r] = fma(al, vprev[r], tp * y[r]);
+        __syncthreads();
+        if (tid == 0) {
+            s_w[0] = w[j];
+            s_w[1] = vprev[j];
+        }
+        __syncthreads();
+        const double wj = s_w[0], vj = s_w[1];
+        for (int r = j + tid; r < n; r += blockDim.x)
+            colj[r] = colj[r] - vprev[r] * wj - w[r] * vj;
+        __syncthreads();
+    }
+    if (tid == 0) d[j] = colj[j];
+    if (j > n - 2) return;
+    // reflector of x = A(j+1:n, j)
+    const double alpha = colj[j + 1];
+    double part = 0.0;
+    for (int r = j + 2 + tid; r < n; r += blockDim.x) part += colj[r] * colj[r];
+    const double xn2 = dn_block_sum(part, sh);
+    if (xn2 == 0.0) {  // nothing to annihilate: H = I
+        for (int r = j + 1 + tid; r < n; r += blockDim.x) vcur[r] = r == j + 1 ? 1.0 : 0.0;
+        if (tid == 0) {
+            tau[j] = 0.0;
+            e[j] = alpha;
+        }
+        return;
+    }
+    const double beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+    const double sc = 1.0 / (alpha - beta);
+    for (int r = j + 2 + tid; r < n; r += blockDim.x) {
+        const double v = colj[r] * sc;
+        vcur[r] = v;
+        colj[r] = v;  // (LAPACK storage of the reflector below the subdiagonal)
+    }
+    if (tid == 0) {
+        vcur[j + 1] = 1.0;
+        colj[j + 1] = beta;
+        tau[j] = (beta - alpha) / beta;
+        e[j] = beta;
+    }
+}
+
+// Step j's O((n - j)^2) part: one warp per column c in (j, n): apply step j-1's update
+// (A(r, c) -= v_{j-1}(r) w_{j-1}(c) + w_{j-1}(r) v_{j-1}(c), rows r > j) and, on the updated
+// values, y_j(c) = sum_r A(r, c) v_j(r) (= (A22 v_j)(c) by symmetry).  Rows r = j of these
+// columns are never read again (row j of the result is e_j, recorded by k_sytd_col).
+__global__ void __launch_bounds__(DN_COLTPB) k_sytd_fused(double *A, int64_t lda, int n, int j,
+                                                          const double *__restrict__ vprev,
+                                                          const double *__restrict__ wprev,
+                                                          const double *__restrict__ v,
+                                                          const double *__restrict__ tau,
+                                                          double *y) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * DN_COLTPB + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * DN_COLTPB) >> 5;
+    const bool upd = j >= 1 && tau[j - 1] != 0.0;
+    const int r0 = j + 1;
+    for (int c = r0 + warp; c < n; c += nwarps) {
+        double *col = A + (int64_t)c * lda;
+        double acc = 0.0;
+        if (upd) {
+            const double wc = wprev[c], vc = vprev[c];
+#pragma unroll 4
+            for (int r = r0 + lane; r < n; r += 32) {
+                const double a = col[r] - vprev[r] * wc - wprev[r] * vc;
+                col[r] = a;
+                acc = fma(a, v[r], acc);
+            }
+        } else {
+#pragma unroll 4
+            for (int r = r0 + lane; r < n; r += 32) acc = fma(col[r], v[r], acc);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[c] = acc;
+    }
+}
+
+// V of reflectors j0 .. j0 + kb - 1 as an explicit (n - j0 - 1) x kb column-major matrix
+// (rows j0 + 1 .. n - 1): zeros above the unit diagonal, the stored entries below
+__global__ void k_build_v(const double *__restrict__ A, int64_t lda, int n, int j0, int kb,
+                          double *V, int64_t ldv) {
+    const int m = n - j0 - 1;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)m * kb) return;
+    const int k = (int)(t / m), i = (int)(t % m);
+    const int r = j0 + 1 + i, jr = j0 + k;  // row of A, reflector index
+    double v;
+    if (r < jr + 1)
+        v = 0.0;
+    else if (r == jr + 1)
+        v = 1.0;
+    else
+        v = A[r + (int64_t)jr * lda];
+    V[i + (int64_t)k * ldv] = v;
+}
+
+// dlarft (forward, columnwise): T upper triangular with H_j0 ... H_j0+kb-1 = I - V T V^T;
+// T(k, k) = tau_k, T(0:k, k) = -tau_k T(0:k, 0:k) (V(:, 0:k)^T v_k), V^T V = G given.
+// One CTA of kb threads; T column-major kb x kb.
+__global__ void k_larft(const double *__restrict__ G, int kb, const double *__restrict__ tau, int j0,
+                        double *T) {
+    const int i = threadIdx.x;
+    for (int q = i; q < kb * kb; q += blockDim.x) T[q] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < kb; k++) {
+        const double tk = tau[j0 + k];
+        double t = 0.0;
+        if (i < k)
+            for (int l = i; l < k; l++) t += T[i + l * kb] * G[l + k * kb];
+        __syncthreads();
+        if (i < k) T[i + k * kb] = -tk * t;
+        if (i == k) T[k + k * kb] = tk;
+        __syncthreads();
+    }
+}
+
+}  // namespace mr3

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl.so.2 is loaded lazily (nccl_api below)
+#include <cublas_v2.h>  // types only: libcublas.so.12 is loaded lazily (dense pipeline)
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +30,7 @@
 #include "k_rqi.cuh"
 #include "k_rqi_fb.cuh"
 #include "k_rqi_chunk.cuh"
+#include "k_dense.cuh"
 #include "kernels.cuh"
 
 using namespace mr3;
@@ -98,6 +100,7 @@ struct mr3_ctx_s {
     mr3_allgather_fn xfn = nullptr;
     void *xuser = nullptr;
     std::vector<int64_t> colb;  // column partition of the last execute (world + 1 entries)
+    cublasHandle_t cublas = nullptr;  // dense pipeline's library GEMMs (created on first use)
 };
 
 // ------------------------------------------------------------------ NCCL (lazy)
@@ -127,6 +130,32 @@ bool nccl_load() {
     g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy &&
                 g_nccl.AllGather && g_nccl.GetErrorString;
     return g_nccl.ok;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ cuBLAS (lazy, dense pipeline)
+namespace {
+struct CublasApi {
+    bool tried = false, ok = false;
+    decltype(&cublasCreate_v2) Create = nullptr;
+    decltype(&cublasDestroy_v2) Destroy = nullptr;
+    decltype(&cublasSetStream_v2) SetStream = nullptr;
+    decltype(&cublasDgemm_v2) Dgemm = nullptr;
+};
+CublasApi g_cublas;
+bool cublas_load() {
+    if (g_cublas.tried) return g_cublas.ok;
+    g_cublas.tried = true;
+    void *h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    g_cublas.Create = (decltype(&cublasCreate_v2))dlsym(h, "cublasCreate_v2");
+    g_cublas.Destroy = (decltype(&cublasDestroy_v2))dlsym(h, "cublasDestroy_v2");
+    g_cublas.SetStream = (decltype(&cublasSetStream_v2))dlsym(h, "cublasSetStream_v2");
+    g_cublas.Dgemm = (decltype(&cublasDgemm_v2))dlsym(h, "cublasDgemm_v2");
+    g_cublas.ok = g_cublas.Create && g_cublas.Destroy && g_cublas.SetStream && g_cublas.Dgemm;
+    return g_cublas.ok;
 }
 }  // namespace
 
@@ -1812,6 +1841,7 @@ int mr3_destroy(mr3_ctx ctx) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
     }
+    if (ctx->cublas && cublas_load()) g_cublas.Destroy(ctx->cublas);
     cudaStreamDestroy(ctx->side);
     cudaEventDestroy(ctx->ev_root);
     cudaEventDestroy(ctx->ev_pp);
@@ -1927,6 +1957,144 @@ int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, 
                  mr3_stats *stats) {
     return solve_common(ctx, 1, jobz, range, n, d, e, vl, vu, il, iu, m, w, Z, ldz, zcap,
                         zcol_begin, zcol_end, stats);
+}
+
+// ------------------------------------------------------------------ dense pipeline (NEXT-4)
+// A = Q T Q^T (k_sytd_col + k_sytd_fused per reflector), the tridiagonal solve of T, and
+// Z <- Q Z in blocks of DN_NB reflectors (library GEMMs).  PAPER.md L1506-L1550; k_dense.cuh.
+int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int64_t lda,
+                  double vl, double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
+                  int64_t ldz, mr3_stats *stats) {
+    if (!ctx) return -1;
+    if (jobz != 'V' && jobz != 'N') return -2;
+    if (range != 'A' && range != 'I' && range != 'V') return -3;
+    if (n < 0 || n > 0x7fffffffLL) return -4;
+    if (n > 0 && !A) return -5;
+    if (lda < std::max<int64_t>(1, n)) return -6;
+    if (!m) return -11;
+    if (n > 0 && !w) return -12;
+    if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -13;
+    if (ctx->cworld > 1) {
+        ctx->err = "mr3_dsyevr_dd: single-rank contexts only";
+        return MR3_ERR_STATE;
+    }
+    *m = 0;
+    if (n == 0) return 0;
+    int rc = 0;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int nn = (int)n;
+    double *dd_ = (double *)getbuf(ctx, "dn_d", (size_t)n * 8, &rc);
+    double *de_ = (double *)getbuf(ctx, "dn_e", (size_t)n * 8, &rc);
+    double *tau = (double *)getbuf(ctx, "dn_tau", (size_t)n * 8, &rc);
+    double *vb = (double *)getbuf(ctx, "dn_v", (size_t)2 * n * 8, &rc);
+    double *wv = (double *)getbuf(ctx, "dn_w", (size_t)n * 8, &rc);
+    double *yv = (double *)getbuf(ctx, "dn_y", (size_t)n * 8, &rc);
+    if (rc) return rc;
+    cudaEvent_t ev[2];
+    CK(cudaEventCreate(&ev[0]));
+    CK(cudaEventCreate(&ev[1]));
+    CK(cudaEventRecord(ev[0], s));
+    // reduction: per reflector the O(n) column step and one sweep of the trailing block
+    int64_t launches = 0;
+    for (int j = 0; j < nn; j++) {
+        double *vcur = vb + (size_t)(j & 1) * n, *vprev = vb + (size_t)((j + 1) & 1) * n;
+        k_sytd_col<<<1, 1024, 0, s>>>(A, lda, nn, j, vprev, yv, wv, vcur, tau, dd_, de_);
+        launches++;
+        if (j > nn - 2) break;
+        const int cols = nn - j - 1;
+        const int grid = std::max(1, std::min((cols + 7) / 8, ctx->nsm * 8));
+        k_sytd_fused<<<grid, DN_COLTPB, 0, s>>>(A, lda, nn, j, vprev, wv, vcur, tau, yv);
+        launches++;
+    }
+    {
+        cudaError_t e2 = cudaGetLastError();
+        if (e2 != cudaSuccess) {
+            ctx->err = std::string("dense reduction: ") + cudaGetErrorString(e2);
+            return MR3_ERR_CUDA;
+        }
+    }
+    CK(cudaEventRecord(ev[1], s));
+    // the tridiagonal eigenproblem of T (the paper's mixed-precision solver)
+    int64_t zb = 0, ze = 0;
+    rc = mr3_dstemr_dd(ctx, jobz, range, n, dd_, de_, vl, vu, il, iu, m, w, Z, ldz,
+                       jobz == 'V' ? n : 0, &zb, &ze, stats);
+    if (rc) return rc;
+    ctx->launches += launches;
+    float ms_red = 0.f;
+    CK(cudaEventSynchronize(ev[1]));
+    CK(cudaEventElapsedTime(&ms_red, ev[0], ev[1]));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    ctx->ktimes.push_back({"k_sytrd", {(double)ms_red, (int)launches}});
+    const int64_t mcols = *m;
+    if (jobz == 'V' && mcols > 0 && n > 2) {
+        // back-transformation, blocks of reflectors from the last to the first
+        if (!cublas_load()) {
+            ctx->err = "libcublas.so.12 not found (dense back-transformation)";
+            return MR3_ERR_CUDA;
+        }
+        if (!ctx->cublas && g_cublas.Create(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) {
+            ctx->cublas = nullptr;
+            ctx->err = "cublasCreate failed";
+            return MR3_ERR_CUDA;
+        }
+        g_cublas.SetStream(ctx->cublas, s);
+        double *V = (double *)getbuf(ctx, "dn_V", (size_t)n * DN_NB * 8, &rc);
+        double *G = (double *)getbuf(ctx, "dn_G", (size_t)DN_NB * DN_NB * 8, &rc);
+        double *Tm = (double *)getbuf(ctx, "dn_T", (size_t)DN_NB * DN_NB * 8, &rc);
+        double *W1 = (double *)getbuf(ctx, "dn_W1", (size_t)DN_NB * mcols * 8, &rc);
+        double *W2 = (double *)getbuf(ctx, "dn_W2", (size_t)DN_NB * mcols * 8, &rc);
+        if (rc) return rc;
+        KTime *tb = kt_begin(ctx, "k_ormtr");
+        const int nref = nn - 2;  // reflectors 0 .. n - 3 (the last one of the reduction is I)
+        const double one = 1.0, zero = 0.0, mone = -1.0;
+        auto gemm = [&](cublasOperation_t ta, cublasOperation_t tb_, int M, int N, int K,
+                        const double *al, const double *Am, int64_t la, const double *Bm,
+                        int64_t lb, const double *be, double *Cm, int64_t lc) -> int {
+            if (g_cublas.Dgemm(ctx->cublas, ta, tb_, M, N, K, al, Am, (int)la, Bm, (int)lb, be, Cm,
+                               (int)lc) != CUBLAS_STATUS_SUCCESS) {
+                ctx->err = "cublasDgemm failed";
+                return MR3_ERR_CUDA;
+            }
+            return 0;
+        };
+        const int nblk = (nref + DN_NB - 1) / DN_NB;
+        for (int b = nblk - 1; b >= 0; b--) {
+            const int j0 = b * DN_NB, kb = std::min(DN_NB, nref - j0);
+            const int mr = nn - j0 - 1;  // rows j0 + 1 .. n - 1
+            const int64_t tot = (int64_t)mr * kb;
+            k_build_v<<<(int)((tot + 255) / 256), 256, 0, s>>>(A, lda, nn, j0, kb, V, n);
+            CKL("k_build_v");
+            if ((rc = gemm(CUBLAS_OP_T, CUBLAS_OP_N, kb, kb, mr, &one, V, n, V, n, &zero, G, kb)))
+                return rc;
+            k_larft<<<1, DN_NB, 0, s>>>(G, kb, tau, j0, Tm);
+            CKL("k_larft");
+            double *Zs = Z + j0 + 1;
+            // W1 = V^T Z(j0+1:, :), W2 = T W1, Z(j0+1:, :) -= V W2
+            if ((rc = gemm(CUBLAS_OP_T, CUBLAS_OP_N, kb, (int)mcols, mr, &one, V, n, Zs, ldz, &zero,
+                           W1, kb)))
+                return rc;
+            if ((rc = gemm(CUBLAS_OP_N, CUBLAS_OP_N, kb, (int)mcols, kb, &one, Tm, kb, W1, kb, &zero,
+                           W2, kb)))
+                return rc;
+            if ((rc = gemm(CUBLAS_OP_N, CUBLAS_OP_N, mr, (int)mcols, kb, &mone, V, n, W2, kb, &one,
+                           Zs, ldz)))
+                return rc;
+            ctx->launches += 3;
+        }
+        kt_end(ctx, tb);
+        kt_collect(ctx);
+    }
+    CK(cudaStreamSynchronize(s));
+    if (stats) {
+        *stats = ctx->stats;
+        for (auto &p : ctx->ktimes) {
+            if (p.first == "k_sytrd") stats->t_ms[6] = p.second.first;
+            if (p.first == "k_ormtr") stats->t_ms[7] = p.second.first;
+        }
+    }
+    return 0;
 }
 
 int mr3_set_exchange(mr3_ctx ctx, mr3_allgather_fn fn, void *user) {
