@@ -208,7 +208,8 @@ int mr3_sstemr_d(mr3_ctx ctx, char jobz, char range, int64_t n, const float *d, 
  *   stats: as mr3_dstemr_dd's, plus t_ms[6] = reduction ms, t_ms[7] = back-transformation ms.
  * Single-rank contexts only (world = 1, else MR3_ERR_STATE).  The back-transformation's GEMMs
  * are cuBLAS (libcublas.so.12, loaded on first use; missing -> MR3_ERR_CUDA).
- * Errors: -1 ctx NULL, -2 jobz, -3 range, -4 n, -5 A NULL, -6 lda, -11 m NULL, -12 w NULL,
+ * n <= 8192 (the reduction's column step keeps a column in the registers of one CTA).
+ * Errors: -1 ctx NULL, -2 jobz, -3 range, -4 n < 0 or n > 8192, -5 A NULL, -6 lda, -11 m NULL, -12 w NULL,
  * -13 Z NULL or ldz < n, the errors of mr3_dstemr_dd, MR3_ERR_CUDA, MR3_ERR_NOMEM.
  */
 int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int64_t lda,

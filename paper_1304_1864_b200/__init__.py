@@ -257,6 +257,9 @@ dstemr = mr3_dstemr_dd
 sstemr = mr3_sstemr_d
 
 
+_dense_work: dict = {}
+
+
 def mr3_dsyevr_dd(A, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, overwrite=False):
     """Dense symmetric fp64 eigenproblem (NEXT-4): reduction to tridiagonal form, the
     double-double tridiagonal solver, back-transformation -- all on the device.
@@ -267,7 +270,18 @@ def mr3_dsyevr_dd(A, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, overwrite=
     if A.dtype != torch.float64 or not A.is_cuda or A.dim() != 2 or A.shape[0] != A.shape[1]:
         raise TypeError("mr3: A must be a square CUDA float64 tensor")
     n = A.shape[0]
-    Aw = A if (overwrite and A.is_contiguous()) else A.contiguous().clone()
+    if overwrite and A.is_contiguous():
+        Aw = A
+    else:
+        # a cached work copy per (device, n): the library replays its captured reduction graph
+        # when the matrix buffer is the same one
+        key = (A.device.index, n)
+        Aw = _dense_work.get(key)
+        if Aw is None:
+            Aw = torch.empty_like(A, memory_format=torch.contiguous_format)
+            _dense_work.clear()
+            _dense_work[key] = Aw
+        Aw.copy_(A)
     c = _ctx(A.device.index)
     w = torch.empty(max(n, 1), dtype=torch.float64, device=A.device)
     Zs = None

@@ -38,96 +38,130 @@ __device__ __forceinline__ double dn_block_sum(double v, double *sh) {
 // Step j's O(n) part (one CTA): finish w_{j-1} = tau y - (tau/2)(tau y^T v) v from y_{j-1},
 // apply step j-1's update to column j, record d_j, and generate the reflector of x = A(j+1:, j)
 // (dlarfg: beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta, v = x / (alpha - beta) with
-// v(j+1) = 1).  j = n - 1 only finishes the last update and records d_{n-1}.
+// v(j+1) = 1).  j = n - 1 only finishes the last update and records d_{n-1}.  Each thread
+// keeps its rows r = j + tid + 1024 k (k < DN_KE) in registers: one read pass, one write
+// pass and two CTA sums per step (the step is on the reduction's critical path).
+constexpr int DN_KE = 8;  // rows per thread: n - j <= 8192
 __global__ void __launch_bounds__(1024) k_sytd_col(double *A, int64_t lda, int n, int j,
                                                    const double *__restrict__ vprev,
                                                    const double *__restrict__ y, double *w,
                                                    double *vcur, double *tau, double *d,
                                                    double *e) {
     __shared__ double sh[32];
-    __shared__ double s_w[2];  // w_{j-1}(j), v_{j-1}(j)
+    __shared__ double s_b[3];  // w_{j-1}(j), v_{j-1}(j), alpha = x(j+1)
     double *colj = A + (int64_t)j * lda;
     const int tid = threadIdx.x;
     const double tp = j >= 1 ? tau[j - 1] : 0.0;
+    double ck[DN_KE], vk[DN_KE], wk[DN_KE];
+#pragma unroll
+    for (int k = 0; k < DN_KE; k++) {
+        const int r = j + tid + 1024 * k;
+        ck[k] = r < n ? colj[r] : 0.0;
+        vk[k] = (tp != 0.0 && r < n) ? vprev[r] : 0.0;
+        wk[k] = (tp != 0.0 && r < n) ? tp * y[r] : 0.0;
+    }
     if (tp != 0.0) {
-        // w = tp y (rows >= j); alpha = -(tp / 2) w^T v
         double part = 0.0;
-        for (int r = j + tid; r < n; r += blockDim.x) part += tp * y[r] * vprev[r];
+#pragma unroll
+        for (int k = 0; k < DN_KE; k++) part = fma(wk[k], vk[k], part);
         const double al = -0.5 * tp * dn_block_sum(part, sh);
-        for (int r = j + tid; r < n; r += blockDim.x) w[r] = fma(al, vprev[r], tp * y[r]);
-        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < DN_KE; k++) {
+            const int r = j + tid + 1024 * k;
+            wk[k] = fma(al, vk[k], wk[k]);
+            if (r < n) w[r] = wk[k];
+        }
         if (tid == 0) {
-            s_w[0] = w[j];
-            s_w[1] = vprev[j];
+            s_b[0] = wk[0];
+            s_b[1] = vk[0];
         }
         __syncthreads();
-        const double wj = s_w[0], vj = s_w[1];
-        for (int r = j + tid; r < n; r += blockDim.x)
-            colj[r] = colj[r] - vprev[r] * wj - w[r] * vj;
-        __syncthreads();
-    }
-    if (tid == 0) d[j] = colj[j];
-    if (j > n - 2) return;
-    // reflector of x = A(j+1:n, j)
-    const double alpha = colj[j + 1];
-    double part = 0.0;
-    for (int r = j + 2 + tid; r < n; r += blockDim.x) part += colj[r] * colj[r];
-    const double xn2 = dn_block_sum(part, sh);
-    if (xn2 == 0.0) {  // nothing to annihilate: H = I
-        for (int r = j + 1 + tid; r < n; r += blockDim.x) vcur[r] = r == j + 1 ? 1.0 : 0.0;
-        if (tid == 0) {
-            tau[j] = 0.0;
-            e[j] = alpha;
-        }
-        return;
-    }
-    const double beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-    const double sc = 1.0 / (alpha - beta);
-    for (int r = j + 2 + tid; r < n; r += blockDim.x) {
-        const double v = colj[r] * sc;
-        vcur[r] = v;
-        colj[r] = v;  // (LAPACK storage of the reflector below the subdiagonal)
+        const double wj = s_b[0], vj = s_b[1];
+#pragma unroll
+        for (int k = 0; k < DN_KE; k++) ck[k] = ck[k] - vk[k] * wj - wk[k] * vj;
     }
     if (tid == 0) {
-        vcur[j + 1] = 1.0;
-        colj[j + 1] = beta;
-        tau[j] = (beta - alpha) / beta;
+        d[j] = ck[0];
+        colj[j] = ck[0];
+    }
+    if (j > n - 2) return;
+    // reflector of x = A(j+1:n, j): alpha = x(j+1) (thread 1's first row), ||x(j+2:)||^2
+    if (tid == 1) s_b[2] = ck[0];
+    double part = 0.0;
+#pragma unroll
+    for (int k = 0; k < DN_KE; k++) {
+        const int r = j + tid + 1024 * k;
+        if (r >= j + 2 && r < n) part = fma(ck[k], ck[k], part);
+    }
+    const double xn2 = dn_block_sum(part, sh);  // (its barriers publish s_b[2])
+    const double alpha = s_b[2];
+    const bool id = xn2 == 0.0;  // nothing to annihilate: H = I
+    const double beta = id ? alpha : -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+    const double sc = id ? 0.0 : 1.0 / (alpha - beta);
+#pragma unroll
+    for (int k = 0; k < DN_KE; k++) {
+        const int r = j + tid + 1024 * k;
+        if (r == j + 1) {
+            vcur[r] = 1.0;
+            colj[r] = beta;
+        } else if (r >= j + 2 && r < n) {
+            const double v = ck[k] * sc;
+            vcur[r] = v;
+            if (!id) colj[r] = v;  // (LAPACK storage of the reflector below the subdiagonal)
+        }
+    }
+    if (tid == 0) {
+        tau[j] = id ? 0.0 : (beta - alpha) / beta;
         e[j] = beta;
     }
 }
 
-// Step j's O((n - j)^2) part: one warp per column c in (j, n): apply step j-1's update
-// (A(r, c) -= v_{j-1}(r) w_{j-1}(c) + w_{j-1}(r) v_{j-1}(c), rows r > j) and, on the updated
-// values, y_j(c) = sum_r A(r, c) v_j(r) (= (A22 v_j)(c) by symmetry).  Rows r = j of these
-// columns are never read again (row j of the result is e_j, recorded by k_sytd_col).
+// Step j's O((n - j)^2) part: DN_SEG warps per column c in (j, n), each over one contiguous
+// segment of rows r > j: apply step j-1's update (A(r, c) -= v_{j-1}(r) w_{j-1}(c) +
+// w_{j-1}(r) v_{j-1}(c)) and, on the updated values, accumulate A(r, c) v_j(r); the segment
+// sums are added in a fixed order, y_j(c) = (A22 v_j)(c) by symmetry.  Rows r = j of these
+// columns are never read again (row j of the result is e_j, recorded by k_sytd_col).  Several
+// warps per column keep enough loads in flight when the trailing block is small.
+constexpr int DN_SEG = 4;
+constexpr int DN_CPB = DN_COLTPB / 32 / DN_SEG;  // columns per CTA (2)
 __global__ void __launch_bounds__(DN_COLTPB) k_sytd_fused(double *A, int64_t lda, int n, int j,
                                                           const double *__restrict__ vprev,
                                                           const double *__restrict__ wprev,
                                                           const double *__restrict__ v,
                                                           const double *__restrict__ tau,
                                                           double *y) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * DN_COLTPB + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * DN_COLTPB) >> 5;
+    __shared__ double part[DN_COLTPB / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int seg = warp % DN_SEG;
+    const int c = j + 1 + blockIdx.x * DN_CPB + warp / DN_SEG;
     const bool upd = j >= 1 && tau[j - 1] != 0.0;
-    const int r0 = j + 1;
-    for (int c = r0 + warp; c < n; c += nwarps) {
+    const int r0 = j + 1, m = n - r0;
+    // segment rows [s0, s1): multiples of 32 rows so every warp load is one aligned run
+    const int per = ((m + DN_SEG - 1) / DN_SEG + 31) & ~31;
+    const int s0 = r0 + seg * per, s1 = min(n, s0 + per);
+    double acc = 0.0;
+    if (c < n) {
         double *col = A + (int64_t)c * lda;
-        double acc = 0.0;
         if (upd) {
             const double wc = wprev[c], vc = vprev[c];
 #pragma unroll 4
-            for (int r = r0 + lane; r < n; r += 32) {
+            for (int r = s0 + lane; r < s1; r += 32) {
                 const double a = col[r] - vprev[r] * wc - wprev[r] * vc;
                 col[r] = a;
                 acc = fma(a, v[r], acc);
             }
         } else {
 #pragma unroll 4
-            for (int r = r0 + lane; r < n; r += 32) acc = fma(col[r], v[r], acc);
+            for (int r = s0 + lane; r < s1; r += 32) acc = fma(col[r], v[r], acc);
         }
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) y[c] = acc;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (seg == 0 && lane == 0 && c < n) {
+        double t = 0.0;
+        for (int q = 0; q < DN_SEG; q++) t += part[warp + q];
+        y[c] = t;
     }
 }
 

@@ -101,6 +101,10 @@ struct mr3_ctx_s {
     void *xuser = nullptr;
     std::vector<int64_t> colb;  // column partition of the last execute (world + 1 entries)
     cublasHandle_t cublas = nullptr;  // dense pipeline's library GEMMs (created on first use)
+    // dense reduction as one CUDA graph (2 kernels per reflector), keyed by its arguments
+    cudaGraphExec_t dn_exec = nullptr;
+    std::vector<const void *> dn_key;
+    cudaEvent_t dn_ev[2] = {nullptr, nullptr};
 };
 
 // ------------------------------------------------------------------ NCCL (lazy)
@@ -1842,6 +1846,9 @@ int mr3_destroy(mr3_ctx ctx) {
         cudaEventDestroy(t.b);
     }
     if (ctx->cublas && cublas_load()) g_cublas.Destroy(ctx->cublas);
+    if (ctx->dn_exec) cudaGraphExecDestroy(ctx->dn_exec);
+    for (auto &ev : ctx->dn_ev)
+        if (ev) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->side);
     cudaEventDestroy(ctx->ev_root);
     cudaEventDestroy(ctx->ev_pp);
@@ -1971,6 +1978,10 @@ int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int6
     if (n < 0 || n > 0x7fffffffLL) return -4;
     if (n > 0 && !A) return -5;
     if (lda < std::max<int64_t>(1, n)) return -6;
+    if (n > 1024 * DN_KE) {  // k_sytd_col keeps a column in registers of one CTA
+        ctx->err = "mr3_dsyevr_dd: n > 8192";
+        return -4;
+    }
     if (!m) return -11;
     if (n > 0 && !w) return -12;
     if (jobz == 'V' && n > 0 && (!Z || ldz < n)) return -13;
@@ -1995,25 +2006,51 @@ int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int6
     CK(cudaEventCreate(&ev[0]));
     CK(cudaEventCreate(&ev[1]));
     CK(cudaEventRecord(ev[0], s));
-    // reduction: per reflector the O(n) column step and one sweep of the trailing block
+    // reduction: per reflector the O(n) column step and one sweep of the trailing block --
+    // 2n - 1 launches, captured once into a CUDA graph (per argument set) and replayed on the
+    // internal stream, ordered after / before the caller's stream by events
     int64_t launches = 0;
-    for (int j = 0; j < nn; j++) {
-        double *vcur = vb + (size_t)(j & 1) * n, *vprev = vb + (size_t)((j + 1) & 1) * n;
-        k_sytd_col<<<1, 1024, 0, s>>>(A, lda, nn, j, vprev, yv, wv, vcur, tau, dd_, de_);
-        launches++;
-        if (j > nn - 2) break;
-        const int cols = nn - j - 1;
-        const int grid = std::max(1, std::min((cols + 7) / 8, ctx->nsm * 8));
-        k_sytd_fused<<<grid, DN_COLTPB, 0, s>>>(A, lda, nn, j, vprev, wv, vcur, tau, yv);
-        launches++;
-    }
-    {
-        cudaError_t e2 = cudaGetLastError();
-        if (e2 != cudaSuccess) {
-            ctx->err = std::string("dense reduction: ") + cudaGetErrorString(e2);
+    auto issue = [&](cudaStream_t st) {
+        for (int j = 0; j < nn; j++) {
+            double *vcur = vb + (size_t)(j & 1) * n, *vprev = vb + (size_t)((j + 1) & 1) * n;
+            k_sytd_col<<<1, 1024, 0, st>>>(A, lda, nn, j, vprev, yv, wv, vcur, tau, dd_, de_);
+            launches++;
+            if (j > nn - 2) break;
+            const int cols = nn - j - 1;
+            k_sytd_fused<<<(cols + DN_CPB - 1) / DN_CPB, DN_COLTPB, 0, st>>>(A, lda, nn, j, vprev, wv,
+                                                                              vcur, tau, yv);
+            launches++;
+        }
+    };
+    const std::vector<const void *> key = {A, (const void *)(intptr_t)lda, (const void *)(intptr_t)n,
+                                           dd_, de_, tau, vb, wv, yv};
+    if (ctx->dn_exec == nullptr || ctx->dn_key != key) {
+        if (ctx->dn_exec) cudaGraphExecDestroy(ctx->dn_exec);
+        ctx->dn_exec = nullptr;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(ctx->side, cudaStreamCaptureModeThreadLocal));
+        issue(ctx->side);
+        CK(cudaStreamEndCapture(ctx->side, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&ctx->dn_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            ctx->dn_exec = nullptr;
+            ctx->err = std::string("dense reduction graph: ") + cudaGetErrorString(ie);
             return MR3_ERR_CUDA;
         }
+        ctx->dn_key = key;
+    } else {
+        launches = 2 * n - 1;
     }
+    if (!ctx->dn_ev[0]) {
+        CK(cudaEventCreateWithFlags(&ctx->dn_ev[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->dn_ev[1], cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->dn_ev[0], s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->dn_ev[0], 0));
+    CK(cudaGraphLaunch(ctx->dn_exec, ctx->side));
+    CK(cudaEventRecord(ctx->dn_ev[1], ctx->side));
+    CK(cudaStreamWaitEvent(s, ctx->dn_ev[1], 0));
     CK(cudaEventRecord(ev[1], s));
     // the tridiagonal eigenproblem of T (the paper's mixed-precision solver)
     int64_t zb = 0, ze = 0;

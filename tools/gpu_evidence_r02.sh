@@ -10,7 +10,7 @@ timeout 2400 python -m pytest tests -m gpu -q -x --durations=25 > $O/${TAG}_pyte
 echo "pytest exit $?" >> $O/${TAG}_pytest.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 echo "bench exit $?" >> $O/${TAG}_bench.err
-CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --other-configs= --emulate-world= --no-zstore"
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --other-configs= --emulate-world= --no-zstore --dense="
 timeout 600 $CMD > $O/${TAG}_plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $O/${TAG}_launches.csv $CMD > $O/${TAG}_ncu_launch.log 2>&1
