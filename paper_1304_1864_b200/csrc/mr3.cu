@@ -1341,6 +1341,15 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         int ntasks = 0;
         if ((rc2 = make_tasks(list, &ntasks, rtpb, ncount))) return rc2;
         if ((rc2 = launch_chunks(true, list, ntasks))) return rc2;
+        if (ctx->dump) {  // located twists of the first and last singletons
+            std::vector<int32_t> hl(ncount), ht(cnt);
+            cudaMemcpy(hl.data(), list, (size_t)ncount * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(ht.data(), W.it.twist, (size_t)cnt * 4, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[mr3] twists (item:r):");
+            for (int i = 0; i < ncount; i++)
+                if (i < 6 || i >= ncount - 6) fprintf(stderr, " %d:%d", hl[i], ht[hl[i]]);
+            fprintf(stderr, "\n");
+        }
         k_twist_keys<<<(ncount + 255) / 256, 256, 0, s>>>(list, ncount, W.it.node, W.it.twist,
                                                           tkeys, tvals);
         CKL("k_twist_keys");
