@@ -1502,7 +1502,12 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
     using M1 = std::integral_constant<int, 1>;
     using G0 = std::integral_constant<bool, false>;
     using G1 = std::integral_constant<bool, true>;
-    auto hload = [&](int t, int (&h)[32]) {  // -> 16 (value - tile maximum)
+    // -> 16 (value - tile maximum); clamped rows (code -127 in tiles flagged by hstore) come
+    // back as -2^24: such a row is not a twist candidate -- clamping it to 127 units below
+    // the tile maximum would overstate it, and where the other half-vector varies as fast the
+    // opposite way (strongly localised eigenvectors, e.g. the spectrum ends of a
+    // Householder-reduced T) that made a far row with |z_r| ~ 0 win the argmax
+    auto hload = [&](int t, int (&h)[32], bool clamped) {
         const uint4 *src = hist + ((int64_t)t * A.S + slot) * 2;
 #pragma unroll
         for (int u = 0; u < 2; u++) {
@@ -1514,11 +1519,19 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                 for (int b = 0; b < 4; b++)
                     h[16 * u + 4 * q + b] = (int)(signed char)((w[q] >> (8 * b)) & 0xffu) * 16;
         }
-    };
-    auto hstore = [&](int t, const int (&h)[32]) -> int {  // returns the tile maximum
-        int m = INT_MIN;
+        if (clamped) {  // (rows exactly 127 units below the maximum go too: no candidates)
 #pragma unroll
-        for (int r = 0; r < 32; r++) m = max(m, h[r]);
+            for (int r = 0; r < 32; r++) h[r] = h[r] == -127 * 16 ? -(1 << 24) : h[r];
+        }
+    };
+    auto hstore = [&](int t, const int (&h)[32]) -> int {  // 2 x the tile maximum + clamp flag
+        int m = INT_MIN, mn = INT_MAX;
+#pragma unroll
+        for (int r = 0; r < 32; r++) {
+            m = max(m, h[r]);
+            mn = min(mn, h[r]);
+        }
+        const bool clamped = mn == INT_MIN || ((mn - m + 8) >> 4) < -127;
         uint4 *dst = hist + ((int64_t)t * A.S + slot) * 2;
 #pragma unroll
         for (int u = 0; u < 2; u++) {
@@ -1536,7 +1549,7 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
             }
             dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        return m;
+        return m * 2 + (clamped ? 1 : 0);
     };
     // both streams over one step's tiles, rows interleaved (fully unrolled: the packed
     // int16 rows live in registers)
@@ -1592,10 +1605,11 @@ __global__ void __launch_bounds__(RQ_TPB) k_rqi_locate(RqiArgs<R> A) {
                 return;
             }
             // second half: score every row against the other stream's stored value
-            hload(iA, hf);
-            hload(iD, hb);
-            const int basef = cand[(int64_t)iA * A.S + slot] - logw(tA + RQ_TR / 2);
-            const int baseb = cand[(int64_t)iD * A.S + slot] - logw(tD + RQ_TR / 2);
+            const int cA = cand[(int64_t)iA * A.S + slot], cD = cand[(int64_t)iD * A.S + slot];
+            hload(iA, hf, (cA & 1) != 0);
+            hload(iD, hb, (cD & 1) != 0);
+            const int basef = (cA >> 1) - logw(tA + RQ_TR / 2);
+            const int baseb = (cD >> 1) - logw(tD + RQ_TR / 2);
             if (guard)
                 step(M1{}, G1{}, bA, tA, bD, tD, basef, baseb, hf, hb);
             else
