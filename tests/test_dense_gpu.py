@@ -99,3 +99,14 @@ def test_dense_bench_size():
     G = Z.T @ Z - torch.eye(n, dtype=torch.float64, device="cuda")
     assert float(G.abs().max()) <= 8 * n * EPS
     assert st["t_ms"]["reduce"] > 0 and st["t_ms"]["backtransform"] > 0
+
+
+def test_dense_reduced_t_needs_no_rqi_fallback():
+    """Regression (R9b): the extreme eigenvectors of a Householder-reduced T live in
+    its first rows; the twist location once clamped the far rows' records and picked r = n - 1
+    for them (bisection fallback).  n = 1024: every eigenpair converges in the RQI, and the
+    solution keeps the dense parity bar."""
+    p = synth.dense_config(1024, 3)
+    w, Z, st = run(p.A)
+    assert st["rqi_fallbacks"] == 0, st["rqi_fallbacks"]
+    _check(p.A, w, Z, oracle_vectors=False)
