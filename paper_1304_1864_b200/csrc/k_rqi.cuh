@@ -113,6 +113,11 @@ __device__ __forceinline__ int sgn_ne_R(R x, R y) {
 __device__ __forceinline__ double pow2mul_d(double v, int k) {
     return k < -1022 ? 0.0 : v * __hiloint2double((k + 1023) << 20, 0);
 }
+// ||z||^2 of a storing pass from the sum of the written squares in z_r = 1 units (reading
+// R9e); a non-finite or sub-unit sum (z_r is one of the terms) cannot be a norm: 1 + nothing
+__device__ __forceinline__ double nz2_of_ss(double ss) {
+    return (ss >= 1.0 && ss <= 1e300) ? ss : 1.0;
+}
 // compensated (Kahan) sum of squares: sum += x^2
 __device__ __forceinline__ void kahan_sq(double x, double &sum, double &comp) {
     const double y = fma(x, x, -comp);
@@ -532,6 +537,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         // z components in product form (k_zprod.cuh): row kk <= r: y = qF / PP_kk,
         // row kk >= r: x = QB PP_kk, written scaled by 2^-ref (ref from the previous pass)
         const bool wz = store && need && zcol != nullptr;
+        const bool sq = store && need;  // squares summed (the norm of a storing pass, R9e)
         auto ppr = [&](int64_t kk, double &pm, double &ipm, int &e) {
             const double2 *q = reinterpret_cast<const double2 *>(nd.pp + kk * PP_STRIDE);
             const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double W2 = clampbig(fma(l2, W, l2));
             const R p2 = dot2_dd(mlam, D, rw.lld, pF);
             if (!GUARD || (int)kk < (int)r) {
-                if (wz) {
+                if (sq) {
                     double pm, ipm;
                     int e;
                     sppr(bA, tA, kk, pm, ipm, e);
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             const double V2 = clampbig(fma(u2, V, u2));
             const R P2 = dot2_dd(mlam, E, rw.d, pB);
             if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
-                if (wz) {
+                if (sq) {
                     double pm, ipm;
                     int e;
                     sppr(bD, tD, kk, pm, ipm, e);
@@ -684,7 +690,6 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
         if (need) {
             gr = add(add(div(pF, qF), div(pB, qB)), lam);
             negc += is_neg(gr) ? 1 : 0;
-            nz2 = 1.0 + W + V;
             rows += n;
             // y_r = qF / PP_r and x_r = QB PP_r: references for the next pass and the
             // per-column factors (z_i = Z_i 2^refF / y_r, z_k = Z_k 2^refB / x_r)
@@ -693,14 +698,22 @@ __global__ void __launch_bounds__(RQ_TPB, 3) k_rqi(RqiArgs<R> A) {
             if (nd.pp != nullptr) ppr(r, pm, ipm, e);
             const double yr = hi(qF) * ipm, xr = hi(qB) * pm;
             const int eyr = EqF - e, exr = EqB + e;
-            if (wz) {
+            if (sq) {  // k_rqi_fb's storing-pass join, the same operations
                 const OutT zo = (OutT)pow2mul(yr, eyr - erefF);
-                zcol[r] = zo;
                 kahan((double)zo, sF, cF_);
-                zinfo.cF = ldexp(1.0, erefF - eyr) / yr;
-                zinfo.cB = ldexp(1.0, erefB - exr) / xr;
-                zinfo.ss = zinfo.cF * zinfo.cF * sF + zinfo.cB * zinfo.cB * sB;
-                zwritten = true;
+                const double fF = ldexp(1.0, erefF - eyr) / yr;
+                const double fB = ldexp(1.0, erefB - exr) / xr;
+                const double ss = fF * fF * sF + fB * fB * sB;
+                nz2 = nz2_of_ss(ss);
+                if (wz) {
+                    zcol[r] = zo;
+                    zinfo.cF = fF;
+                    zinfo.cB = fB;
+                    zinfo.ss = ss;
+                    zwritten = true;
+                }
+            } else {
+                nz2 = 1.0 + W + V;
             }
             erefF = eyr + expo_of(yr);
             erefB = exr + expo_of(xr);

@@ -179,9 +179,13 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             constexpr bool GUARD = decltype(guard)::value;
             const Row4<R> rw = srow<R>(bA, tA, kk);
             const R D = fma_dd(rw.d, qx, px);
-            const double lpx = hi(rw.ld) * hi(qx) * rcp_w(hi(D));  // l+ = ld / d+
-            const double l2 = lpx * lpx;
-            const double N2 = clampbig(fma(l2, nrm, l2));
+            // (a storing pass takes ||z||^2 from the written squares, R9e: no norm identity)
+            double N2 = 0.0;
+            if (!STORE) {
+                const double lpx = hi(rw.ld) * hi(qx) * rcp_w(hi(D));  // l+ = ld / d+
+                const double l2 = lpx * lpx;
+                N2 = clampbig(fma(l2, nrm, l2));
+            }
             const R p2 = DOT2 ? dot2_dd(add(rw.lld, mlam), px, mul(mlam, rw.d), qx)
                               : dot2_dd(mlam, D, rw.lld, px);
             if (!GUARD || (int)kk < (int)r) {
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
                     kahan_sq((double)zo, ks, kc);
                 }
                 negc += sgn_ne_R<R>(D, qx);
-                nrm = N2;
+                if (!STORE) nrm = N2;
                 px = p2;
                 qx = D;
             }
@@ -204,9 +208,12 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             constexpr bool GUARD = decltype(guard)::value;
             const Row4<R> rw = srow<R>(bD, tD, kk - 1);
             const R E = fma_dd(rw.lld, qx, px);
-            const double ux = hi(rw.ld) * hi(qx) * rcp_w(hi(E));  // u- = l d / D-
-            const double u2 = ux * ux;
-            const double N2 = clampbig(fma(u2, nrm, u2));
+            double N2 = 0.0;
+            if (!STORE) {
+                const double ux = hi(rw.ld) * hi(qx) * rcp_w(hi(E));  // u- = l d / D-
+                const double u2 = ux * ux;
+                N2 = clampbig(fma(u2, nrm, u2));
+            }
             const R P2 = DOT2 ? dot2_dd(add(rw.d, mlam), px, mul(mlam, rw.lld), qx)
                               : dot2_dd(mlam, E, rw.d, px);
             if (!GUARD || ((int)kk > (int)r && (int)kk < (int)n)) {
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
                     kahan_sq((double)zo, ks, kc);
                 }
                 negc += sgn_ne_R<R>(E, qx);
-                nrm = N2;
+                if (!STORE) nrm = N2;
                 px = P2;
                 qx = E;
             }
@@ -316,7 +323,6 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
         if (need) {
             gr = add(add(div(F.p, F.q), div(B.p, B.q)), lam);
             negt = F.negc + B.negc + (is_neg(gr) ? 1 : 0);
-            nz2 = 1.0 + F.nrm + B.nrm;
             rows += n;
             double pm = 1.0, ipm = 1.0;
             int e = 0;
@@ -329,15 +335,23 @@ __global__ void __launch_bounds__(FB_TPB, 6) k_rqi_fb(RqiArgs<R> A) {
             }
             const double yr = hi(F.q) * ipm, xr = hi(B.q) * pm;
             const int eyr = F.E - e, exr = B.E + e;
-            if (wz) {
+            if (STORE) {  // ||z||^2 = the sum of the written squares in z_r = 1 units (R9e)
                 const OutT zo = (OutT)pow2mul_d(yr, eyr - erefF);
                 double sF = F.s, cF_ = F.c;
-                if (role == 0) zcol[r] = zo;
                 kahan_sq((double)zo, sF, cF_);
-                zinfo.cF = ldexp(1.0, erefF - eyr) / yr;
-                zinfo.cB = ldexp(1.0, erefB - exr) / xr;
-                zinfo.ss = zinfo.cF * zinfo.cF * sF + zinfo.cB * zinfo.cB * B.s;
-                zwritten = true;
+                const double fF = ldexp(1.0, erefF - eyr) / yr;
+                const double fB = ldexp(1.0, erefB - exr) / xr;
+                const double ss = fF * fF * sF + fB * fB * B.s;
+                nz2 = nz2_of_ss(ss);
+                if (wz) {
+                    if (role == 0) zcol[r] = zo;
+                    zinfo.cF = fF;
+                    zinfo.cB = fB;
+                    zinfo.ss = ss;
+                    zwritten = true;
+                }
+            } else {
+                nz2 = 1.0 + F.nrm + B.nrm;
             }
             erefF = eyr + expo_of(yr);
             erefB = exr + expo_of(xr);

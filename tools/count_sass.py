@@ -42,10 +42,11 @@ def loops(ins):
 
 
 def classify(body):
-    c = {"DADD": 0, "DMUL": 0, "DFMA": 0, "MUFU.RCP64H": 0, "LDG": 0, "DSETP": 0, "total": len(body)}
+    c = {"DADD": 0, "DMUL": 0, "DFMA": 0, "MUFU.RCP64H": 0, "LDG": 0, "DSETP": 0, "LDL": 0, "STL": 0,
+         "LDS": 0, "total": len(body)}
     for t in body:
         op = re.sub(r"^@!?U?P\w+\s+", "", t).split()[0]
-        for k in ("DADD", "DMUL", "DFMA", "DSETP", "LDG"):
+        for k in ("DADD", "DMUL", "DFMA", "DSETP", "LDG", "LDL", "STL", "LDS"):
             if op.startswith(k):
                 c[k] += 1
         if op.startswith("MUFU.RCP64H"):
