@@ -539,298 +539,6 @@ def main():
             traffic_tab = {}
 
     roof = make_roof(ktot, stats, args.steps, mode, traffic_tab, peak_ips)
-
-    cand = [k for k in ("k_bisect", "k_rqi") if k in ktot]
-    dom = max(cand, key=lambda k: ktot[k][0]) if cand else "k_rqi"
-    line = {"config": cfg, "metric": metric_name(p), "value": m_req / (t * 1e-3),
-            "unit": "eigenpairs/s", "ms_per_step": t, "steps": steps, "n": p.n, "m": m_req,
-            "io": p.io, "roofline": roof(dom),
-            "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
-                        for k, v in ktot.items()},
-            "gpu_launches": launches,
-            "stats": {k: v for k, v in (stats or {}).items()}}
-    if cpu:
-        # the oracle in full (north_star: the full run for n <= 20000)
-        idx = np.arange(il, iu + 1)
-        cnt, dt_cpu, cores = cpu_baseline_run(p, 0, idx=idx)
-        line["cpu_baseline"] = {"value": cnt / dt_cpu, "unit": "eigenpairs/s", "cores": cores,
-                                "cpu": cpu_model(), "kind": "oracle",
-                                "sample": f"full run: all {cnt} requested eigenpairs, binary128 "
-                                          f"bisection on T + inverse iteration, {dt_cpu:.1f} s"}
-    del d, e
-    torch.cuda.empty_cache()
-    return line
-
-
-def dense_line(mr3, n, steps, warmup, flush, stream, cpu):
-    """NEXT-4: the dense symmetric pipeline (reduction, tridiagonal solve, back-transformation)
-    through mr3_dsyevr_dd, A = Q T Q^T resident in HBM (copied into the library's work buffer
-    inside the timed region: the call overwrites A).  Roofline of the reduction (both of its
-    kernels, the dominant phase): algorithmic bytes = one read of the trailing block per
-    reflector and one write from the second on, sum_j 8 (n - j - 1)^2 (1 + [j >= 1])."""
-    import torch
-    p = synth.dense_config(n, 0)
-    A = torch.from_numpy(np.ascontiguousarray(p.A)).cuda()
-    times, ktot, launches = [], {}, 0
-    st = None
-    for it in range(warmup + steps):
-        flush.fill_(it)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        w, Z, st = mr3.mr3_dsyevr_dd(A)
-        b.record(stream)
-        torch.cuda.synchronize()
-        if it >= warmup:
-            times.append(a.elapsed_time(b))
-            for k, (ms, nl) in mr3.kernel_times().items():
-                t0, n0 = ktot.get(k, (0.0, 0))
-                ktot[k] = (t0 + ms, n0 + nl)
-            launches += mr3.launch_count()
-        del w, Z
-    t = float(np.mean(times))
-    j = np.arange(n - 1, dtype=np.float64)
-    red_bytes = float(np.sum(8.0 * (n - j - 1) ** 2 * np.where(j >= 1, 2.0, 1.0)))
-    red_ms = ktot.get("k_sytrd", (float("nan"), 0))[0] / steps
-    peak, peak_src = hbm_peak()
-    ach = red_bytes / (red_ms * 1e-3) / 1e9
-    line = {"metric": f"eigenpairs/s, dense symmetric fp64 I/O (A = Q T Q^T), n={n}",
-            "value": n / (t * 1e-3), "unit": "eigenpairs/s", "ms_per_step": t, "steps": steps,
-            "n": n, "m": n, "io": "f64",
-            "config": {"workload": p.name, "n": n, "range": "A",
-                       "pipeline": "Householder reduction (k_sytd_col + k_sytd_fused, one CUDA "
-                                   "graph) -> mr3_dstemr_dd -> blocked back-transformation "
-                                   "(k_build_v, k_larft, cuBLAS DGEMM)"},
-            "roofline": {"bound": "hbm", "kernel": "k_sytrd (k_sytd_fused + k_sytd_col)",
-                         "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "traffic": None, "bytes_per_launch": red_bytes,
-                         "ms_per_launch": red_ms,
-                         "peak_source": peak_src,
-                         "note": "the trailing block is L2-resident once below ~126 MB "
-                                 "(n - j < ~3970): later sweeps run from L2"},
-            "kernels": {k: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
-                        for k, v in ktot.items()},
-            "gpu_launches": launches,
-            "stats": {k: v for k, v in (st or {}).items()}}
-    if cpu:
-        from oracle import dense as odense
-        import oracle
-        ns = 512
-        q = synth.dense_config(ns, 0)
-        t0 = time.time()
-        odense.eig_dense(q.A)
-        dt_cpu = time.time() - t0
-        line["cpu_baseline"] = {"value": ns / dt_cpu, "unit": "eigenpairs/s",
-                                "cores": oracle.num_threads(), "cpu": cpu_model(),
-                                "kind": "oracle",
-                                "sample": f"full run at n={ns} (same recipe): numpy Householder "
-                                          f"reduction + binary128 tridiagonal oracle + Q y, "
-                                          f"{dt_cpu:.1f} s (the n^3 reduction makes n={n} "
-                                          f"~{(n / ns) ** 3:.0f}x longer)"}
-    del A
-    torch.cuda.empty_cache()
-    return line
-
-
-def emulate_world(mr3, p, world, stream):
-    """Ranks of the two-phase form run one after another on this GPU: per rank, device time of
-    mr3_plan (root + its slice's bisection) and of mr3_execute (classification, its columns'
-    child representations and eigenvectors); the bracket all-gather is a device copy."""
-    import ctypes
-
-    import torch
-    L = mr3.lib()
-    d = torch.from_numpy(p.d).cuda()
-    e = torch.from_numpy(p.e).cuda()
-    n = p.n
-    ctxs, bufs, caps, tplan = [], [], [], []
-    for r in range(world):
-        h = ctypes.c_void_p()
-        assert L.mr3_create(ctypes.byref(h), torch.cuda.current_device(),
-                            ctypes.c_void_p(int(stream.cuda_stream) or 1), None, 0, 1) == 0
-        ctxs.append(h)
-        m, brk = ctypes.c_int64(), ctypes.c_void_p()
-        cap, cnt = ctypes.c_int64(), ctypes.c_int64()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        rc = L.mr3_plan(h, 0 if p.io == "f64" else 1, p.range.encode(), n,
-                        ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(e.data_ptr()), 0.0, 0.0,
-                        1, n, r, world, ctypes.byref(m), ctypes.byref(brk), ctypes.byref(cap),
-                        ctypes.byref(cnt))
-        b.record(stream)
-        torch.cuda.synchronize()
-        assert rc == 0, rc
-        tplan.append(a.elapsed_time(b))
-        bufs.append(mr3.distributed.wrap_device(brk.value, world * cap.value * 6, d.device))
-        caps.append(cap.value)
-    rec = 6 * caps[0]
-    full = torch.cat([bufs[r][r * rec:(r + 1) * rec] for r in range(world)])
-    for r in range(world):
-        bufs[r][:world * rec].copy_(full)
-    torch.cuda.synchronize()
-    dt = torch.float64 if p.io == "f64" else torch.float32
-    texec, cols = [], []
-    for r in range(world):
-        w = torch.zeros(n, dtype=dt, device="cuda")
-        zb, ze = ctypes.c_int64(), ctypes.c_int64()
-        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()), None, n, 0,
-                           ctypes.byref(zb), ctypes.byref(ze), None)
-        Zs = torch.empty((max(ze.value - zb.value, 1), n), dtype=dt, device="cuda")
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        rc = L.mr3_execute(ctxs[r], b"V", ctypes.c_void_p(w.data_ptr()),
-                           ctypes.c_void_p(Zs.data_ptr()), n, Zs.shape[0], ctypes.byref(zb),
-                           ctypes.byref(ze), None)
-        b.record(stream)
-        torch.cuda.synchronize()
-        assert rc == 0, rc
-        texec.append(a.elapsed_time(b))
-        cols.append(ze.value - zb.value)
-        del Zs, w
-    for h in ctxs:
-        L.mr3_destroy(h)
-    per_rank = [a + b for a, b in zip(tplan, texec)]
-    torch.cuda.empty_cache()
-    return {"world": world, "per_rank_ms": [round(x, 3) for x in per_rank],
-            "plan_ms": [round(x, 3) for x in tplan], "execute_ms": [round(x, 3) for x in texec],
-            "columns": cols, "max_rank_ms": max(per_rank),
-            "note": "ranks emulated sequentially on one GPU (each alone on the device); the "
-                    "all-gathers are device copies; not a multi-GPU measurement"}
-
-
-def metric_name(p):
-    io = "fp32 I/O fp64-internal" if p.io == "f32" else "fp64 I/O dd-internal"
-    return f"eigenpairs/s, {io}, {p.name} n={p.n}"
-
-
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    p = synth.config(args.config)
-
-    if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist
-            dist.init_process_group("gloo")
-        run_reference(args, p, rank, world)
-        return
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_1304_1864_b200 as mr3
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    mr3.lib()
-    dt = torch.float32 if p.io == "f32" else torch.float64
-    d = torch.from_numpy(p.d).cuda()
-    e = torch.from_numpy(p.e).cuda()
-    n = p.n
-    il, iu = p.index_range()
-    m_req = iu - il + 1
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
-
-    def solve():
-        if world > 1:
-            return mr3.solve_distributed(d, e, "V", p.range, il, iu)
-        fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
-        w, Z, st = fn(d, e, "V", p.range, il, iu)
-        return w, Z, (0, w.numel()), st
-
-    # K7: same-run FP64 peak
-    peak_ips, dd_step_ns = mr3.fp64_peak()
-
-    for _ in range(args.warmup):
-        out = solve()
-        del out
-    torch.cuda.synchronize()
-
-    stream = torch.cuda.current_stream()
-    times = []
-    ktot = {}
-    launches = 0
-    stats = None
-    with Clocks(local) as clk:
-        for s in range(args.steps):
-            flush.fill_(s)  # L2 flush between timed steps (outside the events)
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            w, Z, rng, stats = solve()
-            b.record(stream)
-            torch.cuda.synchronize()
-            times.append(a.elapsed_time(b))
-            for k, (ms, nl) in mr3.kernel_times().items():
-                t0, n0 = ktot.get(k, (0.0, 0))
-                ktot[k] = (t0 + ms, n0 + nl)
-            launches += mr3.launch_count()
-            del w, Z
-    t_step = float(np.mean(times))
-    t_max = t_step
-    if world > 1:
-        tt = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    value = m_req / (t_max * 1e-3)  # all ranks together produce the m eigenpairs of one solve
-
-    # roofline of the dominant kernel (the larger of k_bisect and k_rqi): algorithmic FP64
-    # instructions per launch / its CUDA-event time inside the timed region
-    mode = "f64" if p.io == "f32" else "dd"
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    traffic_tab = {}
-    if os.path.exists(tp):
-        try:
-            traffic_tab = json.load(open(tp)).get(f"config{args.config}", {})
-        except Exception:
-            traffic_tab = {}
-
-    roof = make_roof(ktot, stats, args.steps, mode, traffic_tab, peak_ips)
-    _unused = roof  # (noqa)
-
-    def roof_old(kname):
-        ms, nl = ktot.get(kname, (0.0, 0))
-        if kname == "k_bisect":
-            rows = stats["bisect_rows"] if stats else 0.0
-            rows_x = stats.get("bisect_rows_x", 0.0) if stats else 0.0
-            rows_n = stats.get("newton_rows_x", 0.0) if stats else 0.0
-            inst = (rows * FP64_INST_PER_BISECT_ROW[mode] +
-                    (rows_x - rows_n) * FP64_INST_PER_BISECT_ROW["x"] +
-                    rows_n * FP64_INST_PER_BISECT_ROW["newton"])
-            per = {"binary_y_row": FP64_INST_PER_BISECT_ROW[mode],
-                   "binary_x_row": FP64_INST_PER_BISECT_ROW["x"],
-                   "binary_x_newton_row": FP64_INST_PER_BISECT_ROW["newton"]}
-            units = {"binary_y_rows": rows, "binary_x_rows": rows_x - rows_n,
-                     "binary_x_newton_rows": rows_n}
-        else:
-            rows = stats["rqi_rows"] if stats else 0.0
-            inst = rows * FP64_INST_PER_RQI_ROW[mode]
-            per = {"rqi_row": FP64_INST_PER_RQI_ROW[mode]}
-            units = {"rqi_rows": rows}
-        t_launch = ms / max(nl, 1) * 1e-3  # average launch duration
-        inst_launch = inst / max(nl / args.steps, 1)
-        ach = inst_launch / t_launch if t_launch else 0.0
-        return {"bound": "alu", "kernel": kname, "achieved": ach / 1e12,
-                "peak": DERIVED_FP64_PEAK / 1e12, "unit": "T FP64-inst/s",
-                "frac": ach / DERIVED_FP64_PEAK, "traffic": traffic_tab.get(kname),
-                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1.965 GHz (MEASURED_PEAKS.json "
-                               "has no FP64 entry); measured_peak_same_run = K7 DFMA microbenchmark",
-                "measured_peak_same_run": peak_ips / 1e12,
-                "frac_of_measured": ach / peak_ips if peak_ips else None,
-                "inst_per_unit": per, "units_per_step": units,
-                "launches_per_step": nl / args.steps, "ms_per_launch": t_launch * 1e3}
-
     cand = [k for k in ("k_bisect", "k_rqi") if k in ktot]
     dom = max(cand, key=lambda k: ktot[k][0]) if cand else "k_bisect"
     roofs = {k: roof(k) for k in cand}
@@ -902,14 +610,18 @@ def main():
         # peak; with the default fused epilogue the same traffic runs inside k_rqi
         mr3.set_param("FUSE_SCALE", 0, 0)
         try:
-            zt = []
+            zt, rt, rrows = [], [], 0.0
             for s in range(2):
                 flush.fill_(s)
                 w, Z, st = mr3.mr3_dstemr_dd(d, e, "V", p.range, il, iu)
                 torch.cuda.synchronize()
-                kz = mr3.kernel_times().get("k_zscale")
+                kts = mr3.kernel_times()
+                kz = kts.get("k_zscale")
                 if kz:
                     zt.append(kz[0])
+                if kts.get("k_rqi"):
+                    rt.append(kts["k_rqi"][0])
+                    rrows = float(st["rqi_rows"])
                 del w, Z
         finally:
             mr3.set_param("FUSE_SCALE", -1, 0)
@@ -928,6 +640,20 @@ def main():
                 "note": "Z is written once by the storing RQI pass (8 n m bytes) and read + "
                         "written once more by the exact normalisation (DESIGN.md section 5): 3x "
                         "the algorithmic bytes in total"}
+        if rt and rrows:
+            # the same launch without its HBM-bound epilogue: the two factorization passes alone
+            tr = min(rt) * 1e-3
+            ach = rrows * FP64_INST_PER_RQI_ROW[mode] / tr
+            result["roofline_other"]["k_rqi_passes_only"] = {
+                "bound": "alu", "kernel": "k_rqi (MR3_FUSE_SCALE=0: no normalisation epilogue)",
+                "achieved": ach / 1e12, "peak": DERIVED_FP64_PEAK / 1e12, "unit": "T FP64-inst/s",
+                "frac": ach / DERIVED_FP64_PEAK,
+                "measured_peak_same_run": peak_ips / 1e12,
+                "frac_of_measured": ach / peak_ips if peak_ips else None,
+                "inst_per_unit": {"rqi_row": FP64_INST_PER_RQI_ROW[mode]},
+                "units_per_launch": {"rqi_rows": rrows}, "ms_per_launch": tr * 1e3,
+                "note": "k_rqi_fb timed with the normalisation in its own kernel (k_zscale, "
+                        "z_store above); the headline roofline keeps the fused launch"}
     if rank == 0 and world == 1 and args.other_configs:
         oc = []
         for cfg in [int(x) for x in args.other_configs.split(",") if x.strip()]:
