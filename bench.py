@@ -62,6 +62,10 @@ def parse():
                          "after another on this GPU; per-rank device times under "
                          "'emulated_world' (an emulation, not a multi-GPU measurement)")
     ap.add_argument("--no-zstore", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for --gpus > 1 (gloo: logic tests of the multi-rank "
+                         "path with several ranks sharing one GPU and the host-staged exchange; "
+                         "never a measurement)")
     ap.add_argument("--dense", default="4096",
                     help="NEXT-4 dense pipeline line (mr3_dsyevr_dd on A = Q T Q^T of this size, "
                          "T the config-2 recipe) under 'dense'; '' = none")
@@ -469,9 +473,20 @@ def main():
 
     import paper_1304_1864_b200 as mr3
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    rdev = "cuda" if args.backend == "nccl" else "cpu"  # where the timing reductions live
+
+    def allreduce(v, op):
+        t = torch.tensor([v], dtype=torch.float64, device=rdev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
     mr3.lib()
     dt = torch.float32 if p.io == "f32" else torch.float64
     d = torch.from_numpy(p.d).cuda()
@@ -481,15 +496,32 @@ def main():
     m_req = iu - il + 1
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
 
+    exch = {"mode": "auto"}  # in-library NCCL communicator (mr3_nccl_comm_init + ncclAllGather)
+
     def solve():
         if world > 1:
-            return mr3.solve_distributed(d, e, "V", p.range, il, iu)
+            return mr3.solve_distributed(d, e, "V", p.range, il, iu, exchange=exch["mode"])
         fn = mr3.mr3_sstemr_d if p.io == "f32" else mr3.mr3_dstemr_dd
         w, Z, st = fn(d, e, "V", p.range, il, iu)
         return w, Z, (0, w.numel()), st
 
     # K7: same-run FP64 peak
     peak_ips, dd_step_ns = mr3.fp64_peak()
+
+    if world > 1:
+        # one untimed solve decides the exchange for every rank together: if the in-library
+        # communicator cannot be set up on this box (no usable libnccl.so.2 for the library),
+        # all ranks fall back to the two-phase form whose all-gathers torch.distributed issues
+        # (still NCCL); the line says which one ran
+        bad = 0
+        try:
+            out = solve()
+            del out
+        except Exception as ex:  # noqa: BLE001
+            bad = 1
+            print(f"[rank {rank}] in-library NCCL exchange failed: {ex}", file=sys.stderr)
+        if allreduce(float(bad), dist.ReduceOp.MAX) > 0:
+            exch["mode"] = "torch"
 
     for _ in range(args.warmup):
         out = solve()
@@ -522,9 +554,7 @@ def main():
     t_step = float(np.mean(times))
     t_max = t_step
     if world > 1:
-        tt = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+        t_max = allreduce(t_step, dist.ReduceOp.MAX)
     value = m_req / (t_max * 1e-3)  # all ranks together produce the m eigenpairs of one solve
 
     # roofline of the dominant kernel (the larger of k_bisect and k_rqi): algorithmic FP64
@@ -554,6 +584,11 @@ def main():
             "dtype": "f64" if p.io == "f32" else "dd (f64 pairs)", "data": "synthetic",
             "config": {"workload": p.name, "n": n, "m": m_req, "range": p.range,
                        "io": p.io, "parallelism": f"index-set partition x{world}",
+                       "exchange": ("none" if world == 1 else
+                                    "host-staged callback (gloo logic test)"
+                                    if args.backend != "nccl" else
+                                    "in-library ncclAllGather" if exch["mode"] == "auto" else
+                                    "torch.distributed all_gather (two-phase)"),
                        "l2": "512 MB buffer written between timed steps; Z output > L2"},
             "roofline": roofs.get(dom, {}),
             "roofline_other": {k: v for k, v in roofs.items() if k != dom},
@@ -592,6 +627,46 @@ def main():
                              "d2h_bytes_per_step": (m_req + m_req * n) * esz,
                              "ms_per_step": float(np.mean(et)),
                              "api": "mr3_sstemr_d_host" if p.io == "f32" else "mr3_dstemr_dd_host"}
+        del hZ
+
+    if not args.no_e2e and world > 1:
+        # e2e at N ranks: every rank copies d, e from pinned host memory, runs the multi-rank
+        # solve and reads w and ITS columns of Z back into pinned host memory inside the timed
+        # region (barrier + synchronize on both sides, max over ranks)
+        hd = torch.from_numpy(p.d).pin_memory()
+        he = torch.from_numpy(p.e).pin_memory()
+        w0, Z0, rng0, _ = solve()
+        ncol = Z0.shape[1]
+        del w0, Z0
+        hw = torch.empty(m_req, dtype=dt).pin_memory()
+        hZ = torch.empty((max(ncol, 1), n), dtype=dt).pin_memory()
+        et = []
+        for s in range(max(1, min(args.steps, 2))):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dd_ = hd.cuda(non_blocking=True)
+            ee_ = he.cuda(non_blocking=True)
+            wv, Zv, rg, st = mr3.solve_distributed(dd_, ee_, "V", p.range, il, iu,
+                                                   exchange=exch["mode"])
+            hw.copy_(wv, non_blocking=True)
+            hZ[:Zv.shape[1]].copy_(Zv.T, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            et.append(a.elapsed_time(b))
+            del wv, Zv, dd_, ee_
+        esz = 4 if p.io == "f32" else 8
+        te = allreduce(float(np.mean(et)), dist.ReduceOp.MAX)
+        nb = allreduce(float((m_req + ncol * n) * esz), dist.ReduceOp.SUM)
+        if rank == 0:
+            result["e2e"] = {"value": m_req / (te * 1e-3), "unit": "eigenpairs/s",
+                             "h2d_bytes_per_step": (2 * n - 1) * esz * world,
+                             "d2h_bytes_per_step": nb,
+                             "ms_per_step": te,
+                             "api": "solve_distributed (one C-ABI call per rank; pinned host "
+                                    "d, e in, w and the rank's Z columns out)"}
         del hZ
 
     if rank == 0 and not args.no_cpu:

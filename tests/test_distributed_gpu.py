@@ -137,3 +137,30 @@ def test_nccl_communicator_world1():
     assert torch.equal(w, w0) and torch.equal(Zs.T, Z0)
     L.mr3_destroy(h)
     assert L.mr3_nccl_comm_destroy(comm) == 0
+
+
+def test_bench_two_ranks_gloo_json_line():
+    """The driver's N > 1 launch of bench.py (torch.distributed.run, one rank per process) on
+    the multi-rank path, as a logic test: two ranks share the one GPU over gloo (host-staged
+    exchange).  Rank 0 prints ONE JSON line with the contract's keys, the N-rank e2e among them."""
+    import json
+    import subprocess
+    import sys
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
+           "--backend", "gloo", "--config", "2", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["steps"] == 2 and j["value"] > 0
+    assert j["unit"] == "eigenpairs/s" and j["scaling"] == "strong"
+    assert j["config"]["parallelism"].endswith("x2")
+    e = j["e2e"]
+    n, m = j["config"]["n"], j["config"]["m"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * (2 * n - 1) * 8
+    # both ranks read all of w and, together, every column of Z exactly once
+    assert e["d2h_bytes_per_step"] == (2 * m + m * n) * 8
+    assert j["gpu_launches"] > 0 and "roofline" in j and "clocks" in j
