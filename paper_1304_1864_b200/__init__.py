@@ -189,10 +189,19 @@ def _err(c, rc, what):
         raise MR3Error(rc, f"{what}: {msg}")
 
 
+_last = {"ctx": None}  # the context of the last solve (single-rank or distributed)
+
+
+def _used(c):
+    _last["ctx"] = c
+    return c
+
+
 def kernel_times():
-    """{kernel name: (total ms, launches)} of the last solve on the current context
-    (CUDA events recorded on the context's stream around each launch)."""
-    c = _ctx()
+    """{kernel name: (total ms, launches)} of the last solve (on the context that solve used:
+    the device/stream context, or the rank's distributed context), from CUDA events recorded
+    on the context's stream around each launch."""
+    c = _last["ctx"] or _ctx()
     cnt = ctypes.c_int(0)
     names = (ctypes.c_char_p * 16)()
     ms = (ctypes.c_double * 16)()
@@ -203,7 +212,7 @@ def kernel_times():
 
 def launch_count() -> int:
     """Kernel launches issued by the last solve (all of this library's kernels)."""
-    return int(lib().mr3_last_launch_count(_ctx()))
+    return int(lib().mr3_last_launch_count(_last["ctx"] or _ctx()))
 
 
 def _solve(mode, d, e, jobz, range_, il, iu, vl, vu, w=None, Z=None):
@@ -216,7 +225,7 @@ def _solve(mode, d, e, jobz, range_, il, iu, vl, vu, w=None, Z=None):
     n = d.numel()
     if e.numel() < max(n - 1, 0):
         raise ValueError("mr3: e must have n-1 entries")
-    c = _ctx(d.device.index)
+    c = _used(_ctx(d.device.index))
     if w is None:
         w = torch.empty(max(n, 1), dtype=dt, device=d.device)
     if jobz == "V" and Z is None:
@@ -282,7 +291,7 @@ def mr3_dsyevr_dd(A, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, overwrite=
             _dense_work.clear()
             _dense_work[key] = Aw
         Aw.copy_(A)
-    c = _ctx(A.device.index)
+    c = _used(_ctx(A.device.index))
     w = torch.empty(max(n, 1), dtype=torch.float64, device=A.device)
     Zs = None
     if jobz == "V":
@@ -328,7 +337,7 @@ def solve_host(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, w=None, Z=
         w = torch.empty(max(n, 1), dtype=dt)
     if jobz == "V" and Z is None:
         Z = torch.empty((max(mcap, 1), max(n, 1)), dtype=dt)
-    c = _ctx()
+    c = _used(_ctx())
     m = ctypes.c_int64(0)
     zb, ze = ctypes.c_int64(0), ctypes.c_int64(0)
     st = Stats()

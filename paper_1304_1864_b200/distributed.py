@@ -162,7 +162,8 @@ def solve_distributed(d, e, jobz="V", range="A", il=1, iu=0, vl=0.0, vu=0.0, gro
     d = d.contiguous()
     e = e.contiguous()
     n = d.numel()
-    c = _dist_context(d.device.index, group, exchange)
+    from . import _used
+    c = _used(_dist_context(d.device.index, group, exchange))
     fn = lib().mr3_dstemr_dd if mode == 0 else lib().mr3_sstemr_d
     w = torch.zeros(max(n, 1), dtype=d.dtype, device=d.device)
     m = ctypes.c_int64(0)
@@ -211,7 +212,8 @@ def _solve_two_phase(d, e, jobz, range, il, iu, vl, vu, group):
     d = d.contiguous()
     e = e.contiguous()
     n = d.numel()
-    c = _ctx(d.device.index)
+    from . import _used
+    c = _used(_ctx(d.device.index))
     m = ctypes.c_int64(0)
     brk = ctypes.c_void_p()
     cap = ctypes.c_int64(0)
