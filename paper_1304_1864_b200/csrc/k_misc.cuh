@@ -134,7 +134,12 @@ __global__ void k_item_keys(Items it, int cnt, const NodeInfo *nodes, unsigned l
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cnt) return;
     const NodeInfo nd = nodes[it.node[t]];
-    R m = half(add(reinterpret_cast<R *>(it.lo)[t], reinterpret_cast<R *>(it.hi)[t]));
+    const R a = reinterpret_cast<R *>(it.lo)[t], b = reinterpret_cast<R *>(it.hi)[t];
+    R m = half(add(a, b));
+    // the bisection's last estimate (RQI start, far inside the bracket's tolerance) orders
+    // eigenvalues of different blocks whose brackets overlap
+    const double x0 = it.x0[t];
+    if (!isnan(x0) && x0 > hi(a) && x0 < hi(b)) m = mk<R>(x0);
     double v = hi(add(m, mk2<R>(nd.sig_hi, nd.sig_lo)));
     unsigned long long u = (unsigned long long)__double_as_longlong(v);
     u = (u & 0x8000000000000000ULL) ? ~u : (u | 0x8000000000000000ULL);
@@ -170,6 +175,62 @@ __global__ void k_compact_cols(Items it, int cnt, const int32_t *sorted_ids, int
     if (t >= cnt) return;
     int id = sorted_ids[t];
     if (it.col[id] >= 0) it.col[id] -= first_rank;
+}
+
+// ---- final order of a split matrix's eigenpairs (execute_impl): the columns were assigned from
+// the plan's bracket order, so eigenvalues of different blocks that agree to within the bisection
+// tolerance can come out of order after the RQI.  A stable sort of w and the same permutation
+// of the Z columns, in place and cycle by cycle, restore "w ascending" (include/mr3.h).
+template <class T>
+__global__ void k_sort_keys(const T *__restrict__ w, int m, unsigned long long *keys,
+                            int32_t *vals, int *ninv) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const double v = (double)w[t];
+    unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    u = (u & 0x8000000000000000ULL) ? ~u : (u | 0x8000000000000000ULL);
+    keys[t] = u;
+    vals[t] = t;
+    if (t + 1 < m && (double)w[t + 1] < v) atomicAdd(ninv, 1);
+}
+template <class T>
+__global__ void k_gather_w(const T *__restrict__ w, const int32_t *__restrict__ perm, int m,
+                           T *out) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) out[t] = w[perm[t]];
+}
+// position t takes the old column perm[t]; t leads its cycle iff it is the cycle's smallest index
+__global__ void k_cycle_leaders(const int32_t *__restrict__ perm, int m, char *leader) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    int j = perm[t];
+    bool lead = j != t;
+    while (lead && j != t) {
+        if (j < t) lead = false;
+        j = perm[j];
+    }
+    leader[t] = lead ? 1 : 0;
+}
+// one CTA column (blockIdx.x) per cycle leader, rows over blockIdx.y and the threads
+template <class T>
+__global__ void k_permute_cols(T *Z, int64_t ldz, int64_t n, const int32_t *__restrict__ perm,
+                               const char *__restrict__ leader) {
+    const int t = blockIdx.x;
+    if (!leader[t]) return;
+    for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.y * blockDim.x) {
+        const T save = Z[(int64_t)t * ldz + i];
+        int j = t;
+        for (;;) {
+            const int src = perm[j];
+            if (src == t) {
+                Z[(int64_t)j * ldz + i] = save;
+                break;
+            }
+            Z[(int64_t)j * ldz + i] = Z[(int64_t)src * ldz + i];
+            j = src;
+        }
+    }
 }
 
 }  // namespace mr3

@@ -1773,6 +1773,43 @@ static int execute_impl(mr3_ctx ctx, char jobz, OutT *w, OutT *Z, int64_t ldz, i
         kt_end(ctx, tf);
         CKL("k_zscale");
     }
+    // split matrices: restore "w ascending" over this rank's columns (k_misc.cuh)
+    if (ctx->split && c1 - c0 > 1) {
+        const int mm = (int)(c1 - c0);
+        OutT *wl = w + c0;
+        unsigned long long *sk = (unsigned long long *)getbuf(ctx, "srt_keys", (size_t)mm * 8, &rc);
+        unsigned long long *sk2 = (unsigned long long *)getbuf(ctx, "srt_keys2", (size_t)mm * 8, &rc);
+        int32_t *sv = (int32_t *)getbuf(ctx, "srt_vals", (size_t)mm * 4, &rc);
+        int32_t *perm = (int32_t *)getbuf(ctx, "srt_perm", (size_t)mm * 4, &rc);
+        int *ninv = (int *)getbuf(ctx, "srt_ninv", 16, &rc);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(ninv, 0, 4, s));
+        k_sort_keys<OutT><<<(mm + 255) / 256, 256, 0, s>>>(wl, mm, sk, sv, ninv);
+        CKL("k_sort_keys");
+        int hinv = 0;
+        CK(cudaMemcpyAsync(&hinv, ninv, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s)); hsync_note(ctx, "sync#15b");
+        if (hinv > 0) {
+            size_t tmpb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmpb, sk, sk2, sv, perm, mm, 0, 64, s);
+            void *tmp = getbuf(ctx, "cubtmp", tmpb, &rc);
+            OutT *wt = (OutT *)getbuf(ctx, "srt_w", (size_t)mm * sizeof(OutT), &rc);
+            char *lead = (char *)getbuf(ctx, "srt_lead", (size_t)mm, &rc);
+            if (rc) return rc;
+            cub::DeviceRadixSort::SortPairs(tmp, tmpb, sk, sk2, sv, perm, mm, 0, 64, s);
+            CKL("radix sort (w)");
+            k_gather_w<OutT><<<(mm + 255) / 256, 256, 0, s>>>(wl, perm, mm, wt);
+            CKL("k_gather_w");
+            CK(cudaMemcpyAsync(wl, wt, (size_t)mm * sizeof(OutT), cudaMemcpyDeviceToDevice, s));
+            if (jobz == 'V' && Z != nullptr) {
+                k_cycle_leaders<<<(mm + 255) / 256, 256, 0, s>>>(perm, mm, lead);
+                CKL("k_cycle_leaders");
+                const int gy = (int)std::min<int64_t>(64, (ctx->n + 255) / 256);
+                k_permute_cols<OutT><<<dim3(mm, gy), 256, 0, s>>>(Z, ldz, ctx->n, perm, lead);
+                CKL("k_permute_cols");
+            }
+        }
+    }
     ctx->stats.d_max = level;
     DevStats hst;
     CK(cudaMemcpyAsync(&hst, W.st, sizeof(hst), cudaMemcpyDeviceToHost, s));

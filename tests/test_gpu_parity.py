@@ -107,6 +107,53 @@ def test_split_matrix():
     assert_parity(check_solution(p, w2, Z2, np.arange(10, 71)))
 
 
+def _interleaved_blocks(io):
+    """Blocks whose spectra interleave far below the bisection tolerance: copies of one block
+    (equal eigenvalues across blocks), copies shifted by a few ulps of ||T||, and a strongly
+    graded tail of tiny blocks -- cut by exact zeros in e."""
+    rng = np.random.default_rng(11)
+    dt = np.float32 if io == "f32" else np.float64
+    ulp = float(np.finfo(dt).eps)
+    d0 = rng.standard_normal(37)
+    e0 = rng.random(36) + 0.1
+    ds, es = [], []
+    for c in range(12):
+        ds.append(d0 + (c % 4) * 3.0 * ulp * (c % 3 - 1))
+        es.append(np.concatenate([e0, [0.0]]))
+    k = np.arange(60)
+    ds.append(10.0 ** (-k / 6.0))
+    es.append(np.where(k % 3 == 2, 0.0, 10.0 ** (-k / 6.0) * 0.2))
+    d = np.concatenate(ds).astype(dt)
+    e = np.concatenate(es)[:-1].astype(dt)
+    return synth.Problem("interleaved-blocks", d, e)
+
+
+@pytest.mark.parametrize("io", ["f64", "f32"])
+def test_split_blocks_interleaved_spectra_sorted(io):
+    """include/mr3.h: w ascending.  Eigenvalues of different blocks that agree to within the
+    bisection tolerance get their columns from the bracket order; the final stable sort of w
+    (k_sort_keys .. k_permute_cols) must put w in order and carry the Z columns along."""
+    p = _interleaved_blocks(io)
+    w, Z, st = run(p)
+    assert st["n_blocks"] > 12
+    assert np.all(np.diff(w) >= 0), int(np.sum(np.diff(w) < 0))
+    assert_parity(check_solution(p, w, Z, np.arange(1, p.n + 1), io=io, oracle_vectors=False,
+                                 gate_angles=False), io=io, gate_angles=False)
+    # every column still belongs to its eigenvalue: residual per column in binary64
+    d64, e64 = p.d.astype(np.float64), p.e.astype(np.float64)
+    Zd, wd = Z.astype(np.float64), w.astype(np.float64)
+    TZ = d64[:, None] * Zd
+    TZ[:-1] += e64[:, None] * Zd[1:]
+    TZ[1:] += e64[:, None] * Zd[:-1]
+    eps = 2.0 ** -53 if io == "f64" else 2.0 ** -24
+    nrm = oracle.norm1(d64, e64)
+    assert np.max(np.linalg.norm(TZ - wd[None, :] * Zd, axis=0)) <= 4 * p.n * eps * nrm
+    # values only: the same eigenvalues, ascending
+    w2, _, _ = run(p, jobz="N")
+    assert np.all(np.diff(w2) >= 0)
+    np.testing.assert_allclose(w2, w, rtol=0, atol=8 * eps * nrm)
+
+
 def test_degenerate_inputs():
     # n = 1
     p = synth.Problem("one", np.array([3.5]), np.zeros(0))
