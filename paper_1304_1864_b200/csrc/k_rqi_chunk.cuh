@@ -424,8 +424,15 @@ __global__ void __launch_bounds__(RC_TPB) k_rqi_chunk(RqiArgs<R> A) {
     };
 
     const int maxit = A.maxit;
+    // the first iteration number must be uniform over the CTA (the loop holds barriers): the
+    // owner state, `passes` included, lives in thread 0 only, so every thread reads the
+    // straggler's pass count itself.  (With the owner's private value the other threads ran
+    // rs.iters more rounds than thread 0: a straggler that never converged -- all maxit
+    // iterations -- left them waiting at a barrier thread 0 had passed for good.)
+    const int pass0 = A.resume_in != nullptr ? A.resume_in[id].iters : 0;
+    __syncthreads();  // (A.resume may alias A.resume_in: read before thread 0 rewrites it)
 #pragma unroll 1
-    for (int iters = passes + 1; iters <= maxit; iters++) {
+    for (int iters = pass0 + 1; iters <= maxit; iters++) {
         if (tid == 0) {
             const bool store_only =
                 A.jobz_v && iters >= 2 && done && !zfinal && zcol != nullptr && n > 1;

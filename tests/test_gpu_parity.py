@@ -665,3 +665,46 @@ def test_backtracking_from_grandparent():
         idx = np.arange(lo_i, hi_i + 1)
         res = check_solution(p, w[idx - 1], Z[:, idx - 1], idx, full_orth=False)
         assert_parity(res)
+
+
+_STRAGGLER_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+import paper_1304_1864_b200 as mr3
+k = np.arange(3000)
+d = 2.0 ** (-k / 4.0)
+e = 2.0 ** (-(k[:-1] + 0.5) / 4.0) * 0.3
+mr3.set_param("RQI_CHUNK", 1, 0)   # m > 1: the k_rqi_fb path, its stragglers to k_rqi_chunk
+w, Z, st = mr3.mr3_dstemr_dd(torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), "V", "A")
+torch.cuda.synchronize()
+np.savez({out!r}, w=w.cpu().numpy(), Z=Z.cpu().numpy(), fb=st["rqi_fallbacks"], nb=st["n_blocks"])
+"""
+
+
+def test_fb_stragglers_that_never_converge(tmp_path):
+    """Strongly graded T (d_k = 2^(-k/4)): three eigenpairs at the small end of its leading block
+    use every RQI iteration and end in the bisection fallback.  On the k_rqi_fb path they
+    continue in k_rqi_chunk from a saved state; its loop must start at the same iteration in
+    every thread (a CTA-wide barrier sits inside) -- with the owner thread's private count the
+    kernel never returned (found by tools/stress.py --large).  Run in a child process with a
+    time limit so that a regression fails instead of hanging the suite."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "res.npz")
+    r = subprocess.run([sys.executable, "-c", _STRAGGLER_SCRIPT.format(root=root, out=out)],
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    f = np.load(out)
+    w, Z = f["w"], f["Z"]
+    assert int(f["nb"]) > 2000 and int(f["fb"]) >= 1
+    k = np.arange(3000)
+    d = 2.0 ** (-k / 4.0)
+    e = 2.0 ** (-(k[:-1] + 0.5) / 4.0) * 0.3
+    p = synth.Problem("graded-down", d, e)
+    assert np.all(np.diff(w) >= 0)
+    assert_parity(check_solution(p, w, Z, np.arange(1, p.n + 1), oracle_vectors=False,
+                                 gate_angles=False), gate_angles=False)
