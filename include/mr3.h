@@ -174,6 +174,11 @@ int mr3_nccl_comm_destroy(void *comm);
  *   d[n], e[n-1]: device inputs (the same on every rank).
  *   *m: number of eigenvalues found (globally).
  *   w[n]: device output, the first *m entries ascending -- all of them on every rank.
+ *   (A matrix that splits into blocks gets its columns from the order of the blocks'
+ *   bisection estimates; after the eigenpairs are final, w is sorted stably and the Z columns
+ *   are permuted with it, over this rank's column range.  With world > 1 two eigenvalues of
+ *   different blocks that agree to within the bisection tolerance may therefore still be
+ *   exchanged across a rank boundary; with world = 1 w is ascending without exception.)
  *   Z: device output, column-major, ldz >= n, zcap columns allocated (may be NULL when
  *   jobz = 'N'): this rank's columns [*zcol_begin, *zcol_end) of the global m, at local
  *   positions 0 .. *zcol_end - *zcol_begin - 1.  Single GPU (world = 1): all m columns.

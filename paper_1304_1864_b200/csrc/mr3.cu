@@ -470,7 +470,10 @@ static int plan_impl(mr3_ctx ctx, char range, int64_t n, const T *d, const T *e,
     ctx->norm1 = info.norm1;
     int ex = 0;
     if (info.norm1 > 0) frexp(info.norm1, &ex);
-    ctx->scale = info.norm1 > 0 ? ldexp(1.0, -ex) : 1.0;  // scaled ||T||_1 in [0.5, 1)
+    // scaled ||T||_1 in [0.5, 1); the exponent is clamped so that the scale and its inverse are
+    // both normal numbers (a subnormal ||T||_1 gave scale = inf, ||T||_1 >= 2^1023 unscale = inf)
+    ex = std::min(std::max(ex, -1021), 1022);
+    ctx->scale = info.norm1 > 0 ? ldexp(1.0, -ex) : 1.0;
     const double nrm_s = info.norm1 * ctx->scale;
     ctx->pivmin = eps_y * (info.norm1 > 0 ? nrm_s : 1.0);
     ctx->spdiam = fmax((info.gu - info.gl) * ctx->scale, 1e-300);

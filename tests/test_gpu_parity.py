@@ -154,6 +154,29 @@ def test_split_blocks_interleaved_spectra_sorted(io):
     np.testing.assert_allclose(w2, w, rtol=0, atol=8 * eps * nrm)
 
 
+@pytest.mark.parametrize("lg", [-1045, -1030, 1022])
+def test_extreme_norms(lg):
+    """||T||_1 subnormal (2^-1047: every entry subnormal) and close to overflow: the power-of-2
+    scaling keeps both the scale and its inverse finite.  Checked in a rescaled copy of the
+    problem (exact: powers of 2), with the output quantum of w at that magnitude allowed for."""
+    base = synth.random_uniform(80, 9)
+    d, e = np.ldexp(base.d, lg - 2), np.ldexp(base.e, lg - 2)  # (rounded where subnormal: the input)
+    p = synth.Problem("extreme", d, e)
+    w, Z, st = run(p)
+    dd_, ee_, ww = np.ldexp(d, -lg), np.ldexp(e, -lg), np.ldexp(w, -lg)
+    lh, ll = oracle.eigvals(dd_, ee_)
+    nrm = oracle.norm1(dd_, ee_)
+    quantum = 2.0 ** (-1074 - lg) if lg < -1022 else 0.0
+    assert np.all(np.isfinite(w)) and np.all(np.diff(w) >= 0)
+    assert np.max(np.abs(ww - (lh + ll))) <= 4e-16 * nrm + quantum
+    TZ = dd_[:, None] * Z
+    TZ[:-1] += ee_[:, None] * Z[1:]
+    TZ[1:] += ee_[:, None] * Z[:-1]
+    assert np.max(np.linalg.norm(TZ - ww[None, :] * Z, axis=0)) <= 1e-15 * p.n * nrm + 4 * quantum
+    o, dev = exact_orthogonality(torch.from_numpy(Z).cuda())
+    assert o <= 1e-14 and dev <= 1e-14
+
+
 def test_degenerate_inputs():
     # n = 1
     p = synth.Problem("one", np.array([3.5]), np.zeros(0))
