@@ -204,4 +204,35 @@ __global__ void k_larft(const double *__restrict__ G, int kb, const double *__re
     }
 }
 
+// max |A_ij| over the n x n matrix (bits of a non-negative double order as integers); NaN/inf
+// entries set the maximum to inf (the tridiagonal solver reports them)
+__global__ void k_dense_absmax(const double *__restrict__ A, int64_t lda, int n,
+                               unsigned long long *out) {
+    unsigned long long m = 0;
+    const int64_t tot = (int64_t)n * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const double v = fabs(A[(t / n) * lda + (t % n)]);
+        const unsigned long long u =
+            (v == v) ? (unsigned long long)__double_as_longlong(v) : 0x7ff0000000000000ULL;
+        m = u > m ? u : m;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+        m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+// A <- sc A (sc a power of 2: exact unless an entry becomes subnormal) / w <- sc w
+__global__ void k_dense_scale(double *A, int64_t lda, int n, double sc) {
+    const int64_t tot = (int64_t)n * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x)
+        A[(t / n) * lda + (t % n)] *= sc;
+}
+__global__ void k_vec_scale(double *w, int64_t m, double sc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) w[t] *= sc;
+}
+
 }  // namespace mr3

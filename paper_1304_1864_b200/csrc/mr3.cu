@@ -2051,6 +2051,35 @@ int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int6
     double *wv = (double *)getbuf(ctx, "dn_w", (size_t)n * 8, &rc);
     double *yv = (double *)getbuf(ctx, "dn_y", (size_t)n * 8, &rc);
     if (rc) return rc;
+    // max |a_ij| far from 1: scale A by a power of 2 first (the reflector norms square the
+    // entries: 1e-200 underflows, 1e200 overflows), w back at the end (as LAPACK's dsyevr scales
+    // outside [sqrt(smallest), sqrt(largest)]); nothing is touched in between, so the usual
+    // inputs keep their bits
+    double dn_unscale = 1.0;
+    {
+        unsigned long long *amx = (unsigned long long *)getbuf(ctx, "dn_amax", 16, &rc);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(amx, 0, 8, s));
+        k_dense_absmax<<<ctx->nsm * 4, 256, 0, s>>>(A, lda, nn, amx);
+        CKL("k_dense_absmax");
+        unsigned long long hb = 0;
+        CK(cudaMemcpyAsync(&hb, amx, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double amax;
+        memcpy(&amax, &hb, 8);
+        if (amax > 0.0 && amax < INFINITY && (amax < ldexp(1.0, -400) || amax > ldexp(1.0, 400))) {
+            int ex = 0;
+            frexp(amax, &ex);
+            // two exact steps where one power of 2 would leave the double range
+            const int e1 = -ex / 2, e2 = -ex - e1;
+            k_dense_scale<<<ctx->nsm * 4, 256, 0, s>>>(A, lda, nn, ldexp(1.0, e1));
+            k_dense_scale<<<ctx->nsm * 4, 256, 0, s>>>(A, lda, nn, ldexp(1.0, e2));
+            CKL("k_dense_scale");
+            vl = ldexp(ldexp(vl, e1), e2);
+            vu = ldexp(ldexp(vu, e1), e2);
+            dn_unscale = (double)ex;  // w <- w 2^ex (applied in two steps below)
+        }
+    }
     cudaEvent_t ev[2];
     CK(cudaEventCreate(&ev[0]));
     CK(cudaEventCreate(&ev[1]));
@@ -2106,6 +2135,12 @@ int mr3_dsyevr_dd(mr3_ctx ctx, char jobz, char range, int64_t n, double *A, int6
     rc = mr3_dstemr_dd(ctx, jobz, range, n, dd_, de_, vl, vu, il, iu, m, w, Z, ldz,
                        jobz == 'V' ? n : 0, &zb, &ze, stats);
     if (rc) return rc;
+    if (dn_unscale != 1.0 && *m > 0) {
+        const int ex = (int)dn_unscale, e1 = ex / 2, e2 = ex - e1;
+        k_vec_scale<<<(int)((*m + 255) / 256), 256, 0, s>>>(w, *m, ldexp(1.0, e1));
+        k_vec_scale<<<(int)((*m + 255) / 256), 256, 0, s>>>(w, *m, ldexp(1.0, e2));
+        CKL("k_vec_scale");
+    }
     ctx->launches += launches;
     float ms_red = 0.f;
     CK(cudaEventSynchronize(ev[1]));

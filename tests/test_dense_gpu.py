@@ -110,3 +110,23 @@ def test_dense_reduced_t_needs_no_rqi_fallback():
     w, Z, st = run(p.A)
     assert st["rqi_fallbacks"] == 0, st["rqi_fallbacks"]
     _check(p.A, w, Z, oracle_vectors=False)
+
+
+@pytest.mark.parametrize("lg", [-660, 660])
+def test_dense_extreme_scaling(lg):
+    """Entries near 2^-660 / 2^660: the reflector norms square them (underflow / overflow) unless
+    A is scaled by a power of 2 first (mr3_dsyevr_dd: k_dense_absmax, k_dense_scale; w scaled
+    back).  Compared with the same problem at its natural scale: eigenvalues equal up to the
+    exact factor, eigenvectors the same bits (found by tools/stress_dense.py)."""
+    p = synth.dense_from(synth.random_uniform(150, 8), 8)
+    w0, Z0, _ = run(p.A.copy())
+    A = np.ldexp(p.A, lg)
+    w, Z, st = run(A.copy())
+    _check(p.A, np.ldexp(w, -lg), Z, oracle_vectors=False)
+    # index subset and a value range given at the scaled magnitude
+    w2, Z2, _ = run(A.copy(), range="I", il=10, iu=40)
+    np.testing.assert_allclose(np.ldexp(w2, -lg), w0[9:40], rtol=0,
+                               atol=8 * 150 * EPS * dense.dense_norm1(p.A))
+    vl, vu = 0.5 * (w0[19] + w0[20]), 0.5 * (w0[59] + w0[60])
+    w3, Z3, _ = run(A.copy(), range="V", vl=float(np.ldexp(vl, lg)), vu=float(np.ldexp(vu, lg)))
+    assert w3.shape[0] == 40 and Z3.shape == (150, 40)
